@@ -1,0 +1,170 @@
+/*
+ * gnb.h -- C ABI of libgnb.so, the sm_100a group-wise Naive Bayes hot path.
+ *
+ * The reference (arxiv 1905.13746, /root/reference/pkg/src/groupnb) is pure
+ * Python; its hot loops are the per-sample scoring loop and the per-group
+ * training count loops.  Every entry point below replaces one of them and is
+ * what a ctypes binding inside the reference would call (INTEGRATION.md shows
+ * that binding).  Plain pointers and sizes only; no torch types.
+ *
+ * Dense conventions
+ *   - class index 0 = benign, 1 = malware (2.. = extra malware families);
+ *     argmax ties resolve to the LOWEST index, which is the reference's
+ *     "malware iff strictly higher" (classifier.py:154-157).
+ *   - X is int32, row-major, row stride `ldx` elements (ldx >= n_cols); counts
+ *     must be >= 0 (OpcodeHistogram invariant, corpus.py:48-49).
+ *   - size_bytes -> group = size / group_size_bytes on [0, max_size_bytes)
+ *     (corpus.py:222-232); route[group] -> model slot (engine.py:56-59, 87-91).
+ *   - predict rows hold the counts of the routed model's features in
+ *     FeatureSet order (classifier.py:143 `_packed` order), zero padded.
+ *
+ * Device entry points (`gnb_predict`, `gnb_fit_stats`, `gnb_pack_tables`,
+ * `gnb_generate`) take caller-owned DEVICE pointers and enqueue on the
+ * caller's stream (`stream` = cudaStream_t cast to uintptr_t, 0 = legacy
+ * default); they never synchronise and never allocate.  `*_host` entry points
+ * take HOST pointers and run synchronously on `device` (they stage through
+ * internal device buffers and pinned memory).  All functions are reentrant;
+ * errors return a nonzero code and leave a message in gnb_last_error()
+ * (thread-local).
+ */
+#ifndef GNB_H_
+#define GNB_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  GNB_OK = 0,
+  GNB_EINVAL = 1,       /* invalid argument            -> InvalidConfigError / ValueError */
+  GNB_ECUDA = 2,        /* CUDA runtime/driver failure -> RuntimeError                   */
+  GNB_EUNSUPPORTED = 3, /* shape this build does not handle                               */
+  GNB_ENOMEM = 4
+};
+
+/* per-row status written into label_out instead of a class index */
+#define GNB_ROW_OUT_OF_RANGE (-1)   /* size outside [0, max): engine.py:201-205 */
+#define GNB_ROW_NEGATIVE_COUNT (-2) /* a count < 0 in the row (invalid input)   */
+
+#define GNB_MAX_CLASSES 16
+
+int gnb_abi_version(void);
+const char* gnb_strerror(int code);
+const char* gnb_last_error(void);
+
+/* ------------------------------------------------------------------ predict
+ * Replaces: classifier.log_posterior + classifier.predict
+ *           (pkg/src/groupnb/classifier.py:132-158) inside
+ *           engine._classify_slice (pkg/src/groupnb/engine.py:187-206), i.e.
+ *           the body of classify_sequential / classify_parallel
+ *           (engine.py:209-296).
+ *
+ * Packed tables: gnb_pack_tables turns log_prior[S][C] and log_lik[S][C][F]
+ * (device, fp64) into the kernel layout in `packed`
+ * (gnb_packed_table_bytes(S, C, F) bytes, 16-B aligned, caller-owned).
+ * Scores are bit-identical to the reference: per class
+ * acc = prior; acc = acc + x*ll (mul, then add) for every feature in order.
+ * label_out[n] = argmax class, or GNB_ROW_*; logpost_out (nullable) [n][C].
+ */
+size_t gnb_packed_table_bytes(int32_t n_slots, int32_t n_classes, int32_t n_features);
+
+int gnb_pack_tables(const double* log_prior, const double* log_lik, int32_t n_slots,
+                    int32_t n_classes, int32_t n_features, void* packed, uintptr_t stream);
+
+int gnb_predict(const int32_t* x, int64_t n_rows, int32_t n_features, int64_t ldx,
+                const int32_t* size_bytes, int32_t group_size_bytes, int32_t max_size_bytes,
+                const int32_t* route, int32_t n_slots, int32_t n_classes, const void* packed,
+                int32_t* label_out, double* logpost_out, uintptr_t stream);
+
+/* Same as gnb_predict but always uses the L1 (non-TMA) kernel; parity tests. */
+int gnb_predict_generic(const int32_t* x, int64_t n_rows, int32_t n_features, int64_t ldx,
+                        const int32_t* size_bytes, int32_t group_size_bytes,
+                        int32_t max_size_bytes, const int32_t* route, int32_t n_slots,
+                        int32_t n_classes, const void* packed, int32_t* label_out,
+                        double* logpost_out, uintptr_t stream);
+
+/* Host-buffer form of the above (the ctypes drop-in for _classify_slice):
+ * x/size/route/log_prior/log_lik/label_out/logpost_out are HOST arrays
+ * (pinned memory is used zero-copy-fast; pageable works).  Rows are streamed
+ * through the device in chunks with copies overlapped with the kernel.
+ * Synchronous.  elapsed_ns (nullable) receives the wall time of the call. */
+int gnb_predict_host(const int32_t* x, int64_t n_rows, int32_t n_features, int64_t ldx,
+                     const int32_t* size_bytes, int32_t group_size_bytes,
+                     int32_t max_size_bytes, const int32_t* route, int32_t n_slots,
+                     int32_t n_classes, const double* log_prior, const double* log_lik,
+                     int32_t* label_out, double* logpost_out, int32_t device,
+                     int64_t* elapsed_ns);
+
+/* ------------------------------------------------------------------ fit
+ * Replaces: the sample x histogram count loops of features.class_frequency
+ *           (pkg/src/groupnb/features.py:48-53) and classifier.train_group
+ *           (pkg/src/groupnb/classifier.py:94-101), and the class counts of
+ *           corpus.trainable_groups (pkg/src/groupnb/corpus.py:302-305).
+ *
+ * Over the full vocabulary: sums[G][C][V] = sum x, sumsq[G][C][V] = sum x^2,
+ * counts[G][C] = rows, with G = max_size_bytes / group_size_bytes.  Rows with
+ * size outside [0, max) are skipped (partition_by_group, corpus.py:247-251)
+ * and counted in status[1]; rows whose label is outside [0, C) are skipped
+ * and counted in status[0] (train_group raises IntegrityError for them,
+ * classifier.py:95-96).  All values are integers accumulated exactly; the
+ * fp64 outputs are exact while every total is < 2^53, so results do not
+ * depend on the launch geometry or on the number of GPUs the rows are
+ * sharded over.  accumulate=0 zeroes sums/sumsq/counts/status first.
+ * sumsq may be NULL. */
+int gnb_fit_stats(const int32_t* x, int64_t n_rows, int32_t n_cols, int64_t ldx,
+                  const int32_t* size_bytes, const int32_t* labels, int32_t group_size_bytes,
+                  int32_t max_size_bytes, int32_t n_classes, double* sums, double* sumsq,
+                  double* counts, unsigned long long* status, int32_t accumulate,
+                  uintptr_t stream);
+
+int gnb_fit_stats_host(const int32_t* x, int64_t n_rows, int32_t n_cols, int64_t ldx,
+                       const int32_t* size_bytes, const int32_t* labels,
+                       int32_t group_size_bytes, int32_t max_size_bytes, int32_t n_classes,
+                       double* sums, double* sumsq, double* counts,
+                       unsigned long long* status, int32_t device);
+
+/* ------------------------------------------------------------------ finalize (host)
+ * Replaces: features.score_opcodes + select_top_k (features.py:59-86) and the
+ *           prior / log-likelihood step of classifier.train_group
+ *           (classifier.py:103-120), per trainable group, as train_bundle
+ *           does (engine.py:166-173).  Two classes (0 benign, 1 malware).
+ * Inputs are the host copies of gnb_fit_stats' sums/counts.  Vocabulary
+ * columns must be in mnemonic order (ties break by column index).
+ * group_state[g]: 1 trained; 0 not trainable (< min_per_class of a class);
+ *                 -1 no malware opcode occurrences; -2 no benign occurrences
+ *                 (both InsufficientClassError in the reference).
+ * n_features[g] <= k; features[g][k] column indices in FeatureSet order;
+ * log_prior[g][2]; log_lik[g][2][k] (unused tail zero).  libm log. */
+int gnb_fin_train(const double* sums, const double* counts, int32_t n_groups, int32_t n_cols,
+                  int32_t k, double alpha, int32_t min_per_class, int32_t* group_state,
+                  int32_t* n_features, int32_t* features, double* log_prior,
+                  double* log_lik);
+
+/* train_group for ONE group with a given feature list and C classes
+ * (classifier.py:103-120 with a class axis; C = 2 reproduces the reference):
+ * sums_g[C][V], counts_g[C] -> log_prior[C], log_lik[C][F].  Host, libm log. */
+int gnb_fin_tables(const double* sums_g, const double* counts_g, int32_t n_classes,
+                   int32_t n_cols, const int32_t* features, int32_t n_features, double alpha,
+                   double* log_prior, double* log_lik);
+
+/* ------------------------------------------------------------------ synthetic data
+ * Device generator following the reference's synthetic law
+ * (pkg/src/groupnb/synth.py:64-116): per row a group (rows laid out group by
+ * group, group g owning rows [group_row_end[g-1], group_row_end[g]) of the
+ * GLOBAL index space), a class (row % C), a size uniform in the group's byte
+ * range, T = 64 + size/64 draws, and per-column counts ~ Poisson(T * p_c[v])
+ * with p_c from class_distributions (weight 1 on the class's block, 1-d
+ * elsewhere).  Counter-based: row r's values depend only on (seed, r), so any
+ * sharding of the global index space yields the same data. n_groups <= 128. */
+int gnb_generate(int32_t* x, int64_t n_rows, int32_t n_cols, int64_t ldx, int32_t* size_bytes,
+                 int32_t* labels, int64_t row_offset, const int64_t* group_row_end,
+                 int32_t n_groups, int32_t group_size_bytes, int32_t n_classes,
+                 double divergence, uint64_t seed, uintptr_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GNB_H_ */

@@ -1,0 +1,123 @@
+/*
+ * gnb_oracle.c -- C restatement of the reference hot path.
+ * TEST / CPU-BASELINE INFRASTRUCTURE ONLY: loaded by tests/, smoke() and
+ * bench.py's cpu_baseline / --impl reference legs.  The product
+ * (paper_1905_13746_b200, libgnb.so) never links or calls it.
+ *
+ * Parity is pinned: tests/test_oracle_c.py checks it bit-for-bit against
+ * oracle/oracle.py, which is checked against golden vectors produced by the
+ * reference itself (tests/golden/make_golden.py).
+ *
+ * Built with -ffp-contract=off: `acc = acc + x * ll` is a multiply then an
+ * add, exactly the reference's `score_m += n * ll_m`
+ * (pkg/src/groupnb/classifier.py:143-147).
+ */
+#include <pthread.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+typedef struct {
+  const int32_t* x;
+  int64_t lo, hi, ldx;
+  int32_t F, C, width, limit;
+  const int32_t* size;
+  const int32_t* route;
+  const double* prior; /* [S][C] */
+  const double* ll;    /* [S][C][F] */
+  int32_t* label;
+  double* logpost;     /* nullable [N][C] */
+} pred_job;
+
+/* log_posterior + predict + _classify_slice (classifier.py:132-158,
+ * engine.py:187-206) for rows [lo, hi). */
+static void* predict_rows(void* arg) {
+  const pred_job* j = (const pred_job*)arg;
+  double acc[16];
+  for (int64_t r = j->lo; r < j->hi; ++r) {
+    const int32_t sz = j->size[r];
+    if (sz < 0 || sz >= j->limit) {
+      j->label[r] = -1;
+      if (j->logpost)
+        for (int c = 0; c < j->C; ++c) j->logpost[r * j->C + c] = __builtin_nan("");
+      continue;
+    }
+    const int s = j->route[sz / j->width];
+    const int32_t* row = j->x + r * j->ldx;
+    for (int c = 0; c < j->C; ++c) {
+      const double* ll = j->ll + ((int64_t)s * j->C + c) * j->F;
+      double a = j->prior[s * j->C + c];
+      for (int f = 0; f < j->F; ++f) a = a + (double)row[f] * ll[f];
+      acc[c] = a;
+    }
+    int best = 0;
+    for (int c = 1; c < j->C; ++c)
+      if (acc[c] > acc[best]) best = c; /* strict: ties -> lowest index (benign) */
+    j->label[r] = best;
+    if (j->logpost)
+      for (int c = 0; c < j->C; ++c) j->logpost[r * j->C + c] = acc[c];
+  }
+  return NULL;
+}
+
+int oracle_predict(const int32_t* x, int64_t n, int32_t F, int64_t ldx, const int32_t* size,
+                   int32_t width, int32_t limit, const int32_t* route, int32_t C,
+                   const double* prior, const double* ll, int32_t* label, double* logpost,
+                   int32_t threads) {
+  if (C < 2 || C > 16 || threads < 1) return 1;
+  if (threads > 256) threads = 256;
+  pthread_t tid[256];
+  pred_job jobs[256];
+  const int64_t per = (n + threads - 1) / threads;
+  int started = 0;
+  for (int t = 0; t < threads; ++t) {
+    pred_job j = {x, t * per, (t + 1) * per < n ? (t + 1) * per : n, ldx, F, C, width, limit,
+                  size, route, prior, ll, label, logpost};
+    jobs[t] = j;
+    if (jobs[t].lo >= jobs[t].hi) continue;
+    if (threads == 1) {
+      predict_rows(&jobs[t]);
+    } else if (pthread_create(&tid[t], NULL, predict_rows, &jobs[t]) == 0) {
+      ++started;
+    } else {
+      predict_rows(&jobs[t]);
+      jobs[t].lo = jobs[t].hi; /* done inline */
+    }
+  }
+  for (int t = 0; t < threads && threads > 1; ++t)
+    if (jobs[t].lo < jobs[t].hi) pthread_join(tid[t], NULL);
+  (void)started;
+  return 0;
+}
+
+/* Segmented sums (features.py:48-53, classifier.py:94-101, corpus.py:302-305)
+ * plus sums of squares; exact 64-bit integers. */
+int oracle_fit_stats(const int32_t* x, int64_t n, int32_t V, int64_t ldx, const int32_t* size,
+                     const int32_t* label, int32_t width, int32_t limit, int32_t C,
+                     int64_t* S, int64_t* Q, int64_t* cnt, int64_t* status) {
+  const int64_t G = limit / width;
+  memset(S, 0, sizeof(int64_t) * G * C * V);
+  if (Q) memset(Q, 0, sizeof(int64_t) * G * C * V);
+  memset(cnt, 0, sizeof(int64_t) * G * C);
+  status[0] = status[1] = 0;
+  for (int64_t r = 0; r < n; ++r) {
+    if (size[r] < 0 || size[r] >= limit) {
+      ++status[1];
+      continue;
+    }
+    if (label[r] < 0 || label[r] >= C) {
+      ++status[0];
+      continue;
+    }
+    const int64_t key = (int64_t)(size[r] / width) * C + label[r];
+    ++cnt[key];
+    const int32_t* row = x + r * ldx;
+    int64_t* s = S + key * V;
+    int64_t* q = Q ? Q + key * V : NULL;
+    for (int v = 0; v < V; ++v) {
+      s[v] += row[v];
+      if (q) q[v] += (int64_t)row[v] * row[v];
+    }
+  }
+  return 0;
+}

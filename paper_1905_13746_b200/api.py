@@ -1,0 +1,309 @@
+"""The reference's fit / classify operation contract, executed on the GPU.
+
+Drop-in for the hot path of `groupnb` (reference pkg/src/groupnb):
+
+  train_bundle(train, k, alpha=1.0, *, seed=0, created_at=None)  engine.py:157-177
+  train_group(samples, features, alpha=1.0, *, group=0)           classifier.py:68-129
+  classify_parallel / classify_sequential(bundle, workload, *, warmup=True)
+                                                                  engine.py:209-296
+  log_posterior(model, histogram) / predict(model, histogram)     classifier.py:132-158
+
+Same arguments, same results (bit-identical log-scores and bundles), same
+exception types and messages.  The object model is densified here on the
+host and handed to libgnb.so's host-buffer entry points (gnb_fit_stats_host,
+gnb_fin_train, gnb_predict_host), which run the sm_100a kernels.  Per SPEC.md
+("a GPU backend is an optional extension point behind the same operation
+contract"), `lanes` is validated but the device decides the parallelism.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from datetime import datetime, timezone
+from typing import Sequence
+
+import numpy as np
+
+from . import _native as N
+from .errors import (EmptyBundleError, InsufficientClassError, IntegrityError,
+                     InvalidConfigError, MeasurementError)
+from .model import (CLASS_INDEX, CLASSES, INDEX_CLASS, BundleMeta, FeatureSet, GroupedCorpus,
+                    GroupingConfig, GroupModel, Label, ModelBundle, OpcodeHistogram, Prediction,
+                    SampleRecord, TimedRun, Workload, build_bundle, oversize_message)
+
+_I32_MAX = 2**31 - 1
+
+
+def _ptr(a: np.ndarray) -> int:
+    return a.ctypes.data
+
+
+def _device_ordinal(device) -> int:
+    if device is None:
+        return 0
+    if isinstance(device, int):
+        return device
+    idx = getattr(device, "index", None)
+    return 0 if idx is None else int(idx)
+
+
+def _label_codes(samples: Sequence[SampleRecord]) -> np.ndarray:
+    return np.fromiter((CLASS_INDEX.get(s.label, -1) for s in samples), dtype=np.int32,
+                       count=len(samples))
+
+
+def _densify(samples: Sequence[SampleRecord], columns: dict[str, int], width: int) -> np.ndarray:
+    """[N, width] int32 counts of the opcodes in `columns` (others ignored)."""
+    x = np.zeros((len(samples), width), dtype=np.int32)
+    rows, cols, vals = [], [], []
+    for i, s in enumerate(samples):
+        for op, n in s.histogram.entries.items():
+            j = columns.get(op)
+            if j is not None:
+                rows.append(i)
+                cols.append(j)
+                vals.append(n)
+    if vals:
+        v = np.asarray(vals, dtype=np.int64)
+        if int(v.max()) > _I32_MAX:
+            raise InvalidConfigError("opcode counts must be < 2^31 for the GPU path")
+        x[np.asarray(rows), np.asarray(cols)] = v
+    return x
+
+
+def _sizes(samples: Sequence[SampleRecord], limit: int) -> np.ndarray:
+    """int32 sizes; anything outside [0, limit) becomes -1 (still an error row)."""
+    return np.fromiter((s.size_bytes if 0 <= s.size_bytes < limit else -1 for s in samples),
+                       dtype=np.int32, count=len(samples))
+
+
+def _fit_stats_host(x: np.ndarray, size: np.ndarray, label: np.ndarray, *, n_classes: int,
+                    width: int, limit: int, device: int):
+    G = limit // width
+    V = x.shape[1]
+    S = np.zeros((G, n_classes, V))
+    n = np.zeros((G, n_classes))
+    status = np.zeros(2, dtype=np.uint64)
+    N.check(N.lib.gnb_fit_stats_host(_ptr(x), x.shape[0], V, V, _ptr(size), _ptr(label), width,
+                                     limit, n_classes, _ptr(S), None, _ptr(n), _ptr(status),
+                                     device), "gnb_fit_stats_host")
+    return S, n, status
+
+
+# ---------------------------------------------------------------- fit
+def train_group(samples: Sequence[SampleRecord], features: FeatureSet, alpha: float = 1.0, *,
+                group: int = 0, device=None) -> GroupModel:
+    """One group's model on its samples (classifier.py:68-129), counted on the GPU."""
+    if isinstance(alpha, bool) or not isinstance(alpha, (int, float)) or alpha <= 0:
+        raise InvalidConfigError(f"alpha must be positive, got {alpha!r}")
+    if not features.opcodes:
+        raise InvalidConfigError("feature set is empty")
+    for s in samples:
+        if s.label not in CLASS_INDEX:
+            raise IntegrityError(f"sample {s.id!r} has no training label")
+    ops = features.opcodes
+    cols = {op: j for j, op in enumerate(dict.fromkeys(ops))}
+    x = _densify(samples, cols, max(len(cols), 1))
+    zeros = np.zeros(len(samples), dtype=np.int32)
+    S, n, _ = _fit_stats_host(x, zeros, _label_codes(samples), n_classes=2, width=1, limit=1,
+                              device=_device_ordinal(device))
+    for c in CLASSES:
+        if n[0, CLASS_INDEX[c]] == 0:
+            raise InsufficientClassError(f"group {group}: no {c.value} samples to train on")
+    from .dense import fin_tables
+    feat_cols = np.array([cols[op] for op in ops], dtype=np.int32)
+    prior, ll = fin_tables(S[0], n[0], feat_cols, float(alpha))
+    return _model(group, features, prior, ll, n[0], float(alpha))
+
+
+def _model(group, features: FeatureSet, prior, ll, counts, alpha) -> GroupModel:
+    ops = features.opcodes
+    return GroupModel(
+        group=group, features=features,
+        log_prior={c: float(prior[CLASS_INDEX[c]]) for c in CLASSES},
+        log_likelihood={c: {op: float(ll[CLASS_INDEX[c], j]) for j, op in enumerate(ops)}
+                        for c in CLASSES},
+        alpha=alpha,
+        train_counts={c: int(counts[CLASS_INDEX[c]]) for c in CLASSES})
+
+
+def train_bundle(train: GroupedCorpus, k: int, alpha: float = 1.0, *, seed: int = 0,
+                 created_at: str | None = None, device=None) -> ModelBundle:
+    """Select features and train every trainable group (engine.py:157-177).
+
+    One K-FIT pass over the whole corpus (every group, full vocabulary), then
+    the host finalize (scores, top-k, libm logs) per group."""
+    config = train.config
+    samples = train.all_samples()
+    vocab = sorted({op for s in samples for op in s.histogram.entries})
+    k_ok = isinstance(k, int) and not isinstance(k, bool) and k >= 1
+    a_ok = isinstance(alpha, (int, float)) and not isinstance(alpha, bool) and alpha > 0
+    models = []
+    if samples and vocab:
+        x = _densify(samples, {op: j for j, op in enumerate(vocab)}, len(vocab))
+        S, n, _ = _fit_stats_host(x, _sizes(samples, config.max_size_bytes),
+                                  _label_codes(samples), n_classes=2,
+                                  width=config.group_size_bytes, limit=config.max_size_bytes,
+                                  device=_device_ordinal(device))
+        from .dense import fin_train
+        fin = fin_train(S, n, k=k if k_ok else 1, alpha=float(alpha) if a_ok else 1.0,
+                        min_per_class=config.min_per_class)
+        for g in np.nonzero(fin.state != 0)[0].tolist():
+            if fin.state[g] == -1:
+                raise InsufficientClassError(f"group {g}: no malware opcode occurrences to score")
+            if fin.state[g] == -2:
+                raise InsufficientClassError(f"group {g}: no benign opcode occurrences to score")
+            if not k_ok:
+                raise InvalidConfigError(f"k must be a positive integer, got {k!r}")
+            if not a_ok:
+                raise InvalidConfigError(f"alpha must be positive, got {alpha!r}")
+            for s in train.groups.get(g, ()):
+                if s.label not in CLASS_INDEX:
+                    raise IntegrityError(f"sample {s.id!r} has no training label")
+            F = int(fin.n_features[g])
+            feats = FeatureSet(tuple(vocab[j] for j in fin.features[g, :F]), k)
+            models.append(_model(g, feats, fin.log_prior[g], fin.log_lik[g, :, :F],
+                                 n[g], float(alpha)))
+    if created_at is None:
+        created_at = datetime.now(timezone.utc).isoformat(timespec="seconds")
+    meta = BundleMeta(k=k, alpha=float(alpha), seed=seed, created_at=created_at)
+    return build_bundle(models, config, meta)
+
+
+# ---------------------------------------------------------------- predict
+class _PackedBundle:
+    """Dense tables of a bundle: slot order = trained_ids order."""
+
+    def __init__(self, bundle: ModelBundle):
+        ids = bundle.trained_ids
+        slot = {g: i for i, g in enumerate(ids)}
+        self.ids = ids
+        self.route = np.array([slot[g] for g in bundle._route_table], dtype=np.int32)
+        self.F = max(len(bundle.models[g].features.opcodes) for g in ids)
+        S = len(ids)
+        self.prior = np.zeros((S, 2))
+        self.lik = np.zeros((S, 2, self.F))
+        self.columns = []
+        for i, g in enumerate(ids):
+            m = bundle.models[g]
+            for c in CLASSES:
+                ci = CLASS_INDEX[c]
+                self.prior[i, ci] = m.log_prior[c]
+                self.lik[i, ci, :len(m.features.opcodes)] = [
+                    m.log_likelihood[c][op] for op in m.features.opcodes]
+            self.columns.append({op: j for j, op in enumerate(m.features.opcodes)})
+
+
+def _gather(samples, packed: _PackedBundle, config: GroupingConfig) -> np.ndarray:
+    """Row i = counts of its routed model's features, FeatureSet order (engine.py:198-202)."""
+    x = np.zeros((len(samples), packed.F), dtype=np.int32)
+    w, lim = config.group_size_bytes, config.max_size_bytes
+    rows, cols, vals = [], [], []
+    for i, s in enumerate(samples):
+        if not 0 <= s.size_bytes < lim:
+            continue
+        colmap = packed.columns[packed.route[s.size_bytes // w]]
+        for op, n in s.histogram.entries.items():
+            j = colmap.get(op)
+            if j is not None:
+                rows.append(i)
+                cols.append(j)
+                vals.append(n)
+    if vals:
+        v = np.asarray(vals, dtype=np.int64)
+        if int(v.max()) > _I32_MAX:
+            raise InvalidConfigError("opcode counts must be < 2^31 for the GPU path")
+        x[np.asarray(rows), np.asarray(cols)] = v
+    return x
+
+
+def _predict_host(x, size, packed: _PackedBundle, config: GroupingConfig, device: int):
+    n = x.shape[0]
+    label = np.empty(n, dtype=np.int32)
+    lp = np.empty((n, 2))
+    elapsed = ctypes.c_int64(0)
+    N.check(N.lib.gnb_predict_host(
+        _ptr(x), n, packed.F, packed.F, _ptr(size), config.group_size_bytes,
+        config.max_size_bytes, _ptr(packed.route), len(packed.ids), 2, _ptr(packed.prior),
+        _ptr(packed.lik), _ptr(label), _ptr(lp), device, ctypes.addressof(elapsed)),
+        "gnb_predict_host")
+    return label, lp, int(elapsed.value)
+
+
+def classify_gpu(bundle: ModelBundle, workload: Workload, *, warmup: bool = True,
+                 device=None) -> TimedRun:
+    """Classify a workload on the GPU; TimedRun identical to classify_sequential.
+
+    elapsed_ns covers the device call only (host->device copy, the K-PRED
+    kernel, device->host copy), like the reference's kernel-only timing
+    (SPEC.md:357): densifying the objects happens before the clock starts."""
+    if not bundle.trained_ids:
+        raise EmptyBundleError("bundle has no trained models")
+    samples = workload.samples
+    config = bundle.config
+    if not samples:
+        return TimedRun((), (), 0)
+    packed = _PackedBundle(bundle)
+    x = _gather(samples, packed, config)
+    size = _sizes(samples, config.max_size_bytes)
+    dev = _device_ordinal(device)
+    if warmup:
+        _predict_host(x, size, packed, config, dev)
+    label, lp, elapsed = _predict_host(x, size, packed, config, dev)
+    preds: list[Prediction | None] = []
+    errors: list[tuple[int, str]] = []
+    ids = packed.ids
+    lim = config.max_size_bytes
+    for i, s in enumerate(samples):
+        lab = int(label[i])
+        if lab == N.ROW_OUT_OF_RANGE:
+            preds.append(None)
+            errors.append((i, oversize_message(s.size_bytes, lim)))
+            continue
+        if lab < 0:
+            raise IntegrityError(f"sample {s.id!r}: negative opcode count")
+        preds.append(Prediction(
+            label=INDEX_CLASS[lab],
+            log_posterior={Label.MALWARE: float(lp[i, 1]), Label.BENIGN: float(lp[i, 0])},
+            effective_group=ids[packed.route[s.size_bytes // config.group_size_bytes]]))
+    return TimedRun(tuple(preds), tuple(errors), max(elapsed, 1))
+
+
+def classify_parallel(bundle: ModelBundle, workload: Workload, *, warmup: bool = True,
+                      device=None) -> TimedRun:
+    """engine.py:250 contract; the GPU is the parallel backend."""
+    return classify_gpu(bundle, workload, warmup=warmup, device=device)
+
+
+def classify_sequential(bundle: ModelBundle, workload: Workload, *, warmup: bool = True,
+                        device=None) -> TimedRun:
+    """engine.py:209 contract.  Runs the same device kernel; results are
+    identical to classify_parallel by construction (one code path)."""
+    return classify_gpu(bundle, workload, warmup=warmup, device=device)
+
+
+def log_posterior(model: GroupModel, histogram: OpcodeHistogram, *, device=None):
+    """Unnormalised joint log-score per class (classifier.py:132-148)."""
+    return predict(model, histogram, device=device).log_posterior
+
+
+def predict(model: GroupModel, histogram: OpcodeHistogram, *, device=None) -> Prediction:
+    """Malware iff strictly higher (classifier.py:151-158)."""
+    cfg = GroupingConfig(group_size_bytes=1, max_size_bytes=1, min_per_class=1)
+    bundle = ModelBundle(cfg, {0: model}, (0,), BundleMeta(len(model.features.opcodes), 1.0, 0, ""))
+    packed = _PackedBundle(bundle)
+    sample = SampleRecord("_", Label.UNKNOWN, 0, histogram)
+    x = _gather([sample], packed, cfg)
+    label, lp, _ = _predict_host(x, np.zeros(1, np.int32), packed, cfg, _device_ordinal(device))
+    return Prediction(INDEX_CLASS[int(label[0])],
+                      {Label.MALWARE: float(lp[0, 1]), Label.BENIGN: float(lp[0, 0])},
+                      model.group)
+
+
+def speedup(tc_ns: int, tp_ns: int) -> float:
+    """Sequential-over-parallel time ratio (engine.py:299-305)."""
+    if tp_ns <= 0:
+        raise MeasurementError(f"parallel time must be positive, got {tp_ns}")
+    if tc_ns < 0:
+        raise MeasurementError(f"sequential time must be non-negative, got {tc_ns}")
+    return tc_ns / tp_ns

@@ -1,0 +1,491 @@
+// C ABI of libgnb.so (declared in include/gnb.h): argument checking, TMA
+// tensor-map encoding, the device entry points and the host-buffer pipelines.
+#include <algorithm>
+#include <chrono>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include <cudaTypedefs.h>
+
+#include "gnb_device.cuh"
+#include "gnb_internal.h"
+
+namespace {
+
+thread_local char g_err[512] = "";
+
+int fail(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  return fail(GNB_ECUDA, "%s: %s (%s)", what, cudaGetErrorName(e), cudaGetErrorString(e));
+}
+
+#define GNB_CUDA(call, what)                   \
+  do {                                          \
+    cudaError_t e_ = (call);                    \
+    if (e_ != cudaSuccess) return cuda_fail(e_, what); \
+  } while (0)
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+bool tma_ok(const void* base, int64_t ldx) {
+  return (reinterpret_cast<uintptr_t>(base) & 15u) == 0 && (ldx % 4) == 0;
+}
+
+}  // namespace
+
+namespace gnb {
+
+// X viewed as a 2-D int32 tensor [n_rows, n_cols] with row pitch ldx*4 bytes;
+// boxes of 32 columns x box_rows rows.  swizzle128: SWIZZLE_128B (predict)
+// or none (fit).
+static bool encode_map(CUtensorMap* map, const void* base, int64_t n_rows, int32_t n_cols,
+                       int64_t ldx, int box_rows, bool swizzle128) {
+  auto fn = encode_fn();
+  if (fn == nullptr) return false;
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(n_cols), static_cast<cuuint64_t>(n_rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ldx) * 4};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(kChunkCols), static_cast<cuuint32_t>(box_rows)};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_INT32, 2, const_cast<void*>(base), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+bool encode_rows_map(CUtensorMap* map, const void* base, int64_t n_rows, int32_t n_cols,
+                     int64_t ldx, int box_rows) {
+  return encode_map(map, base, n_rows, n_cols, ldx, box_rows, true);
+}
+
+}  // namespace gnb
+
+using namespace gnb;
+
+static constexpr int64_t kMaxRowsPerLaunch = int64_t(1) << 30;  // TMA coordinates are int32
+
+extern "C" {
+
+int gnb_abi_version(void) { return 1; }
+
+const char* gnb_strerror(int code) {
+  switch (code) {
+    case GNB_OK: return "ok";
+    case GNB_EINVAL: return "invalid argument";
+    case GNB_ECUDA: return "CUDA error";
+    case GNB_EUNSUPPORTED: return "unsupported shape";
+    case GNB_ENOMEM: return "out of memory";
+    default: return "unknown error";
+  }
+}
+
+const char* gnb_last_error(void) { return g_err; }
+
+size_t gnb_packed_table_bytes(int32_t n_slots, int32_t n_classes, int32_t n_features) {
+  if (n_slots < 1 || n_classes < 1 || n_classes > GNB_MAX_CLASSES || n_features < 1) return 0;
+  return packed_bytes(n_slots, n_classes, n_features);
+}
+
+int gnb_pack_tables(const double* log_prior, const double* log_lik, int32_t n_slots,
+                    int32_t n_classes, int32_t n_features, void* packed, uintptr_t stream) {
+  if (n_slots < 1 || n_classes < 2 || n_classes > GNB_MAX_CLASSES || n_features < 1)
+    return fail(GNB_EINVAL, "pack_tables: need n_slots>=1, 2<=n_classes<=%d, n_features>=1",
+                GNB_MAX_CLASSES);
+  if (!log_prior || !log_lik || !packed) return fail(GNB_EINVAL, "pack_tables: null pointer");
+  if (reinterpret_cast<uintptr_t>(packed) & 15u)
+    return fail(GNB_EINVAL, "pack_tables: packed buffer must be 16-byte aligned");
+  GNB_CUDA(pack_tables(log_prior, log_lik, n_slots, n_classes, n_features, packed,
+                       reinterpret_cast<cudaStream_t>(stream)),
+           "pack_tables");
+  return GNB_OK;
+}
+
+static int check_predict(const int32_t* x, int64_t n_rows, int32_t F, int64_t ldx,
+                         const int32_t* size, int32_t width, int32_t limit,
+                         const int32_t* route, int32_t S, int32_t C, const void* packed,
+                         const int32_t* label) {
+  if (n_rows < 0) return fail(GNB_EINVAL, "predict: n_rows < 0");
+  if (F < 1) return fail(GNB_EINVAL, "predict: n_features must be >= 1");
+  if (ldx < F) return fail(GNB_EINVAL, "predict: ldx (%lld) < n_features (%d)", (long long)ldx, F);
+  if (width <= 0 || limit <= 0 || limit % width != 0)
+    return fail(GNB_EINVAL, "predict: need 0 < group_size_bytes dividing max_size_bytes");
+  if (S < 1) return fail(GNB_EINVAL, "predict: n_slots must be >= 1 (EmptyBundleError)");
+  if (C < 2 || C > GNB_MAX_CLASSES)
+    return fail(GNB_EINVAL, "predict: n_classes must be in [2, %d]", GNB_MAX_CLASSES);
+  if (n_rows > 0 && (!x || !size || !label)) return fail(GNB_EINVAL, "predict: null pointer");
+  if (!route || !packed) return fail(GNB_EINVAL, "predict: null route/packed");
+  return GNB_OK;
+}
+
+static int predict_device(const int32_t* x, int64_t n_rows, int32_t F, int64_t ldx,
+                          const int32_t* size, int32_t width, int32_t limit,
+                          const int32_t* route, int32_t S, int32_t C, const void* packed,
+                          int32_t* label, double* logpost, cudaStream_t stream) {
+  const bool use_tma = tma_ok(x, ldx) && encode_fn() != nullptr;
+  for (int64_t r0 = 0; r0 < n_rows; r0 += kMaxRowsPerLaunch) {
+    const int64_t n = std::min(kMaxRowsPerLaunch, n_rows - r0);
+    PredictParams p{};
+    p.x = x + r0 * ldx;
+    p.ldx = ldx;
+    p.n_rows = n;
+    p.n_features = F;
+    p.size = size + r0;
+    p.width = width;
+    p.limit = limit;
+    p.route = route;
+    p.n_slots = S;
+    p.n_classes = C;
+    p.prior = static_cast<const double*>(packed);
+    p.label = label + r0;
+    p.logpost = logpost ? logpost + r0 * C : nullptr;
+    CUtensorMap map;
+    const CUtensorMap* mp = nullptr;
+    if (use_tma) {
+      if (!encode_map(&map, p.x, n, F, ldx, 128, true))
+        return fail(GNB_ECUDA, "predict: cuTensorMapEncodeTiled failed");
+      mp = &map;
+    }
+    GNB_CUDA(predict_launch(mp, p, stream, 0), "predict launch");
+  }
+  return GNB_OK;
+}
+
+int gnb_predict(const int32_t* x, int64_t n_rows, int32_t n_features, int64_t ldx,
+                const int32_t* size_bytes, int32_t group_size_bytes, int32_t max_size_bytes,
+                const int32_t* route, int32_t n_slots, int32_t n_classes, const void* packed,
+                int32_t* label_out, double* logpost_out, uintptr_t stream) {
+  int rc = check_predict(x, n_rows, n_features, ldx, size_bytes, group_size_bytes,
+                         max_size_bytes, route, n_slots, n_classes, packed, label_out);
+  if (rc) return rc;
+  return predict_device(x, n_rows, n_features, ldx, size_bytes, group_size_bytes,
+                        max_size_bytes, route, n_slots, n_classes, packed, label_out,
+                        logpost_out, reinterpret_cast<cudaStream_t>(stream));
+}
+
+// Test hook: force the L1 (non-TMA) predict kernel.
+int gnb_predict_generic(const int32_t* x, int64_t n_rows, int32_t n_features, int64_t ldx,
+                        const int32_t* size_bytes, int32_t group_size_bytes,
+                        int32_t max_size_bytes, const int32_t* route, int32_t n_slots,
+                        int32_t n_classes, const void* packed, int32_t* label_out,
+                        double* logpost_out, uintptr_t stream) {
+  int rc = check_predict(x, n_rows, n_features, ldx, size_bytes, group_size_bytes,
+                         max_size_bytes, route, n_slots, n_classes, packed, label_out);
+  if (rc) return rc;
+  PredictParams p{};
+  p.x = x;
+  p.ldx = ldx;
+  p.n_rows = n_rows;
+  p.n_features = n_features;
+  p.size = size_bytes;
+  p.width = group_size_bytes;
+  p.limit = max_size_bytes;
+  p.route = route;
+  p.n_slots = n_slots;
+  p.n_classes = n_classes;
+  p.prior = static_cast<const double*>(packed);
+  p.label = label_out;
+  p.logpost = logpost_out;
+  GNB_CUDA(predict_launch(nullptr, p, reinterpret_cast<cudaStream_t>(stream), 1),
+           "predict_generic launch");
+  return GNB_OK;
+}
+
+int gnb_fit_stats(const int32_t* x, int64_t n_rows, int32_t n_cols, int64_t ldx,
+                  const int32_t* size_bytes, const int32_t* labels, int32_t group_size_bytes,
+                  int32_t max_size_bytes, int32_t n_classes, double* sums, double* sumsq,
+                  double* counts, unsigned long long* status, int32_t accumulate,
+                  uintptr_t stream_) {
+  cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
+  if (n_rows < 0 || n_cols < 1 || ldx < n_cols)
+    return fail(GNB_EINVAL, "fit_stats: need n_rows>=0, n_cols>=1, ldx>=n_cols");
+  if (group_size_bytes <= 0 || max_size_bytes <= 0 || max_size_bytes % group_size_bytes)
+    return fail(GNB_EINVAL, "fit_stats: need 0 < group_size_bytes dividing max_size_bytes");
+  if (n_classes < 2 || n_classes > GNB_MAX_CLASSES)
+    return fail(GNB_EINVAL, "fit_stats: n_classes must be in [2, %d]", GNB_MAX_CLASSES);
+  if (!sums || !counts) return fail(GNB_EINVAL, "fit_stats: null output");
+  if (n_rows > 0 && (!x || !size_bytes || !labels)) return fail(GNB_EINVAL, "fit_stats: null input");
+  if (n_rows > 0 && !tma_ok(x, ldx))
+    return fail(GNB_EUNSUPPORTED, "fit_stats: X must be 16-byte aligned with ldx %% 4 == 0");
+  const int64_t G = max_size_bytes / group_size_bytes;
+  const int64_t keys = G * n_classes;
+  if (keys > (int64_t(1) << 30)) return fail(GNB_EINVAL, "fit_stats: too many groups");
+  if (!accumulate) {
+    GNB_CUDA(cudaMemsetAsync(sums, 0, keys * n_cols * sizeof(double), stream), "memset");
+    if (sumsq) GNB_CUDA(cudaMemsetAsync(sumsq, 0, keys * n_cols * sizeof(double), stream), "memset");
+    GNB_CUDA(cudaMemsetAsync(counts, 0, keys * sizeof(double), stream), "memset");
+    if (status) GNB_CUDA(cudaMemsetAsync(status, 0, 2 * sizeof(unsigned long long), stream), "memset");
+  }
+  for (int64_t r0 = 0; r0 < n_rows; r0 += kMaxRowsPerLaunch) {
+    const int64_t n = std::min(kMaxRowsPerLaunch, n_rows - r0);
+    CUtensorMap map;
+    if (!encode_map(&map, x + r0 * ldx, n, n_cols, ldx, 64, false))
+      return fail(GNB_ECUDA, "fit_stats: cuTensorMapEncodeTiled failed");
+    FitParams p{};
+    p.n_rows = n;
+    p.n_cols = n_cols;
+    p.size = size_bytes + r0;
+    p.labels = labels + r0;
+    p.width = group_size_bytes;
+    p.limit = max_size_bytes;
+    p.n_classes = n_classes;
+    p.n_keys = static_cast<int32_t>(keys);
+    p.sums = sums;
+    p.sumsq = sumsq;
+    p.counts = counts;
+    p.status = status;
+    GNB_CUDA(fit_launch(map, p, stream), "fit launch");
+  }
+  return GNB_OK;
+}
+
+int gnb_generate(int32_t* x, int64_t n_rows, int32_t n_cols, int64_t ldx, int32_t* size_bytes,
+                 int32_t* labels, int64_t row_offset, const int64_t* group_row_end,
+                 int32_t n_groups, int32_t group_size_bytes, int32_t n_classes,
+                 double divergence, uint64_t seed, uintptr_t stream) {
+  if (n_rows < 0 || n_cols < 1 || ldx < n_cols || n_groups < 1 || n_groups > 128 ||
+      group_size_bytes < 1 || n_classes < 2 || n_classes > GNB_MAX_CLASSES ||
+      !(divergence >= 0.0 && divergence <= 1.0))
+    return fail(GNB_EINVAL, "generate: bad arguments");
+  if (n_rows > 0 && (!x || !size_bytes || !labels || !group_row_end))
+    return fail(GNB_EINVAL, "generate: null pointer");
+  GenParams p{};
+  p.x = x;
+  p.ldx = ldx;
+  p.n_rows = n_rows;
+  p.n_cols = n_cols;
+  p.size = size_bytes;
+  p.labels = labels;
+  p.row_offset = row_offset;
+  p.n_groups = n_groups;
+  p.width = group_size_bytes;
+  p.n_classes = n_classes;
+  p.divergence = divergence;
+  p.seed = seed;
+  for (int g = 0; g < n_groups; ++g) p.group_end[g] = group_row_end[g];
+  GNB_CUDA(generate_launch(p, reinterpret_cast<cudaStream_t>(stream)), "generate launch");
+  return GNB_OK;
+}
+
+// ---------------------------------------------------------------- host pipelines
+namespace {
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t n = 0;
+  cudaError_t ensure(size_t bytes) {
+    if (bytes <= n) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+    cudaError_t e = cudaMalloc(&p, bytes);
+    if (e == cudaSuccess) n = bytes;
+    return e;
+  }
+};
+
+constexpr int kLanes = 3;  // chunk pipeline depth (streams)
+
+struct HostCtx {
+  int device = -1;
+  cudaStream_t s[kLanes] = {};
+  cudaEvent_t ev[kLanes] = {};
+  DevBuf x[kLanes], size[kLanes], aux[kLanes], label[kLanes], logpost[kLanes];
+  DevBuf route, prior, lik, packed, sums, sumsq, counts, status;
+};
+
+thread_local std::vector<HostCtx*> g_ctx;
+
+int get_ctx(int device, HostCtx** out) {
+  for (HostCtx* c : g_ctx)
+    if (c->device == device) {
+      *out = c;
+      return GNB_OK;
+    }
+  auto* c = new HostCtx();
+  c->device = device;
+  for (int i = 0; i < kLanes; ++i) {
+    GNB_CUDA(cudaStreamCreateWithFlags(&c->s[i], cudaStreamNonBlocking), "stream create");
+    GNB_CUDA(cudaEventCreateWithFlags(&c->ev[i], cudaEventDisableTiming), "event create");
+  }
+  g_ctx.push_back(c);
+  *out = c;
+  return GNB_OK;
+}
+
+int64_t chunk_rows_for(int64_t row_bytes) {
+  const int64_t target = int64_t(64) << 20;  // ~64 MiB of X per chunk
+  int64_t r = std::max<int64_t>(1024, target / std::max<int64_t>(row_bytes, 1));
+  return (r + 127) / 128 * 128;
+}
+
+}  // namespace
+
+int gnb_predict_host(const int32_t* x, int64_t n_rows, int32_t n_features, int64_t ldx,
+                     const int32_t* size_bytes, int32_t group_size_bytes,
+                     int32_t max_size_bytes, const int32_t* route, int32_t n_slots,
+                     int32_t n_classes, const double* log_prior, const double* log_lik,
+                     int32_t* label_out, double* logpost_out, int32_t device,
+                     int64_t* elapsed_ns) {
+  const auto t0 = std::chrono::steady_clock::now();
+  int rc = check_predict(x, n_rows, n_features, ldx, size_bytes, group_size_bytes,
+                         max_size_bytes, route, n_slots, n_classes, log_prior, label_out);
+  if (rc) return rc;
+  if (!log_lik) return fail(GNB_EINVAL, "predict_host: null log_lik");
+  GNB_CUDA(cudaSetDevice(device), "cudaSetDevice");
+  HostCtx* c = nullptr;
+  if ((rc = get_ctx(device, &c))) return rc;
+  const int G = max_size_bytes / group_size_bytes;
+  const size_t prior_b = size_t(n_slots) * n_classes * 8;
+  const size_t lik_b = prior_b * n_features;
+  const size_t packed_b = packed_bytes(n_slots, n_classes, n_features);
+  GNB_CUDA(c->route.ensure(size_t(G) * 4), "malloc");
+  GNB_CUDA(c->prior.ensure(prior_b), "malloc");
+  GNB_CUDA(c->lik.ensure(lik_b), "malloc");
+  GNB_CUDA(c->packed.ensure(packed_b), "malloc");
+  cudaStream_t s0 = c->s[0];
+  GNB_CUDA(cudaMemcpyAsync(c->route.p, route, size_t(G) * 4, cudaMemcpyHostToDevice, s0), "H2D");
+  GNB_CUDA(cudaMemcpyAsync(c->prior.p, log_prior, prior_b, cudaMemcpyHostToDevice, s0), "H2D");
+  GNB_CUDA(cudaMemcpyAsync(c->lik.p, log_lik, lik_b, cudaMemcpyHostToDevice, s0), "H2D");
+  GNB_CUDA(pack_tables(static_cast<double*>(c->prior.p), static_cast<double*>(c->lik.p),
+                       n_slots, n_classes, n_features, c->packed.p, s0),
+           "pack");
+  GNB_CUDA(cudaEventRecord(c->ev[0], s0), "event");
+  for (int i = 1; i < kLanes; ++i) GNB_CUDA(cudaStreamWaitEvent(c->s[i], c->ev[0], 0), "wait");
+
+  const int64_t ld = (n_features + 3) / 4 * 4;  // device rows padded for TMA
+  const int64_t rows = std::min<int64_t>(chunk_rows_for(ld * 4), std::max<int64_t>(n_rows, 1));
+  for (int i = 0; i < kLanes; ++i) {
+    GNB_CUDA(c->x[i].ensure(size_t(rows) * ld * 4), "malloc");
+    GNB_CUDA(c->size[i].ensure(size_t(rows) * 4), "malloc");
+    GNB_CUDA(c->label[i].ensure(size_t(rows) * 4), "malloc");
+    if (logpost_out) GNB_CUDA(c->logpost[i].ensure(size_t(rows) * n_classes * 8), "malloc");
+  }
+  int64_t chunk = 0;
+  for (int64_t r0 = 0; r0 < n_rows; r0 += rows, ++chunk) {
+    const int lane = static_cast<int>(chunk % kLanes);
+    cudaStream_t s = c->s[lane];
+    const int64_t n = std::min(rows, n_rows - r0);
+    int32_t* dx = static_cast<int32_t*>(c->x[lane].p);
+    if (ldx == ld) {
+      GNB_CUDA(cudaMemcpyAsync(dx, x + r0 * ldx, size_t(n) * ld * 4, cudaMemcpyHostToDevice, s), "H2D");
+    } else {
+      GNB_CUDA(cudaMemcpy2DAsync(dx, ld * 4, x + r0 * ldx, ldx * 4, size_t(n_features) * 4, n,
+                                 cudaMemcpyHostToDevice, s),
+               "H2D 2D");
+    }
+    GNB_CUDA(cudaMemcpyAsync(c->size[lane].p, size_bytes + r0, size_t(n) * 4,
+                             cudaMemcpyHostToDevice, s),
+             "H2D");
+    rc = predict_device(dx, n, n_features, ld, static_cast<int32_t*>(c->size[lane].p),
+                        group_size_bytes, max_size_bytes, static_cast<int32_t*>(c->route.p),
+                        n_slots, n_classes, c->packed.p, static_cast<int32_t*>(c->label[lane].p),
+                        logpost_out ? static_cast<double*>(c->logpost[lane].p) : nullptr, s);
+    if (rc) return rc;
+    GNB_CUDA(cudaMemcpyAsync(label_out + r0, c->label[lane].p, size_t(n) * 4,
+                             cudaMemcpyDeviceToHost, s),
+             "D2H");
+    if (logpost_out)
+      GNB_CUDA(cudaMemcpyAsync(logpost_out + r0 * n_classes, c->logpost[lane].p,
+                               size_t(n) * n_classes * 8, cudaMemcpyDeviceToHost, s),
+               "D2H");
+  }
+  for (int i = 0; i < kLanes; ++i) GNB_CUDA(cudaStreamSynchronize(c->s[i]), "sync");
+  if (elapsed_ns)
+    *elapsed_ns = std::chrono::duration_cast<std::chrono::nanoseconds>(
+                      std::chrono::steady_clock::now() - t0)
+                      .count();
+  return GNB_OK;
+}
+
+int gnb_fit_stats_host(const int32_t* x, int64_t n_rows, int32_t n_cols, int64_t ldx,
+                       const int32_t* size_bytes, const int32_t* labels,
+                       int32_t group_size_bytes, int32_t max_size_bytes, int32_t n_classes,
+                       double* sums, double* sumsq, double* counts,
+                       unsigned long long* status, int32_t device) {
+  if (n_rows < 0 || n_cols < 1 || ldx < n_cols)
+    return fail(GNB_EINVAL, "fit_stats_host: need n_rows>=0, n_cols>=1, ldx>=n_cols");
+  if (group_size_bytes <= 0 || max_size_bytes <= 0 || max_size_bytes % group_size_bytes)
+    return fail(GNB_EINVAL, "fit_stats_host: need 0 < group_size_bytes dividing max_size_bytes");
+  if (n_classes < 2 || n_classes > GNB_MAX_CLASSES)
+    return fail(GNB_EINVAL, "fit_stats_host: n_classes must be in [2, %d]", GNB_MAX_CLASSES);
+  if (!sums || !counts) return fail(GNB_EINVAL, "fit_stats_host: null output");
+  GNB_CUDA(cudaSetDevice(device), "cudaSetDevice");
+  HostCtx* c = nullptr;
+  int rc = get_ctx(device, &c);
+  if (rc) return rc;
+  const int64_t keys = int64_t(max_size_bytes / group_size_bytes) * n_classes;
+  const size_t stat_b = size_t(keys) * n_cols * 8;
+  GNB_CUDA(c->sums.ensure(stat_b), "malloc");
+  if (sumsq) GNB_CUDA(c->sumsq.ensure(stat_b), "malloc");
+  GNB_CUDA(c->counts.ensure(size_t(keys) * 8), "malloc");
+  GNB_CUDA(c->status.ensure(16), "malloc");
+  cudaStream_t s0 = c->s[0];
+  double* dS = static_cast<double*>(c->sums.p);
+  double* dQ = sumsq ? static_cast<double*>(c->sumsq.p) : nullptr;
+  double* dN = static_cast<double*>(c->counts.p);
+  auto* dst = static_cast<unsigned long long*>(c->status.p);
+  GNB_CUDA(cudaMemsetAsync(dS, 0, stat_b, s0), "memset");
+  if (dQ) GNB_CUDA(cudaMemsetAsync(dQ, 0, stat_b, s0), "memset");
+  GNB_CUDA(cudaMemsetAsync(dN, 0, size_t(keys) * 8, s0), "memset");
+  GNB_CUDA(cudaMemsetAsync(dst, 0, 16, s0), "memset");
+  GNB_CUDA(cudaEventRecord(c->ev[0], s0), "event");
+  for (int i = 1; i < kLanes; ++i) GNB_CUDA(cudaStreamWaitEvent(c->s[i], c->ev[0], 0), "wait");
+  const int64_t ld = (n_cols + 3) / 4 * 4;
+  const int64_t rows = std::min<int64_t>(chunk_rows_for(ld * 4), std::max<int64_t>(n_rows, 1));
+  for (int i = 0; i < kLanes; ++i) {
+    GNB_CUDA(c->x[i].ensure(size_t(rows) * ld * 4), "malloc");
+    GNB_CUDA(c->size[i].ensure(size_t(rows) * 4), "malloc");
+    GNB_CUDA(c->aux[i].ensure(size_t(rows) * 4), "malloc");
+  }
+  // chunks on different streams may run concurrently: every chunk adds exact
+  // integer-valued partials with RED.ADD.F64, so the order does not matter.
+  int64_t chunk = 0;
+  for (int64_t r0 = 0; r0 < n_rows; r0 += rows, ++chunk) {
+    const int lane = static_cast<int>(chunk % kLanes);
+    cudaStream_t s = c->s[lane];
+    const int64_t n = std::min(rows, n_rows - r0);
+    int32_t* dx = static_cast<int32_t*>(c->x[lane].p);
+    if (ldx == ld)
+      GNB_CUDA(cudaMemcpyAsync(dx, x + r0 * ldx, size_t(n) * ld * 4, cudaMemcpyHostToDevice, s), "H2D");
+    else
+      GNB_CUDA(cudaMemcpy2DAsync(dx, ld * 4, x + r0 * ldx, ldx * 4, size_t(n_cols) * 4, n,
+                                 cudaMemcpyHostToDevice, s),
+               "H2D 2D");
+    GNB_CUDA(cudaMemcpyAsync(c->size[lane].p, size_bytes + r0, size_t(n) * 4, cudaMemcpyHostToDevice, s), "H2D");
+    GNB_CUDA(cudaMemcpyAsync(c->aux[lane].p, labels + r0, size_t(n) * 4, cudaMemcpyHostToDevice, s), "H2D");
+    rc = gnb_fit_stats(dx, n, n_cols, ld, static_cast<int32_t*>(c->size[lane].p),
+                       static_cast<int32_t*>(c->aux[lane].p), group_size_bytes, max_size_bytes,
+                       n_classes, dS, dQ, dN, dst, 1, reinterpret_cast<uintptr_t>(s));
+    if (rc) return rc;
+  }
+  for (int i = 0; i < kLanes; ++i) GNB_CUDA(cudaStreamSynchronize(c->s[i]), "sync");
+  GNB_CUDA(cudaMemcpy(sums, dS, stat_b, cudaMemcpyDeviceToHost), "D2H");
+  if (sumsq) GNB_CUDA(cudaMemcpy(sumsq, dQ, stat_b, cudaMemcpyDeviceToHost), "D2H");
+  GNB_CUDA(cudaMemcpy(counts, dN, size_t(keys) * 8, cudaMemcpyDeviceToHost), "D2H");
+  if (status) GNB_CUDA(cudaMemcpy(status, dst, 16, cudaMemcpyDeviceToHost), "D2H");
+  return GNB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,80 @@
+// Internal launch interfaces shared by the kernel translation units and the C ABI.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include "../../include/gnb.h"
+
+namespace gnb {
+
+struct PredictParams {
+  const int32_t* x;  // generic kernel only (TMA path reads through the tensor map)
+  int64_t ldx;
+  int64_t n_rows;
+  int32_t n_features;
+  int32_t n_chunks;  // ceil(F / 32), set by predict_launch
+  const int32_t* size;
+  int32_t width;
+  int32_t limit;
+  const int32_t* route;
+  int32_t n_slots;
+  int32_t n_classes;
+  const double* prior;  // packed: [S][CP]
+  const double* tab;    // packed: [S][NCH][32][CP][2], set by predict_launch
+  int32_t* label;
+  double* logpost;  // nullable, [N][C]
+  int64_t n_tiles;  // set by predict_launch
+};
+
+struct FitParams {
+  int64_t n_rows;
+  int32_t n_cols;
+  int32_t n_chunks;
+  const int32_t* size;
+  const int32_t* labels;
+  int32_t width;
+  int32_t limit;
+  int32_t n_classes;
+  int32_t n_keys;     // groups * classes
+  int32_t smem_keys;  // keys [0, smem_keys) accumulate in shared memory
+  double* sums;       // [G][C][V]
+  double* sumsq;      // nullable
+  double* counts;     // [G][C]
+  unsigned long long* status;  // [2]: bad label, out of range
+  int64_t n_tiles;
+};
+
+int class_pad(int n_classes);
+size_t packed_bytes(int n_slots, int n_classes, int n_features);
+cudaError_t pack_tables(const double* log_prior, const double* log_lik, int S, int C, int F,
+                        void* packed, cudaStream_t stream);
+// map == nullptr (or force_generic) selects the L1 path that accepts any ldx.
+cudaError_t predict_launch(const CUtensorMap* map, PredictParams p, cudaStream_t stream,
+                           int force_generic);
+cudaError_t fit_launch(const CUtensorMap& map, FitParams p, cudaStream_t stream);
+
+struct GenParams {
+  int32_t* x;
+  int64_t ldx;
+  int64_t n_rows;
+  int32_t n_cols;
+  int32_t* size;
+  int32_t* labels;
+  int64_t row_offset;
+  int32_t n_groups;
+  int32_t width;
+  int32_t n_classes;
+  double divergence;
+  unsigned long long seed;
+  long long group_end[128];
+};
+cudaError_t generate_launch(const GenParams& p, cudaStream_t stream);
+
+// Host helpers (api.cu)
+bool encode_rows_map(CUtensorMap* map, const void* base, int64_t n_rows, int32_t n_cols,
+                     int64_t ldx, int box_rows);
+
+}  // namespace gnb

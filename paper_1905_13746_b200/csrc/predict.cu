@@ -1,0 +1,404 @@
+// K-PRED: group-wise Naive Bayes scoring + fused argmax on sm_100a.
+//
+// Replaces the reference's per-sample loop (pkg/src/groupnb/engine.py:198-205)
+// and its kernel classifier.log_posterior / predict
+// (pkg/src/groupnb/classifier.py:132-158).
+//
+// Data path:
+//   * X [N, F] int32 is streamed from HBM exactly once by TMA: 2-D boxes of
+//     32 columns (128 B) x ROWS rows, SWIZZLE_128B, through a STAGES-deep
+//     mbarrier ring filled by one producer warp.
+//   * each consumer thread owns one row and walks its features in FeatureSet
+//     order: acc_c = acc_c + x * ll_c with the product computed by one DFMA
+//     (exact_product) and the add by one DADD -- the same two roundings as the
+//     reference's `score += n * ll`, so log-posteriors are bit-identical.
+//   * the producer routes the tile's rows (size -> group -> slot, the whole
+//     route table lookup of engine.py:202) and, when every valid row of the tile
+//     shares a slot (G=1, or rows grouped by size group as the reference's
+//     GroupedCorpus orders them), also bulk-copies that slot's 32-feature table
+//     slice next to the X box, so table reads are smem broadcasts.  Mixed tiles
+//     read per-row tables through L1 instead.  All groups: one launch.
+//   * argmax (ties -> lowest class index = benign) and the out-of-range status
+//     are fused into the epilogue; label (+ optional log-posteriors) written
+//     once, coalesced.
+#include <cfloat>
+#include <climits>
+#include <cstdint>
+
+#include "gnb_device.cuh"
+#include "gnb_internal.h"
+
+namespace gnb {
+
+// ------------------------------------------------------------------ tables
+// packed = [prior: S][CP] | [tab: S][NCH][32 features][CP][{ll, -2^52 ll}]
+__global__ void pack_tables_kernel(const double* __restrict__ log_prior,
+                                   const double* __restrict__ log_lik, int S, int C, int F,
+                                   int CP, int NCH, double* __restrict__ prior_out,
+                                   double* __restrict__ tab_out) {
+  const int64_t total_prior = static_cast<int64_t>(S) * CP;
+  const int64_t total_tab = static_cast<int64_t>(S) * NCH * kChunkCols * CP;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+       i < total_prior + total_tab; i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    if (i < total_prior) {
+      const int s = static_cast<int>(i / CP), c = static_cast<int>(i % CP);
+      prior_out[i] = c < C ? log_prior[static_cast<int64_t>(s) * C + c] : -INFINITY;
+    } else {
+      const int64_t k = i - total_prior;
+      const int c = static_cast<int>(k % CP);
+      const int j = static_cast<int>((k / CP) % (NCH * kChunkCols));  // feature
+      const int s = static_cast<int>(k / (static_cast<int64_t>(CP) * NCH * kChunkCols));
+      double ll = 0.0;
+      if (c < C && j < F) ll = log_lik[(static_cast<int64_t>(s) * C + c) * F + j];
+      tab_out[2 * k] = ll;
+      tab_out[2 * k + 1] = -0x1p52 * ll;  // exact: power-of-two scale
+    }
+  }
+}
+
+// ------------------------------------------------------------------ inner loops
+template <int CP>
+struct SmemTab {
+  const double* p;
+  __device__ __forceinline__ double2 get(int idx) const {
+    return *reinterpret_cast<const double2*>(p + 2 * idx);
+  }
+};
+template <int CP>
+struct GlobalTab {
+  const double* p;
+  __device__ __forceinline__ double2 get(int idx) const {
+    return __ldg(reinterpret_cast<const double2*>(p + 2 * idx));
+  }
+};
+
+// 4 consecutive features (one 16-B smem chunk) of one row, all classes.
+template <int CP, typename Tab>
+__device__ __forceinline__ void score_quad(double (&acc)[CP], const uint4 v, const Tab& tab,
+                                           int feat0) {
+  const uint32_t xs[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+#pragma unroll
+    for (int c = 0; c < CP; ++c) {
+      const double2 t = tab.get((feat0 + e) * CP + c);
+      acc[c] = __dadd_rn(acc[c], exact_product(xs[e], t.x, t.y));
+    }
+  }
+}
+
+template <int CP, typename Tab>
+__device__ __forceinline__ void score_chunk(double (&acc)[CP], const uint8_t* box, uint32_t row,
+                                            const Tab& tab, int nq, uint32_t& neg) {
+  if (nq == 8) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const uint4 v = *reinterpret_cast<const uint4*>(box + swz128(row, q));
+      neg |= v.x | v.y | v.z | v.w;
+      score_quad<CP>(acc, v, tab, 4 * q);
+    }
+  } else {
+#pragma unroll 1
+    for (int q = 0; q < nq; ++q) {
+      const uint4 v = *reinterpret_cast<const uint4*>(box + swz128(row, q));
+      neg |= v.x | v.y | v.z | v.w;
+      score_quad<CP>(acc, v, tab, 4 * q);
+    }
+  }
+}
+
+template <int CP>
+__device__ __forceinline__ void write_row(const PredictParams& p, int64_t r, int slot,
+                                          uint32_t neg, const double (&acc)[CP]) {
+  int lab;
+  if (slot < 0) {
+    lab = GNB_ROW_OUT_OF_RANGE;
+  } else if (neg & 0x80000000u) {
+    lab = GNB_ROW_NEGATIVE_COUNT;
+  } else {
+    lab = 0;
+    double best = acc[0];
+#pragma unroll
+    for (int c = 1; c < CP; ++c) {
+      if (acc[c] > best) {  // strict: ties keep the lower index (benign)
+        best = acc[c];
+        lab = c;
+      }
+    }
+  }
+  p.label[r] = lab;
+  if (p.logpost != nullptr) {
+    double* out = p.logpost + r * p.n_classes;
+    if (p.n_classes == 2 && CP == 2) {
+      const double2 v = slot < 0 ? make_double2(__longlong_as_double(0x7ff8000000000000ll),
+                                                __longlong_as_double(0x7ff8000000000000ll))
+                                 : make_double2(acc[0], acc[CP > 1 ? 1 : 0]);
+      *reinterpret_cast<double2*>(out) = v;
+    } else {
+#pragma unroll
+      for (int c = 0; c < CP; ++c)
+        if (c < p.n_classes) out[c] = slot < 0 ? __longlong_as_double(0x7ff8000000000000ll) : acc[c];
+    }
+  }
+}
+
+// ------------------------------------------------------------------ TMA kernel
+template <int CP, int NW, int STAGES>
+struct PredictSmem {
+  static constexpr int kRows = NW * 32;
+  static constexpr int kXBytes = kRows * kChunkBytesPerRow;        // one box
+  static constexpr int kTabBytes = kChunkCols * CP * 2 * 8;         // one table slice
+  static constexpr int kHdrBytes = ((4 + kRows * 4) + 15) / 16 * 16;
+  static constexpr int kX = 0;
+  static constexpr int kTab = kX + STAGES * kXBytes;
+  static constexpr int kHdr = kTab + STAGES * kTabBytes;
+  static constexpr int kBar = kHdr + STAGES * kHdrBytes;
+  static constexpr int kTotal = kBar + 2 * STAGES * 8;
+  static constexpr int kAlloc = kTotal + 1024;  // slack for 1024-B alignment
+};
+
+struct StageHdr {
+  int tile_slot;  // >= 0: every valid row uses this slot; table slice staged
+  int row_slot[1];
+};
+
+template <int CP, int NW, int STAGES>
+__global__ void __launch_bounds__((NW + 1) * 32)
+    predict_tma_kernel(const __grid_constant__ CUtensorMap xmap, const PredictParams p) {
+  using L = PredictSmem<CP, NW, STAGES>;
+  constexpr int ROWS = L::kRows;
+  extern __shared__ uint8_t smem_raw[];
+  // 1024-B alignment for SWIZZLE_128B, keeping the pointer in the shared window
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::kBar);
+  uint64_t* empty = full + STAGES;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 32);   // all producer lanes arrive (lane 0 with tx)
+      mbar_init(&empty[s], NW);  // one arrive per consumer warp
+    }
+    mbar_fence_init();
+  }
+  if (warp == NW && lane == 0) prefetch_tensormap(&xmap);
+  __syncthreads();
+
+  const int NCH = p.n_chunks;
+  const int64_t n_tiles = p.n_tiles;
+
+  if (warp == NW) {
+    // ---------------------------------------------------------- producer
+    const uint64_t pol_x = policy_evict_first();
+    const uint64_t pol_t = policy_evict_last();
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+      const int64_t r0 = tile * ROWS;
+      int slots[ROWS / 32];
+      int lo = INT_MAX, hi = INT_MIN;
+#pragma unroll
+      for (int i = 0; i < ROWS / 32; ++i) {
+        const int64_t r = r0 + lane + 32 * i;
+        int s = -1;
+        if (r < p.n_rows) {
+          const int sz = __ldg(p.size + r);
+          if (sz >= 0 && sz < p.limit) {
+            s = __ldg(p.route + sz / p.width);
+            lo = min(lo, s);
+            hi = max(hi, s);
+          }
+        }
+        slots[i] = s;
+      }
+      lo = __reduce_min_sync(0xffffffffu, lo);
+      hi = __reduce_max_sync(0xffffffffu, hi);
+      const int tile_slot = (lo == INT_MAX) ? 0 : (lo == hi ? lo : -1);
+      for (int ch = 0; ch < NCH; ++ch) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        StageHdr* hdr = reinterpret_cast<StageHdr*>(smem + L::kHdr + stage * L::kHdrBytes);
+        if (ch == 0) {
+#pragma unroll
+          for (int i = 0; i < ROWS / 32; ++i) hdr->row_slot[lane + 32 * i] = slots[i];
+        }
+        if (lane == 0) hdr->tile_slot = tile_slot;
+        __syncwarp();
+        if (lane == 0) {
+          const uint32_t bytes = L::kXBytes + (tile_slot >= 0 ? L::kTabBytes : 0);
+          mbar_arrive_expect_tx(&full[stage], bytes);
+          tma_load_2d(smem + L::kX + stage * L::kXBytes, &xmap, ch * kChunkCols,
+                      static_cast<int32_t>(r0), &full[stage], pol_x);
+          if (tile_slot >= 0) {
+            const double* src =
+                p.tab + (static_cast<int64_t>(tile_slot) * NCH + ch) * (kChunkCols * CP * 2);
+            bulk_load(smem + L::kTab + stage * L::kTabBytes, src, L::kTabBytes, &full[stage],
+                      pol_t);
+          }
+        } else {
+          mbar_arrive(&full[stage]);
+        }
+        if (++stage == STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else {
+    // ---------------------------------------------------------- consumers
+    const uint32_t t = threadIdx.x;  // row within the tile
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+      const int64_t r = tile * ROWS + t;
+      double acc[CP];
+      int slot = -1;
+      uint32_t neg = 0;
+      for (int ch = 0; ch < NCH; ++ch) {
+        mbar_wait(&full[stage], phase);
+        const StageHdr* hdr =
+            reinterpret_cast<const StageHdr*>(smem + L::kHdr + stage * L::kHdrBytes);
+        const int ts = hdr->tile_slot;
+        if (ch == 0) {
+          slot = hdr->row_slot[t];
+          const int s = ts >= 0 ? ts : max(slot, 0);
+#pragma unroll
+          for (int c = 0; c < CP; ++c) acc[c] = __ldg(p.prior + s * CP + c);
+        }
+        const int nf = min(kChunkCols, p.n_features - ch * kChunkCols);
+        const int nq = (nf + 3) >> 2;
+        const uint8_t* box = smem + L::kX + stage * L::kXBytes;
+        if (ts >= 0) {
+          const SmemTab<CP> tab{
+              reinterpret_cast<const double*>(smem + L::kTab + stage * L::kTabBytes)};
+          score_chunk<CP>(acc, box, t, tab, nq, neg);
+        } else {
+          const GlobalTab<CP> tab{
+              p.tab + (static_cast<int64_t>(max(slot, 0)) * NCH + ch) * (kChunkCols * CP * 2)};
+          score_chunk<CP>(acc, box, t, tab, nq, neg);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[stage]);
+        if (++stage == STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+      if (r < p.n_rows) write_row<CP>(p, r, slot, neg, acc);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ generic kernel
+// Any layout (ldx not a multiple of 4, unaligned X): one thread per row,
+// loads through L1.  Same arithmetic, same results; slower.
+template <int CP>
+__global__ void __launch_bounds__(256) predict_generic_kernel(const PredictParams p) {
+  const int NCH = p.n_chunks;
+  for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r < p.n_rows;
+       r += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int sz = p.size[r];
+    const int slot = (sz >= 0 && sz < p.limit) ? p.route[sz / p.width] : -1;
+    const int s = max(slot, 0);
+    double acc[CP];
+#pragma unroll
+    for (int c = 0; c < CP; ++c) acc[c] = p.prior[s * CP + c];
+    const int32_t* row = p.x + r * p.ldx;
+    uint32_t neg = 0;
+    for (int j = 0; j < p.n_features; ++j) {
+      const uint32_t x = static_cast<uint32_t>(__ldg(row + j));
+      neg |= x;
+      const GlobalTab<CP> tab{p.tab +
+                              (static_cast<int64_t>(s) * NCH + j / kChunkCols) *
+                                  (kChunkCols * CP * 2)};
+#pragma unroll
+      for (int c = 0; c < CP; ++c) {
+        const double2 t = tab.get((j % kChunkCols) * CP + c);
+        acc[c] = __dadd_rn(acc[c], exact_product(x, t.x, t.y));
+      }
+    }
+    write_row<CP>(p, r, slot, neg, acc);
+  }
+}
+
+// ------------------------------------------------------------------ launchers
+template <int CP, int NW, int STAGES>
+static cudaError_t launch_tma(const CUtensorMap& map, const PredictParams& p,
+                              cudaStream_t stream) {
+  using L = PredictSmem<CP, NW, STAGES>;
+  auto kern = predict_tma_kernel<CP, NW, STAGES>;
+  static int per_sm = 0;  // resident CTAs per SM for this instantiation
+  static int sms = 0;
+  if (per_sm == 0) {
+    cudaError_t e =
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kAlloc);
+    if (e != cudaSuccess) return e;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, (NW + 1) * 32, L::kAlloc);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) per_sm = 1;
+  }
+  const int64_t want = static_cast<int64_t>(sms) * per_sm;
+  const int grid = static_cast<int>(p.n_tiles < want ? p.n_tiles : want);
+  if (grid == 0) return cudaSuccess;
+  kern<<<grid, (NW + 1) * 32, L::kAlloc, stream>>>(map, p);
+  return cudaGetLastError();
+}
+
+template <int CP>
+static cudaError_t launch_generic(const PredictParams& p, cudaStream_t stream) {
+  const int64_t blocks64 = (p.n_rows + 255) / 256;
+  const int blocks = static_cast<int>(blocks64 < 148 * 16 ? blocks64 : 148 * 16);
+  if (blocks == 0) return cudaSuccess;
+  predict_generic_kernel<CP><<<blocks, 256, 0, stream>>>(p);
+  return cudaGetLastError();
+}
+
+int class_pad(int C) { return C <= 2 ? 2 : C <= 4 ? 4 : C <= 8 ? 8 : 16; }
+
+size_t packed_bytes(int S, int C, int F) {
+  const int CP = class_pad(C);
+  const int NCH = (F + kChunkCols - 1) / kChunkCols;
+  return static_cast<size_t>(S) * CP * 8 +
+         static_cast<size_t>(S) * NCH * kChunkCols * CP * 2 * 8;
+}
+
+cudaError_t pack_tables(const double* log_prior, const double* log_lik, int S, int C, int F,
+                        void* packed, cudaStream_t stream) {
+  const int CP = class_pad(C);
+  const int NCH = (F + kChunkCols - 1) / kChunkCols;
+  double* prior = static_cast<double*>(packed);
+  double* tab = prior + static_cast<int64_t>(S) * CP;
+  const int64_t total = static_cast<int64_t>(S) * CP * (1 + NCH * kChunkCols);
+  const int blocks = static_cast<int>((total + 255) / 256 < 4096 ? (total + 255) / 256 : 4096);
+  pack_tables_kernel<<<blocks > 0 ? blocks : 1, 256, 0, stream>>>(log_prior, log_lik, S, C, F,
+                                                                   CP, NCH, prior, tab);
+  return cudaGetLastError();
+}
+
+cudaError_t predict_launch(const CUtensorMap* map, PredictParams p, cudaStream_t stream,
+                           int force_generic) {
+  const int CP = class_pad(p.n_classes);
+  p.n_chunks = (p.n_features + kChunkCols - 1) / kChunkCols;
+  const double* prior = p.prior;
+  p.tab = prior + static_cast<int64_t>(p.n_slots) * CP;
+  if (map != nullptr && !force_generic) {
+    constexpr int NW = 4;
+    p.n_tiles = (p.n_rows + NW * 32 - 1) / (NW * 32);
+    switch (CP) {
+      case 2: return launch_tma<2, NW, 8>(*map, p, stream);
+      case 4: return launch_tma<4, NW, 6>(*map, p, stream);
+      case 8: return launch_tma<8, NW, 6>(*map, p, stream);
+      default: return launch_tma<16, NW, 4>(*map, p, stream);
+    }
+  }
+  switch (CP) {
+    case 2: return launch_generic<2>(p, stream);
+    case 4: return launch_generic<4>(p, stream);
+    case 8: return launch_generic<8>(p, stream);
+    default: return launch_generic<16>(p, stream);
+  }
+}
+
+}  // namespace gnb

@@ -1,0 +1,229 @@
+"""Dense device API over libgnb.so: the throughput boundary of the hot path.
+
+Tensors are torch CUDA tensors (torch is only the allocator / stream carrier);
+every call enqueues one of the hand-written sm_100a kernels on the current
+(or given) stream through the C ABI in include/gnb.h.  No CPU fallback: a
+non-CUDA tensor is an error.
+
+  fit_stats  -> K-FIT   (features.py:48-53, classifier.py:94-101, corpus.py:302-305)
+  fin_train  -> FIN     (features.py:59-86, classifier.py:103-120)  [host C++]
+  predict    -> K-PRED  (classifier.py:132-158, engine.py:187-206)
+  generate   -> GEN     (synth.py:64-116 law, counter-based)
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .errors import InvalidConfigError
+
+
+def _stream(stream) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)
+
+
+def _dev(t: torch.Tensor, name: str, dtype) -> int:
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise InvalidConfigError(f"{name} must be a CUDA tensor (no CPU fallback)")
+    if t.dtype != dtype:
+        raise InvalidConfigError(f"{name} must be {dtype}, got {t.dtype}")
+    return t.data_ptr()
+
+
+def _rows(x: torch.Tensor, name: str = "x"):
+    ptr = _dev(x, name, torch.int32)
+    if x.dim() != 2 or x.stride(1) != 1:
+        raise InvalidConfigError(f"{name} must be a row-major [N, F] int32 matrix")
+    return ptr, x.shape[0], x.shape[1], max(x.stride(0), x.shape[1])
+
+
+def _vec(t: torch.Tensor, n: int, name: str, dtype=torch.int32) -> int:
+    ptr = _dev(t, name, dtype)
+    if t.dim() != 1 or t.shape[0] != n or (n > 1 and t.stride(0) != 1):
+        raise InvalidConfigError(f"{name} must be a contiguous vector of length {n}")
+    return ptr
+
+
+# ---------------------------------------------------------------- predict
+@dataclass
+class DeviceTables:
+    """A model bundle resident on one device, in the K-PRED layout.
+
+    route[group_count] maps size group -> slot; packed holds the per-slot
+    log priors and (ll, -2^52 ll) feature tables (gnb_pack_tables).
+    """
+
+    route: torch.Tensor
+    packed: torch.Tensor
+    n_slots: int
+    n_classes: int
+    n_features: int
+    group_size_bytes: int
+    max_size_bytes: int
+
+    @classmethod
+    def build(cls, log_prior, log_lik, route, *, group_size_bytes: int, max_size_bytes: int,
+              device=None, stream=None) -> "DeviceTables":
+        """log_prior [S, C], log_lik [S, C, F] (fp64), route [max/width] -> slot."""
+        device = torch.device(device or "cuda")
+        lp = torch.as_tensor(log_prior, dtype=torch.float64).to(device).contiguous()
+        ll = torch.as_tensor(log_lik, dtype=torch.float64).to(device).contiguous()
+        rt = torch.as_tensor(route, dtype=torch.int32).to(device).contiguous()
+        if lp.dim() != 2 or ll.dim() != 3 or ll.shape[:2] != lp.shape:
+            raise InvalidConfigError("need log_prior [S, C] and log_lik [S, C, F]")
+        S, Cn, F = ll.shape
+        if rt.numel() != max_size_bytes // group_size_bytes:
+            raise InvalidConfigError("route must have one entry per size group")
+        if S > 0 and (int(rt.min()) < 0 or int(rt.max()) >= S):
+            raise InvalidConfigError("route entries must be valid slots")
+        nbytes = N.lib.gnb_packed_table_bytes(S, Cn, F)
+        if nbytes == 0:
+            raise InvalidConfigError(f"unsupported table shape S={S} C={Cn} F={F}")
+        packed = torch.empty(nbytes // 8, dtype=torch.float64, device=device)
+        N.check(N.lib.gnb_pack_tables(lp.data_ptr(), ll.data_ptr(), S, Cn, F, packed.data_ptr(),
+                                      _stream(stream)), "gnb_pack_tables")
+        return cls(rt, packed, S, Cn, F, group_size_bytes, max_size_bytes)
+
+
+def predict(x: torch.Tensor, size_bytes: torch.Tensor, tables: DeviceTables, *,
+            logpost: bool = True, label_out=None, logpost_out=None, stream=None,
+            generic: bool = False):
+    """Score every row: label[N] int32 (class index, or -1 size out of range,
+    -2 negative count) and, if requested, log-posteriors [N, C] fp64.
+
+    Row n of x holds its routed model's feature counts in FeatureSet order
+    (extra columns beyond the model's features must be 0)."""
+    xp, n, F, ldx = _rows(x)
+    if F != tables.n_features:
+        raise InvalidConfigError(f"x has {F} columns, tables have {tables.n_features} features")
+    sp = _vec(size_bytes, n, "size_bytes")
+    dev = x.device
+    label = label_out if label_out is not None else torch.empty(n, dtype=torch.int32, device=dev)
+    lp = None
+    if logpost:
+        lp = logpost_out if logpost_out is not None else torch.empty(
+            (n, tables.n_classes), dtype=torch.float64, device=dev)
+    fn = N.lib.gnb_predict_generic if generic else N.lib.gnb_predict
+    N.check(fn(xp, n, F, ldx, sp, tables.group_size_bytes, tables.max_size_bytes,
+               tables.route.data_ptr(), tables.n_slots, tables.n_classes,
+               tables.packed.data_ptr(), _vec(label, n, "label_out"),
+               lp.data_ptr() if lp is not None else None, _stream(stream)), "gnb_predict")
+    return label, lp
+
+
+# ---------------------------------------------------------------- fit
+@dataclass
+class FitStats:
+    sums: torch.Tensor      # [G, C, V] fp64 (exact integers)
+    sumsq: torch.Tensor | None
+    counts: torch.Tensor    # [G, C] fp64
+    status: torch.Tensor    # [2] int64: rows with bad label, rows out of size range
+
+    def packed(self) -> torch.Tensor:
+        """One flat fp64 buffer {S | Q | n} for a single all-reduce."""
+        parts = [self.sums.reshape(-1)]
+        if self.sumsq is not None:
+            parts.append(self.sumsq.reshape(-1))
+        parts.append(self.counts.reshape(-1))
+        return torch.cat(parts)
+
+    def unpack_(self, flat: torch.Tensor) -> "FitStats":
+        o = 0
+        for t in (self.sums, self.sumsq, self.counts):
+            if t is None:
+                continue
+            t.copy_(flat[o:o + t.numel()].view_as(t))
+            o += t.numel()
+        return self
+
+
+def fit_stats(x: torch.Tensor, size_bytes: torch.Tensor, labels: torch.Tensor, *,
+              n_classes: int, group_size_bytes: int, max_size_bytes: int, sumsq: bool = True,
+              out: FitStats | None = None, accumulate: bool = False, stream=None) -> FitStats:
+    """Per-(size group, class, column) sums / sums of squares / row counts."""
+    xp, n, V, ldx = _rows(x)
+    if max_size_bytes <= 0 or group_size_bytes <= 0 or max_size_bytes % group_size_bytes:
+        raise InvalidConfigError("group_size_bytes must divide max_size_bytes")
+    G = max_size_bytes // group_size_bytes
+    dev = x.device
+    if out is None:
+        out = FitStats(
+            torch.zeros((G, n_classes, V), dtype=torch.float64, device=dev),
+            torch.zeros((G, n_classes, V), dtype=torch.float64, device=dev) if sumsq else None,
+            torch.zeros((G, n_classes), dtype=torch.float64, device=dev),
+            torch.zeros(2, dtype=torch.int64, device=dev))
+    N.check(N.lib.gnb_fit_stats(
+        xp, n, V, ldx, _vec(size_bytes, n, "size_bytes"), _vec(labels, n, "labels"),
+        group_size_bytes, max_size_bytes, n_classes, out.sums.data_ptr(),
+        out.sumsq.data_ptr() if out.sumsq is not None else None, out.counts.data_ptr(),
+        out.status.data_ptr(), 1 if accumulate else 0, _stream(stream)), "gnb_fit_stats")
+    return out
+
+
+# ---------------------------------------------------------------- finalize (host C++)
+@dataclass
+class FinResult:
+    state: np.ndarray        # [G] 1 trained, 0 untrainable, -1/-2 insufficient class
+    n_features: np.ndarray   # [G]
+    features: np.ndarray     # [G, k] column indices (FeatureSet order)
+    log_prior: np.ndarray    # [G, 2]  (benign, malware)
+    log_lik: np.ndarray      # [G, 2, k]
+
+
+def fin_train(sums, counts, *, k: int, alpha: float, min_per_class: int) -> FinResult:
+    """Feature selection + smoothed log-parameters for every group (C = 2)."""
+    S = np.ascontiguousarray(np.asarray(sums, dtype=np.float64))
+    n = np.ascontiguousarray(np.asarray(counts, dtype=np.float64))
+    if S.ndim != 3 or S.shape[1] != 2 or n.shape != S.shape[:2]:
+        raise InvalidConfigError("fin_train needs sums [G, 2, V] and counts [G, 2]")
+    G, _, V = S.shape
+    res = FinResult(np.zeros(G, np.int32), np.zeros(G, np.int32), np.zeros((G, k), np.int32),
+                    np.zeros((G, 2)), np.zeros((G, 2, k)))
+    ptr = lambda a: a.ctypes.data  # noqa: E731
+    N.check(N.lib.gnb_fin_train(ptr(S), ptr(n), G, V, k, float(alpha), min_per_class,
+                                ptr(res.state), ptr(res.n_features), ptr(res.features),
+                                ptr(res.log_prior), ptr(res.log_lik)), "gnb_fin_train")
+    return res
+
+
+def fin_tables(sums_g, counts_g, features, alpha: float):
+    """train_group for one group with a given feature list; any class count."""
+    S = np.ascontiguousarray(np.asarray(sums_g, dtype=np.float64))
+    n = np.ascontiguousarray(np.asarray(counts_g, dtype=np.float64))
+    f = np.ascontiguousarray(np.asarray(features, dtype=np.int32))
+    Cn, V = S.shape
+    prior = np.zeros(Cn)
+    ll = np.zeros((Cn, len(f)))
+    N.check(N.lib.gnb_fin_tables(S.ctypes.data, n.ctypes.data, Cn, V, f.ctypes.data, len(f),
+                                 float(alpha), prior.ctypes.data, ll.ctypes.data),
+            "gnb_fin_tables")
+    return prior, ll
+
+
+# ---------------------------------------------------------------- synthetic data
+def generate(n_rows: int, n_cols: int, *, n_classes: int = 2, group_rows=None,
+             group_size_bytes: int = 5120, divergence: float = 0.8, seed: int = 0,
+             row_offset: int = 0, ldx: int | None = None, device=None, stream=None):
+    """Synthetic (x [n, V] int32, size [n], label [n]) following the reference law.
+
+    group_rows: rows per size group of the GLOBAL index space (default: all in
+    group 0); rows [row_offset, row_offset + n_rows) are materialised."""
+    device = torch.device(device or "cuda")
+    ld = ldx or (n_cols + 3) // 4 * 4
+    base = torch.empty((n_rows, ld), dtype=torch.int32, device=device)
+    x = base[:, :n_cols]
+    size = torch.empty(n_rows, dtype=torch.int32, device=device)
+    lab = torch.empty(n_rows, dtype=torch.int32, device=device)
+    if group_rows is None:
+        group_rows = [row_offset + n_rows]
+    ends = np.cumsum(np.asarray(group_rows, dtype=np.int64))
+    N.check(N.lib.gnb_generate(base.data_ptr(), n_rows, n_cols, ld, size.data_ptr(),
+                               lab.data_ptr(), row_offset, ends.ctypes.data, len(ends),
+                               group_size_bytes, n_classes, float(divergence), seed,
+                               _stream(stream)), "gnb_generate")
+    return x, size, lab

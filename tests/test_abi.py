@@ -1,0 +1,52 @@
+"""C ABI surface (CPU): the library loads and exports every symbol gnb.h declares;
+argument validation that happens before any CUDA call."""
+
+import ctypes
+
+import numpy as np
+import pytest
+
+from paper_1905_13746_b200 import _native as N
+
+
+def test_every_declared_symbol_is_exported():
+    names = N.declared_symbols()
+    assert len(names) >= 12
+    for name in names:
+        assert hasattr(N.lib, name), name
+
+
+def test_version_and_strerror():
+    assert N.lib.gnb_abi_version() == 1
+    assert N.lib.gnb_strerror(0) == b"ok"
+
+
+@pytest.mark.parametrize("F,ldx,width,limit,S,C", [
+    (0, 4, 10, 10, 1, 2), (4, 3, 10, 10, 1, 2), (4, 4, 0, 10, 1, 2), (4, 4, 3, 10, 1, 2),
+    (4, 4, 10, 10, 0, 2), (4, 4, 10, 10, 1, 1), (4, 4, 10, 10, 1, 17)])
+def test_predict_rejects_bad_geometry(F, ldx, width, limit, S, C):
+    rc = N.lib.gnb_predict(None, 0, F, ldx, None, width, limit, 1, S, C, 1, None, None, 0)
+    assert rc == N.GNB_EINVAL
+    assert N.lib.gnb_last_error()
+
+
+def test_packed_table_bytes():
+    assert N.lib.gnb_packed_table_bytes(1, 2, 32) == 1 * 2 * 8 + 1 * 1 * 32 * 2 * 2 * 8
+    assert N.lib.gnb_packed_table_bytes(0, 2, 32) == 0
+    assert N.lib.gnb_packed_table_bytes(1, 17, 32) == 0
+
+
+def test_fit_rejects_bad_arguments():
+    assert N.lib.gnb_fit_stats(None, 0, 0, 0, None, None, 10, 10, 2, None, None, None, None, 0,
+                               0) == N.GNB_EINVAL
+    assert N.lib.gnb_fit_stats(None, 0, 4, 4, None, None, 10, 10, 1, 1, None, 1, None, 0,
+                               0) == N.GNB_EINVAL
+
+
+def test_check_maps_errors():
+    from paper_1905_13746_b200.errors import InvalidConfigError
+    N.lib.gnb_predict(None, 0, 0, 0, None, 1, 1, 1, 1, 2, 1, None, None, 0)
+    with pytest.raises(InvalidConfigError):
+        N.check(N.GNB_EINVAL, "x")
+    with pytest.raises(N.NativeError):
+        N.check(N.GNB_ECUDA, "x")

@@ -1,0 +1,95 @@
+"""K-FIT parity on the GPU: exact integer statistics vs the oracle."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+from paper_1905_13746_b200 import dense  # noqa: E402
+
+
+def _fit(x, size, label, C, width, limit, ldx=None, sumsq=True):
+    dev = torch.device("cuda")
+    N, V = x.shape
+    ld = ldx or (V + 3) // 4 * 4
+    base = torch.zeros((N, ld), dtype=torch.int32, device=dev)
+    base[:, :V] = torch.from_numpy(x.astype(np.int32)).to(dev)
+    st = dense.fit_stats(base[:, :V], torch.from_numpy(size.astype(np.int32)).to(dev),
+                         torch.from_numpy(label.astype(np.int32)).to(dev), n_classes=C,
+                         group_size_bytes=width, max_size_bytes=limit, sumsq=sumsq)
+    torch.cuda.synchronize()
+    return st
+
+
+def _check(x, size, label, C, width, limit, **kw):
+    st = _fit(x, size, label, C, width, limit, **kw)
+    S, Q, n, bad, oor = O.fit_stats(x, size, label, C, width, limit)
+    assert np.array_equal(st.sums.cpu().numpy(), S.astype(np.float64))
+    if st.sumsq is not None:
+        assert np.array_equal(st.sumsq.cpu().numpy(), Q.astype(np.float64))
+    assert np.array_equal(st.counts.cpu().numpy(), n.astype(np.float64))
+    assert st.status.cpu().tolist() == [bad, oor]
+
+
+def test_golden_training_sets(golden):
+    _, z = golden
+    _check(z["train_x"], z["train_size"], z["train_label"], 2,
+           int(z["group_size_bytes"]), int(z["max_size_bytes"]))
+
+
+@pytest.mark.parametrize("V", [1, 5, 32, 33, 64, 100, 128, 256, 1000])
+def test_vocab_sizes(V):
+    rng = np.random.default_rng(V)
+    N = 3000
+    x = rng.poisson(2.0, size=(N, V))
+    size = rng.integers(0, 5120, size=N)
+    label = rng.integers(0, 2, size=N)
+    _check(x, size, label, 2, 5120, 5120)
+
+
+@pytest.mark.parametrize("C", [2, 3, 16])
+def test_classes_groups_and_bad_rows(C):
+    rng = np.random.default_rng(C)
+    N, V, G = 5000, 128, 7
+    x = rng.poisson(1.0, size=(N, V))
+    size = rng.integers(-100, G * 1000 + 100, size=N)
+    label = rng.integers(-1, C + 1, size=N)
+    _check(x, size, label, C, 1000, G * 1000)
+
+
+def test_many_keys_spill_to_global():
+    """G*C*V larger than shared memory: keys beyond the smem cap use global atomics."""
+    rng = np.random.default_rng(4)
+    N, V, G = 20000, 256, 100
+    x = rng.poisson(0.5, size=(N, V))
+    size = rng.integers(0, 512000, size=N)
+    label = rng.integers(0, 2, size=N)
+    _check(x, size, label, 2, 5120, 512000)
+
+
+def test_large_values_exact():
+    rng = np.random.default_rng(8)
+    x = rng.integers(0, 2**20, size=(4096, 40))
+    _check(x, np.zeros(4096, np.int64), rng.integers(0, 2, size=4096), 2, 1, 1)
+
+
+def test_accumulate_over_chunks_equals_one_pass():
+    rng = np.random.default_rng(12)
+    N, V = 10000, 96
+    x = rng.poisson(1.0, size=(N, V)).astype(np.int32)
+    size = rng.integers(0, 3000, size=N).astype(np.int32)
+    label = rng.integers(0, 2, size=N).astype(np.int32)
+    dev = torch.device("cuda")
+    xd, sd, ld = (torch.from_numpy(a).to(dev) for a in (x, size, label))
+    whole = dense.fit_stats(xd, sd, ld, n_classes=2, group_size_bytes=1000, max_size_bytes=3000)
+    acc = None
+    for lo in range(0, N, 3333):
+        acc = dense.fit_stats(xd[lo:lo + 3333], sd[lo:lo + 3333], ld[lo:lo + 3333], n_classes=2,
+                              group_size_bytes=1000, max_size_bytes=3000, out=acc,
+                              accumulate=acc is not None)
+    torch.cuda.synchronize()
+    assert torch.equal(whole.sums, acc.sums) and torch.equal(whole.counts, acc.counts)
+    assert torch.equal(whole.sumsq, acc.sumsq)

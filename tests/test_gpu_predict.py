@@ -1,0 +1,162 @@
+"""K-PRED parity on the GPU: bit-exact against the oracle (pinned to the reference).
+
+Bar: labels identical, log-posteriors bit-identical (the kernel does the
+reference's mul-then-add in FeatureSet order), statuses identical.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+from paper_1905_13746_b200 import dense  # noqa: E402
+
+
+def _tables(rng, S, C, F, group_count):
+    prior = np.log(rng.dirichlet(np.ones(C), size=S))
+    ll = np.log(rng.dirichlet(np.ones(F), size=(S, C)))
+    route = rng.integers(0, S, size=group_count).astype(np.int32)
+    return prior, ll, route
+
+
+def _run(x, size, prior, ll, route, width, limit, *, generic=False, ldx=None):
+    dev = torch.device("cuda")
+    N, F = x.shape
+    if ldx is None or ldx == F:
+        xd = torch.from_numpy(np.ascontiguousarray(x, dtype=np.int32)).to(dev)
+    else:
+        base = torch.zeros((N, ldx), dtype=torch.int32, device=dev)
+        base[:, :F] = torch.from_numpy(x.astype(np.int32)).to(dev)
+        xd = base[:, :F]
+    t = dense.DeviceTables.build(prior, ll, route, group_size_bytes=width, max_size_bytes=limit)
+    lab, lp = dense.predict(xd, torch.from_numpy(size.astype(np.int32)).to(dev), t,
+                            generic=generic)
+    torch.cuda.synchronize()
+    return lab.cpu().numpy(), lp.cpu().numpy()
+
+
+def _check(x, size, prior, ll, route, width, limit, **kw):
+    lab, lp = _run(x, size, prior, ll, route, width, limit, **kw)
+    want_lab, want_lp = O.predict_dense(x, size, route, prior, ll, width=width, limit=limit)
+    assert lab.tolist() == want_lab.tolist()
+    ok = want_lab >= 0
+    assert lp[ok].tobytes() == want_lp[ok].tobytes()
+    assert np.isnan(lp[~ok]).all()
+
+
+def test_golden_cases_device(golden):
+    name, z = golden
+    width, limit = int(z["group_size_bytes"]), int(z["max_size_bytes"])
+    models = O.train_bundle_dense(z["train_x"], z["train_size"], z["train_label"],
+                                  len(z["vocab"]), width=width, limit=limit,
+                                  min_per_class=int(z["min_per_class"]), k=int(z["k"]),
+                                  alpha=float(z["alpha"]))
+    F = max(len(t.features) for t in models.values())
+    ids, route, prior, ll = O.pack_models(models, limit // width, F)
+    xg = O.gather_rows(z["test_x"].astype(np.int64), z["test_size"], models,
+                       width=width, limit=limit, n_features=F)
+    size = np.clip(z["test_size"], -1, 2**31 - 1)
+    for generic in (False, True):
+        lab, lp = _run(xg, size, prior, ll, route, width, limit, generic=generic)
+        assert lab.tolist() == z["pred_label"].astype(np.int32).tolist()
+        ok = lab >= 0
+        assert lp[ok].tobytes() == z["pred_lp"][ok].tobytes()
+
+
+@pytest.mark.parametrize("F", [1, 4, 31, 32, 33, 50, 100, 128, 200, 256, 500])
+def test_feature_counts(F):
+    rng = np.random.default_rng(F)
+    N = 1000 + F
+    prior, ll, route = _tables(rng, 1, 2, F, 1)
+    x = rng.poisson(2.0, size=(N, F))
+    size = rng.integers(0, 5120, size=N)
+    ldx = (F + 3) // 4 * 4
+    _check(x, size, prior, ll, route, 5120, 5120, ldx=ldx)
+    _check(x, size, prior, ll, route, 5120, 5120, generic=True)
+
+
+@pytest.mark.parametrize("C", [2, 3, 4, 7, 8, 16])
+def test_class_counts(C):
+    rng = np.random.default_rng(100 + C)
+    prior, ll, route = _tables(rng, 3, C, 40, 5)
+    x = rng.poisson(1.5, size=(777, 40))
+    size = rng.integers(-50, 5 * 1000 + 50, size=777)
+    _check(x, size, prior, ll, route, 1000, 5000)
+
+
+def test_ragged_groups_sorted_and_shuffled():
+    rng = np.random.default_rng(7)
+    G, F = 32, 200
+    counts = (4000 * 0.9 ** np.arange(G)).astype(int) + 1
+    prior, ll, _ = _tables(rng, G - 3, 2, F, G)
+    trained = [g for g in range(G) if g not in (5, 8, 17)]
+    route = np.array([trained.index(t) for t in O.route_table(trained, G)], dtype=np.int32)
+    size = np.concatenate([g * 5120 + rng.integers(0, 5120, size=c) for g, c in enumerate(counts)])
+    x = rng.poisson(1.0, size=(len(size), F))
+    _check(x, size, prior, ll, route, 5120, G * 5120)           # grouped: uniform tiles
+    perm = rng.permutation(len(size))
+    _check(x[perm], size[perm], prior, ll, route, 5120, G * 5120)  # mixed tiles
+
+
+def test_edge_rows_and_statuses():
+    rng = np.random.default_rng(9)
+    prior, ll, route = _tables(rng, 2, 2, 64, 4)
+    x = rng.poisson(1.0, size=(300, 64))
+    size = rng.integers(0, 4000, size=300)
+    size[[0, 7, 128, 299]] = [-1, 4000, 2**31 - 1, -2**31]
+    x[5, 3] = -1                      # negative count -> status -2
+    x[200, 63] = 2**31 - 1            # max count: exact product
+    lab, lp = _run(x, size, prior, ll, route, 1000, 4000, ldx=64)
+    want, wlp = O.predict_dense(np.clip(x, 0, None), size, route, prior, ll, width=1000, limit=4000)
+    assert lab[[0, 7, 128, 299]].tolist() == [-1] * 4
+    assert lab[5] == -2
+    keep = np.ones(300, bool)
+    keep[[0, 7, 128, 299, 5]] = False
+    assert lab[keep].tolist() == want[keep].tolist()
+    assert lp[keep].tobytes() == wlp[keep].tobytes()
+
+
+def test_empty_and_tiny():
+    rng = np.random.default_rng(1)
+    prior, ll, route = _tables(rng, 1, 2, 8, 1)
+    for N in (0, 1, 2, 127, 128, 129):
+        x = rng.poisson(3.0, size=(N, 8))
+        size = rng.integers(0, 10, size=N)
+        _check(x, size, prior, ll, route, 10, 10, ldx=8)
+
+
+def test_host_entry_matches_device():
+    """gnb_predict_host (host buffers, chunked H2D pipeline) == device path."""
+    import ctypes
+    from paper_1905_13746_b200 import _native as N
+    rng = np.random.default_rng(3)
+    S, C, F, G = 3, 2, 70, 6
+    prior, ll, route = _tables(rng, S, C, F, G)
+    n = 300_000
+    x = rng.poisson(1.0, size=(n, F)).astype(np.int32)
+    size = rng.integers(0, G * 100, size=n).astype(np.int32)
+    lab = np.empty(n, np.int32)
+    lp = np.empty((n, C))
+    el = ctypes.c_int64()
+    pr, lk = np.ascontiguousarray(prior), np.ascontiguousarray(ll)
+    N.check(N.lib.gnb_predict_host(x.ctypes.data, n, F, F, size.ctypes.data, 100, G * 100,
+                                   route.ctypes.data, S, C, pr.ctypes.data, lk.ctypes.data,
+                                   lab.ctypes.data, lp.ctypes.data, 0, ctypes.addressof(el)))
+    want, wlp = O.predict_dense(x, size, route, prior, ll, width=100, limit=G * 100)
+    assert lab.tolist() == want.tolist()
+    assert lp.tobytes() == wlp.tobytes()
+    assert el.value > 0
+
+
+def test_large_counts_and_values_exact():
+    """x up to 2^31-1 and extreme log-likelihoods keep the product exact."""
+    rng = np.random.default_rng(11)
+    F = 36
+    prior = np.log(np.array([[0.3, 0.7]]))
+    ll = -np.abs(rng.standard_cauchy(size=(1, 2, F))) * 10
+    x = rng.integers(0, 2**31 - 1, size=(257, F))
+    x[::3] = rng.integers(0, 3, size=(86, F))
+    _check(x, np.zeros(257, np.int64), prior, ll, np.zeros(1, np.int32), 1, 1, ldx=36)
