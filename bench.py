@@ -1,0 +1,418 @@
+#!/usr/bin/env python
+"""Benchmark of the group-wise Naive Bayes predict hot path (BASELINE.json metric:
+samples classified/s and achieved HBM GB/s, % of roofline, at 1/2/4/8 B200).
+
+Workload (BASELINE.json configs[3]): 100M samples x 256 opcode features per
+GPU, 2 classes, one size group; one K-PRED launch per step over the whole
+HBM-resident shard (label + both log-posteriors written).  Inputs (102 GB)
+are far larger than L2, so every step streams X from HBM.  Synthetic data
+follows the reference's law (GEN, counter-based, identical under sharding);
+the model is FITTED on that data with K-FIT (+ NCCL all-reduce of the stats
+for N > 1) and FIN, then X is re-materialised in the model's FeatureSet
+order (the predict layout) -- all outside the timed region.
+
+    python bench.py [--gpus N --steps K --warmup W]     # our sm_100a kernels
+    python bench.py --impl reference ...                 # CPU reference arm
+    torchrun --nproc-per-node N bench.py --gpus N ...    # one rank per GPU
+
+Prints ONE JSON line on rank 0.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "samples classified/sec (predict, fused argmax)"
+UNIT = "samples/s"
+DEFAULT_ROWS = 100_000_000
+DEFAULT_F = 256
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--rows", type=int, default=DEFAULT_ROWS, help="samples per GPU (weak scaling)")
+    ap.add_argument("--features", type=int, default=DEFAULT_F)
+    ap.add_argument("--e2e-rows", type=int, default=8_000_000)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-logpost", action="store_true")
+    return ap.parse_args()
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def ncu_traffic():
+    """Per-sample DRAM bytes of K-PRED from the committed ncu --set full capture."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_predict.json")) as fh:
+            d = json.load(fh)
+        return float(d["dram_bytes_per_sample"]), d
+    except Exception:
+        return None, None
+
+
+class ClockSampler:
+    """nvidia-smi sampling DURING the timed region (clocks + throttle reasons)."""
+
+    FIELDS = ("timestamp,clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap,power.draw")
+
+    def __init__(self, device_index: int):
+        self.dev = device_index
+        self.rows = []
+        self.proc = None
+        self.t0 = self.t1 = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append((time.time(), line.strip()))
+
+    def mark(self, begin: bool):
+        if begin:
+            self.t0 = time.time()
+        else:
+            self.t1 = time.time()
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.15)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        inside = [r for t, r in self.rows if self.t0 - 0.06 <= t <= self.t1 + 0.06] or \
+            [r for _, r in self.rows]
+        sm, mx, reasons, power = [], [], set(), []
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for r in inside:
+            parts = [p.strip() for p in r.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx.append(float(parts[2]))
+                power.append(float(parts[7]))
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[3:7]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm),
+                "power_w_median": statistics.median(power) if power else None}
+
+
+# ---------------------------------------------------------------- distributed plumbing
+def dist_init(args):
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1 and not dist.is_initialized():
+        backend = "nccl" if args.impl == "ours" else "gloo"
+        if args.impl == "ours":
+            torch.cuda.set_device(local)
+        dist.init_process_group(backend=backend)
+    return world, rank, local
+
+
+def barrier_max(value: float, world: int, device=None) -> float:
+    if world == 1:
+        return value
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([value], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier_sum(value: float, world: int, device=None) -> float:
+    if world == 1:
+        return value
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([value], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+# ---------------------------------------------------------------- our arm
+def run_ours(args, world, rank, local):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_1905_13746_b200 import _native as N
+    from paper_1905_13746_b200 import dense
+
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    n, V = args.rows, args.features
+    width = 5120
+    offset = rank * n                      # contiguous shard of the global index space
+    group_rows = [world * n]
+
+    # ---- data + model (outside the timed region)
+    x, size, lab = dense.generate(n, V, group_rows=group_rows, divergence=0.8, seed=0,
+                                  row_offset=offset, device=dev)
+    st = dense.fit_stats(x, size, lab, n_classes=2, group_size_bytes=width,
+                         max_size_bytes=width)
+    if world > 1:
+        flat = st.packed()
+        dist.all_reduce(flat)               # NCCL over NVLink: the fit's only exchange
+        st.unpack_(flat)
+    fin = dense.fin_train(st.sums.cpu().numpy(), st.counts.cpu().numpy(), k=V, alpha=1.0,
+                          min_per_class=6)
+    assert fin.state[0] == 1, "synthetic group must be trainable"
+    F = int(fin.n_features[0])
+    feats = fin.features[0, :F].copy()
+    # the same samples gathered into FeatureSet order: the predict input layout
+    dense.generate(n, F, group_rows=group_rows, divergence=0.8, seed=0, row_offset=offset,
+                   col_map=feats, out=(x[:, :F], size, lab), device=dev)
+    xg = x[:, :F]
+    tables = dense.DeviceTables.build(fin.log_prior[:1], fin.log_lik[:1, :, :F],
+                                      np.zeros(1, np.int32), group_size_bytes=width,
+                                      max_size_bytes=width, device=dev)
+    label = torch.empty(n, dtype=torch.int32, device=dev)
+    logpost = None if args.no_logpost else torch.empty((n, 2), dtype=torch.float64, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        dense.predict(xg, size, tables, logpost=logpost is not None, label_out=label,
+                      logpost_out=logpost)
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.mark(True)
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for a, b in evs:
+        a.record(stream)
+        step()
+        b.record(stream)
+    t1.record(stream)
+    torch.cuda.synchronize()
+    clocks.mark(False)
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    total_ms = t0.elapsed_time(t1)
+    launch_ms = [a.elapsed_time(b) for a, b in evs]
+    total_ms = barrier_max(total_ms, world, dev)
+    mean_launch_ms = barrier_max(sum(launch_ms) / len(launch_ms), world, dev)
+    ms_per_step = total_ms / args.steps
+    value = world * n * args.steps / (total_ms / 1e3)
+
+    # ---- correctness spot check of this run (labels vs generator classes)
+    acc = float((label[:1_000_000] == lab[:1_000_000]).float().mean().item())
+
+    # ---- roofline of the dominant (only) kernel
+    out_bytes = 4 + (16 if logpost is not None else 0)
+    bytes_per_sample = 4 * F + 4 + out_bytes
+    achieved = n * bytes_per_sample / (mean_launch_ms / 1e3) / 1e9
+    peak, peak_kind = peaks()
+    tps, ncu = ncu_traffic()
+    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "peak_source": peak_kind,
+                "traffic": round(tps * n) if tps else None,
+                "algorithmic_bytes_per_launch": n * bytes_per_sample,
+                "bytes_per_sample": f"4F+4+{out_bytes} = {bytes_per_sample}",
+                "kernel": "gnb::predict_tma_kernel<2,4,8>"}
+    if ncu:
+        roofline["traffic_source"] = ncu.get("source")
+
+    # ---- end to end through the C ABI with host (pinned) buffers
+    e2e = None
+    if not args.no_e2e:
+        m = min(args.e2e_rows, n)
+        xh = torch.empty((m, F), dtype=torch.int32, pin_memory=True)
+        xh.copy_(xg[:m])
+        sh = torch.empty(m, dtype=torch.int32, pin_memory=True)
+        sh.copy_(size[:m])
+        lh = torch.empty(m, dtype=torch.int32, pin_memory=True)
+        ph = torch.empty((m, 2), dtype=torch.float64, pin_memory=True)
+        prior = np.ascontiguousarray(fin.log_prior[:1])
+        lik = np.ascontiguousarray(fin.log_lik[:1, :, :F])
+        route = np.zeros(1, np.int32)
+        el = ctypes.c_int64()
+
+        def e2e_step():
+            N.check(N.lib.gnb_predict_host(
+                xh.data_ptr(), m, F, F, sh.data_ptr(), width, width, route.ctypes.data, 1, 2,
+                prior.ctypes.data, lik.ctypes.data, lh.data_ptr(), ph.data_ptr(), local,
+                ctypes.addressof(el)), "gnb_predict_host")
+
+        e2e_step()
+        if world > 1:
+            dist.barrier()
+        t = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            e2e_step()
+        dt = barrier_max(time.perf_counter() - t, world, dev)
+        ok = bool(torch.equal(lh, label[:m].cpu()))
+        e2e = {"value": round(world * m * args.e2e_steps / dt, 1), "unit": UNIT,
+               "h2d_bytes_per_step": m * (4 * F + 4), "d2h_bytes_per_step": m * (4 + 16),
+               "rows_per_step_per_gpu": m, "api": "gnb_predict_host (C ABI, pinned host buffers)",
+               "matches_device_labels": ok}
+        del xh, sh, lh, ph
+
+    # ---- CPU baseline: C oracle on the box's host cores (rank 0, N=1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline_from(xg, size, fin, F, width, args.cpu_seconds)
+
+    return {
+        "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": round(ms_per_step, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (reference synth law, GEN kernel, seed 0); model fitted on it",
+        "config": {"workload": "cfg4: predict 100M samples x 256 features per GPU, 2 classes, "
+                               "1 size group" if (n == DEFAULT_ROWS and V == DEFAULT_F)
+                   else f"predict {n} samples x {V} features per GPU, 2 classes",
+                   "rows_per_gpu": n, "features": F, "classes": 2, "x_dtype": "int32",
+                   "outputs": "label int32 + log-posterior fp64 x2" if logpost is not None
+                   else "label int32", "parity": "bit-exact vs reference (exact mode)",
+                   "l2": "inputs (%.1f GB/GPU) >> 126 MB L2; no flush needed" % (n * 4 * F / 1e9),
+                   "parallelism": f"dp{world} (row shards, no predict collective)"},
+        "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+        "gpu_launches": args.steps * world, "clocks": clk,
+        "accuracy_vs_generator_labels": round(acc, 4),
+        "mean_launch_ms": round(mean_launch_ms, 4),
+    }
+
+
+def cpu_baseline_from(xg, size, fin, F, width, seconds):
+    """C oracle (reference algorithm, exact) on a bounded sample of the same rows."""
+    import numpy as np
+    from oracle import oracle as O
+    sample = min(2_000_000, xg.shape[0])
+    xs = xg[:sample].cpu().numpy()
+    ss = size[:sample].cpu().numpy()
+    threads = os.cpu_count() or 1
+    prior, lik = fin.log_prior[:1], fin.log_lik[:1, :, :F]
+    route = np.zeros(1, np.int32)
+    done, t = 0, time.perf_counter()
+    while True:
+        O.c_predict(xs, ss, route, prior, lik, width=width, limit=width, threads=threads)
+        done += sample
+        if time.perf_counter() - t >= seconds:
+            break
+    dt = time.perf_counter() - t
+    return {"value": round(done / dt, 1), "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"{sample} rows of this workload, {done // sample} passes in {dt:.1f}s",
+            "impl": "oracle/gnb_oracle.c (exact mul-then-add, pthreads)"}
+
+
+# ---------------------------------------------------------------- reference arm
+def run_reference(args, world, rank):
+    """The reference algorithm on the box's host cores (oracle port: the reference
+    is pure Python and cannot be compiled)."""
+    import numpy as np
+    from oracle import oracle as O
+    if rank != 0:
+        return None
+    V = args.features
+    sample = 2_000_000
+    x, size, label = O.synth_dense(sample, V, seed=0, divergence=0.8)
+    S, _, n, _, _ = O.fit_stats(x, size, label, 2, 5120, 5120)
+    feats, _ = O.select_features(S[0], V, 0)
+    t = O.train_tables(S[0], n[0], feats, 1.0, 0)
+    xg = np.ascontiguousarray(x[:, feats])
+    route = np.zeros(1, np.int32)
+    threads = os.cpu_count() or 1
+
+    def step():
+        O.c_predict(xg, size, route, t.log_prior[None], t.log_lik[None], width=5120,
+                    limit=5120, threads=threads)
+
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    dt = time.perf_counter() - t0
+    value = sample * args.steps / dt
+    return {
+        "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(dt / args.steps * 1e3, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "impl": "reference",
+        "data": "synthetic (reference synth law, numpy)",
+        "config": {"workload": "cfg4: predict 100M samples x 256 features per GPU, 2 classes, "
+                               "1 size group (CPU: bounded sample per step)",
+                   "rows_per_step": sample, "features": V, "classes": 2},
+        "cpu_baseline": {"value": round(value, 1), "unit": UNIT, "cores": threads,
+                         "kind": "port", "sample": f"{sample} rows per step",
+                         "impl": "oracle/gnb_oracle.c"},
+        "e2e": {"value": round(value, 1), "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    args = parse()
+    world, rank, local = dist_init(args)
+    if args.impl == "reference":
+        out = run_reference(args, world, rank)
+    else:
+        out = run_ours(args, world, rank, local)
+    if rank == 0 and out is not None:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -158,11 +158,15 @@ int gnb_fin_tables(const double* sums_g, const double* counts_g, int32_t n_class
  * range, T = 64 + size/64 draws, and per-column counts ~ Poisson(T * p_c[v])
  * with p_c from class_distributions (weight 1 on the class's block, 1-d
  * elsewhere).  Counter-based: row r's values depend only on (seed, r), so any
- * sharding of the global index space yields the same data. n_groups <= 128. */
+ * sharding of the global index space yields the same data. n_groups <= 128.
+ * col_map (device, nullable, [n_cols]): output column j holds the counts of
+ * vocabulary column col_map[j] of a vocab_cols-wide vocabulary -- the same
+ * samples gathered into a model's FeatureSet order (predict layout). */
 int gnb_generate(int32_t* x, int64_t n_rows, int32_t n_cols, int64_t ldx, int32_t* size_bytes,
                  int32_t* labels, int64_t row_offset, const int64_t* group_row_end,
                  int32_t n_groups, int32_t group_size_bytes, int32_t n_classes,
-                 double divergence, uint64_t seed, uintptr_t stream);
+                 double divergence, uint64_t seed, const int32_t* col_map,
+                 int32_t vocab_cols, uintptr_t stream);
 
 #ifdef __cplusplus
 }

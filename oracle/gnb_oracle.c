@@ -30,32 +30,67 @@ typedef struct {
 } pred_job;
 
 /* log_posterior + predict + _classify_slice (classifier.py:132-158,
- * engine.py:187-206) for rows [lo, hi). */
+ * engine.py:187-206) for rows [lo, hi).  Four rows are scored together so
+ * 4*C independent accumulator chains overlap (each chain is still the
+ * reference's exact sequence of multiply-then-add in feature order). */
+static void finish_row(const pred_job* j, int64_t r, const double* acc) {
+  int best = 0;
+  for (int c = 1; c < j->C; ++c)
+    if (acc[c] > acc[best]) best = c; /* strict: ties -> lowest index (benign) */
+  j->label[r] = best;
+  if (j->logpost)
+    for (int c = 0; c < j->C; ++c) j->logpost[r * j->C + c] = acc[c];
+}
+
 static void* predict_rows(void* arg) {
   const pred_job* j = (const pred_job*)arg;
-  double acc[16];
-  for (int64_t r = j->lo; r < j->hi; ++r) {
-    const int32_t sz = j->size[r];
-    if (sz < 0 || sz >= j->limit) {
-      j->label[r] = -1;
-      if (j->logpost)
-        for (int c = 0; c < j->C; ++c) j->logpost[r * j->C + c] = __builtin_nan("");
-      continue;
+  const int C = j->C, F = j->F;
+  int64_t r = j->lo;
+  while (r < j->hi) {
+    /* gather up to 4 in-range rows that share a slot */
+    int64_t rows[4];
+    int nr = 0, s = -1;
+    while (r < j->hi && nr < 4) {
+      const int32_t sz = j->size[r];
+      if (sz < 0 || sz >= j->limit) {
+        j->label[r] = -1;
+        if (j->logpost)
+          for (int c = 0; c < C; ++c) j->logpost[r * C + c] = __builtin_nan("");
+        ++r;
+        continue;
+      }
+      const int rs = j->route[sz / j->width];
+      if (nr > 0 && rs != s) break;
+      s = rs;
+      rows[nr++] = r++;
     }
-    const int s = j->route[sz / j->width];
-    const int32_t* row = j->x + r * j->ldx;
-    for (int c = 0; c < j->C; ++c) {
-      const double* ll = j->ll + ((int64_t)s * j->C + c) * j->F;
-      double a = j->prior[s * j->C + c];
-      for (int f = 0; f < j->F; ++f) a = a + (double)row[f] * ll[f];
-      acc[c] = a;
+    if (nr == 0) continue;
+    double acc[4][16];
+    const int32_t* xr[4];
+    for (int i = 0; i < nr; ++i) {
+      xr[i] = j->x + rows[i] * j->ldx;
+      for (int c = 0; c < C; ++c) acc[i][c] = j->prior[s * C + c];
     }
-    int best = 0;
-    for (int c = 1; c < j->C; ++c)
-      if (acc[c] > acc[best]) best = c; /* strict: ties -> lowest index (benign) */
-    j->label[r] = best;
-    if (j->logpost)
-      for (int c = 0; c < j->C; ++c) j->logpost[r * j->C + c] = acc[c];
+    const double* ll = j->ll + (int64_t)s * C * F;
+    if (nr == 4) {
+      for (int f = 0; f < F; ++f) {
+        const double x0 = xr[0][f], x1 = xr[1][f], x2 = xr[2][f], x3 = xr[3][f];
+        for (int c = 0; c < C; ++c) {
+          const double w = ll[(int64_t)c * F + f];
+          acc[0][c] = acc[0][c] + x0 * w;
+          acc[1][c] = acc[1][c] + x1 * w;
+          acc[2][c] = acc[2][c] + x2 * w;
+          acc[3][c] = acc[3][c] + x3 * w;
+        }
+      }
+    } else {
+      for (int i = 0; i < nr; ++i)
+        for (int f = 0; f < F; ++f) {
+          const double x = xr[i][f];
+          for (int c = 0; c < C; ++c) acc[i][c] = acc[i][c] + x * ll[(int64_t)c * F + f];
+        }
+    }
+    for (int i = 0; i < nr; ++i) finish_row(j, rows[i], acc[i]);
   }
   return NULL;
 }

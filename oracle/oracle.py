@@ -74,8 +74,10 @@ def fit_stats(x, size, label, n_classes: int, width: int, limit: int):
     xs = x[good]
     S = np.zeros((keys, x.shape[1]), dtype=np.int64)
     Q = np.zeros((keys, x.shape[1]), dtype=np.int64)
-    np.add.at(S, key, xs)
-    np.add.at(Q, key, xs * xs)
+    for k in np.unique(key):
+        rows = xs[key == k]
+        S[k] = rows.sum(0)
+        Q[k] = (rows * rows).sum(0)
     n = np.bincount(key, minlength=keys).astype(np.int64)
     shape = (n_groups, n_classes, x.shape[1])
     return (S.reshape(shape), Q.reshape(shape), n.reshape(n_groups, n_classes),
@@ -276,3 +278,24 @@ def c_fit_stats(x, size, label, n_classes: int, width: int, limit: int):
                                 width, limit, n_classes, S.ctypes.data, Q.ctypes.data,
                                 cnt.ctypes.data, status.ctypes.data)
     return S, Q, cnt, int(status[0]), int(status[1])
+
+
+# ---------------------------------------------------------------- synthetic (CPU)
+def synth_dense(n: int, V: int, *, seed: int = 0, divergence: float = 0.8, width: int = 5120,
+                n_classes: int = 2):
+    """The reference's synthetic law (synth.py:64-116) as dense numpy arrays,
+    one size group, per-cell Poisson counts (the multinomial's cell limit).
+    Used by the CPU reference arm, which may not touch the GPU generator."""
+    rng = np.random.default_rng(seed)
+    label = (np.arange(n) % n_classes).astype(np.int32)
+    size = rng.integers(0, width, size=n).astype(np.int32)
+    draws = 64 + size // 64
+    low = 1.0 - divergence
+    bounds = [-(-b * V // n_classes) for b in range(n_classes + 1)]
+    w = np.full((n_classes, V), low)
+    for c in range(n_classes):
+        b = n_classes - 1 - c
+        w[c, bounds[b]:bounds[b + 1]] = 1.0
+    p = w / w.sum(1, keepdims=True)
+    x = rng.poisson(draws[:, None] * p[label]).astype(np.int32)
+    return x, size, label

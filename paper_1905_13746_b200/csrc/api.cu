@@ -263,8 +263,11 @@ int gnb_fit_stats(const int32_t* x, int64_t n_rows, int32_t n_cols, int64_t ldx,
 int gnb_generate(int32_t* x, int64_t n_rows, int32_t n_cols, int64_t ldx, int32_t* size_bytes,
                  int32_t* labels, int64_t row_offset, const int64_t* group_row_end,
                  int32_t n_groups, int32_t group_size_bytes, int32_t n_classes,
-                 double divergence, uint64_t seed, uintptr_t stream) {
+                 double divergence, uint64_t seed, const int32_t* col_map,
+                 int32_t vocab_cols, uintptr_t stream) {
+  if (col_map == nullptr) vocab_cols = n_cols;
   if (n_rows < 0 || n_cols < 1 || ldx < n_cols || n_groups < 1 || n_groups > 128 ||
+      vocab_cols < 1 ||
       group_size_bytes < 1 || n_classes < 2 || n_classes > GNB_MAX_CLASSES ||
       !(divergence >= 0.0 && divergence <= 1.0))
     return fail(GNB_EINVAL, "generate: bad arguments");
@@ -283,6 +286,8 @@ int gnb_generate(int32_t* x, int64_t n_rows, int32_t n_cols, int64_t ldx, int32_
   p.n_classes = n_classes;
   p.divergence = divergence;
   p.seed = seed;
+  p.col_map = col_map;
+  p.vocab_cols = vocab_cols;
   for (int g = 0; g < n_groups; ++g) p.group_end[g] = group_row_end[g];
   GNB_CUDA(generate_launch(p, reinterpret_cast<cudaStream_t>(stream)), "generate launch");
   return GNB_OK;

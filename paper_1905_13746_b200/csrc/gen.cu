@@ -36,20 +36,21 @@ __device__ __forceinline__ int block_lo(int b, int V, int C) {
 }
 
 __global__ void generate_kernel(const GenParams p) {
-  const int V = p.n_cols, C = p.n_classes;
-  const int64_t total = p.n_rows * static_cast<int64_t>(V);
+  const int NC = p.n_cols, V = p.vocab_cols, C = p.n_classes;
+  const int64_t total = p.n_rows * static_cast<int64_t>(NC);
   const double low = 1.0 - p.divergence;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t r = i / V;
-    const int v = static_cast<int>(i - r * V);
+    const int64_t r = i / NC;
+    const int j = static_cast<int>(i - r * NC);
+    const int v = p.col_map ? __ldg(p.col_map + j) : j;  // vocabulary column
     const long long R = p.row_offset + r;
     int g = 0;
     while (g < p.n_groups - 1 && R >= p.group_end[g]) ++g;
     const int c = static_cast<int>(R % C);
     const unsigned long long hr = mix64(p.seed ^ mix64(static_cast<unsigned long long>(R)));
     const int size = g * p.width + static_cast<int>(unit(hr) * p.width);
-    if (v == 0) {
+    if (j == 0) {
       p.size[r] = size;
       p.labels[r] = c;
     }
@@ -76,7 +77,7 @@ __global__ void generate_kernel(const GenParams p) {
       const double z = sqrt(-2.0 * log(u > 0.0 ? u : 0x1p-53)) * cospi(2.0 * u2);
       k = static_cast<int>(fmax(0.0, rint(lam + sqrt(lam) * z)));
     }
-    p.x[r * p.ldx + v] = k;
+    p.x[r * p.ldx + j] = k;
   }
 }
 

@@ -69,6 +69,8 @@ struct GenParams {
   int32_t n_classes;
   double divergence;
   unsigned long long seed;
+  const int32_t* col_map;  // nullable: output column -> vocabulary column
+  int32_t vocab_cols;
   long long group_end[128];
 };
 cudaError_t generate_launch(const GenParams& p, cudaStream_t stream);

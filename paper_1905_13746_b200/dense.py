@@ -37,7 +37,7 @@ def _dev(t: torch.Tensor, name: str, dtype) -> int:
 
 def _rows(x: torch.Tensor, name: str = "x"):
     ptr = _dev(x, name, torch.int32)
-    if x.dim() != 2 or x.stride(1) != 1:
+    if x.dim() != 2 or (x.numel() > 0 and x.shape[1] > 1 and x.stride(1) != 1):
         raise InvalidConfigError(f"{name} must be a row-major [N, F] int32 matrix")
     return ptr, x.shape[0], x.shape[1], max(x.stride(0), x.shape[1])
 
@@ -208,22 +208,38 @@ def fin_tables(sums_g, counts_g, features, alpha: float):
 # ---------------------------------------------------------------- synthetic data
 def generate(n_rows: int, n_cols: int, *, n_classes: int = 2, group_rows=None,
              group_size_bytes: int = 5120, divergence: float = 0.8, seed: int = 0,
-             row_offset: int = 0, ldx: int | None = None, device=None, stream=None):
+             row_offset: int = 0, ldx: int | None = None, col_map=None, out=None,
+             device=None, stream=None):
     """Synthetic (x [n, V] int32, size [n], label [n]) following the reference law.
 
     group_rows: rows per size group of the GLOBAL index space (default: all in
-    group 0); rows [row_offset, row_offset + n_rows) are materialised."""
+    group 0); rows [row_offset, row_offset + n_rows) are materialised.
+    col_map: output column j holds vocabulary column col_map[j] (vocabulary of
+    `vocab_cols` = max(col_map)+1 columns) -- i.e. the same samples gathered
+    into a FeatureSet order.  out: reuse (x, size, label) buffers."""
     device = torch.device(device or "cuda")
-    ld = ldx or (n_cols + 3) // 4 * 4
-    base = torch.empty((n_rows, ld), dtype=torch.int32, device=device)
-    x = base[:, :n_cols]
-    size = torch.empty(n_rows, dtype=torch.int32, device=device)
-    lab = torch.empty(n_rows, dtype=torch.int32, device=device)
+    if out is not None:
+        x, size, lab = out
+        ld = max(x.stride(0), x.shape[1])
+    else:
+        ld = ldx or (n_cols + 3) // 4 * 4
+        x = torch.empty((n_rows, ld), dtype=torch.int32, device=device)[:, :n_cols]
+        size = torch.empty(n_rows, dtype=torch.int32, device=device)
+        lab = torch.empty(n_rows, dtype=torch.int32, device=device)
+    cmap = None
+    vocab_cols = n_cols
+    if col_map is not None:
+        cm = np.asarray(col_map, dtype=np.int32)
+        if cm.shape != (n_cols,) or cm.min() < 0:
+            raise InvalidConfigError("col_map must give one vocabulary column per output column")
+        vocab_cols = int(cm.max()) + 1
+        cmap = torch.from_numpy(cm).to(device)
     if group_rows is None:
         group_rows = [row_offset + n_rows]
     ends = np.cumsum(np.asarray(group_rows, dtype=np.int64))
-    N.check(N.lib.gnb_generate(base.data_ptr(), n_rows, n_cols, ld, size.data_ptr(),
+    N.check(N.lib.gnb_generate(x.data_ptr(), n_rows, n_cols, ld, size.data_ptr(),
                                lab.data_ptr(), row_offset, ends.ctypes.data, len(ends),
                                group_size_bytes, n_classes, float(divergence), seed,
+                               cmap.data_ptr() if cmap is not None else None, vocab_cols,
                                _stream(stream)), "gnb_generate")
     return x, size, lab
