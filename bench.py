@@ -268,7 +268,7 @@ def run_ours(args, world, rank, local):
                 "traffic": round(tps * n) if tps else None,
                 "algorithmic_bytes_per_launch": n * bytes_per_sample,
                 "bytes_per_sample": f"4F+4+{out_bytes} = {bytes_per_sample}",
-                "kernel": "gnb::predict_tma_kernel<2,4,8>"}
+                "kernel": "gnb::predict_tma_kernel<2,1,4,2>"}
     if ncu:
         roofline["traffic_source"] = ncu.get("source")
 

@@ -4,6 +4,7 @@
 #include <chrono>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -49,6 +50,20 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
+// L2 sector promotion of the X boxes (GNB_L2_PROMO=0..3 = none/64/128/256 B, for
+// profiling).  Default 256 B: measured best with evict_normal X loads
+// (profiles/r01_tuning.md): the promoted neighbour sector is the same row's
+// next 32-column chunk, which the next stage of the same CTA reads.
+CUtensorMapL2promotion l2_promotion() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("GNB_L2_PROMO");
+    v = e ? atoi(e) : 3;
+    if (v < 0 || v > 3) v = 3;
+  }
+  return static_cast<CUtensorMapL2promotion>(v);
+}
+
 bool tma_ok(const void* base, int64_t ldx) {
   return (reinterpret_cast<uintptr_t>(base) & 15u) == 0 && (ldx % 4) == 0;
 }
@@ -71,7 +86,7 @@ static bool encode_map(CUtensorMap* map, const void* base, int64_t n_rows, int32
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_INT32, 2, const_cast<void*>(base), dims, strides,
                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                   swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
-                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                  l2_promotion(), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
 
@@ -163,7 +178,7 @@ static int predict_device(const int32_t* x, int64_t n_rows, int32_t F, int64_t l
     CUtensorMap map;
     const CUtensorMap* mp = nullptr;
     if (use_tma) {
-      if (!encode_map(&map, p.x, n, F, ldx, 128, true))
+      if (!encode_map(&map, p.x, n, F, ldx, predict_box_rows(C), true))
         return fail(GNB_ECUDA, "predict: cuTensorMapEncodeTiled failed");
       mp = &map;
     }

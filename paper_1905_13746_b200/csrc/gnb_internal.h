@@ -27,6 +27,7 @@ struct PredictParams {
   int32_t* label;
   double* logpost;  // nullable, [N][C]
   int64_t n_tiles;  // set by predict_launch
+  int32_t x_policy; // 0 evict_normal (default), 1 evict_first
 };
 
 struct FitParams {
@@ -52,6 +53,7 @@ size_t packed_bytes(int n_slots, int n_classes, int n_features);
 cudaError_t pack_tables(const double* log_prior, const double* log_lik, int S, int C, int F,
                         void* packed, cudaStream_t stream);
 // map == nullptr (or force_generic) selects the L1 path that accepts any ldx.
+int predict_box_rows(int n_classes);  // TMA box height of the K-PRED variant
 cudaError_t predict_launch(const CUtensorMap* map, PredictParams p, cudaStream_t stream,
                            int force_generic);
 cudaError_t fit_launch(const CUtensorMap& map, FitParams p, cudaStream_t stream);

@@ -24,6 +24,7 @@
 #include <cfloat>
 #include <climits>
 #include <cstdint>
+#include <cstdlib>
 
 #include "gnb_device.cuh"
 #include "gnb_internal.h"
@@ -143,9 +144,12 @@ __device__ __forceinline__ void write_row(const PredictParams& p, int64_t r, int
 }
 
 // ------------------------------------------------------------------ TMA kernel
-template <int CP, int NW, int STAGES>
+// A consumer thread owns R rows of the tile (rows lane + 32*(w + NW*i)), so one
+// broadcast table read feeds R*CP independent accumulator chains and the
+// DADD latency of each chain is hidden behind the others.
+template <int CP, int R, int NW, int STAGES>
 struct PredictSmem {
-  static constexpr int kRows = NW * 32;
+  static constexpr int kRows = NW * 32 * R;                      // rows per tile (<= 256)
   static constexpr int kXBytes = kRows * kChunkBytesPerRow;        // one box
   static constexpr int kTabBytes = kChunkCols * CP * 2 * 8;         // one table slice
   static constexpr int kHdrBytes = ((4 + kRows * 4) + 15) / 16 * 16;
@@ -155,6 +159,7 @@ struct PredictSmem {
   static constexpr int kBar = kHdr + STAGES * kHdrBytes;
   static constexpr int kTotal = kBar + 2 * STAGES * 8;
   static constexpr int kAlloc = kTotal + 1024;  // slack for 1024-B alignment
+  static_assert(kRows <= 256, "TMA box rows <= 256");
 };
 
 struct StageHdr {
@@ -162,10 +167,64 @@ struct StageHdr {
   int row_slot[1];
 };
 
-template <int CP, int NW, int STAGES>
+// Uniform tile: the chunk's table slice is in smem and shared by all R rows.
+template <int CP, int R>
+__device__ __forceinline__ void score_chunk_uniform(double (&acc)[R][CP], const uint8_t* box,
+                                                    const uint32_t (&rows)[R], const double* tab,
+                                                    int nq, uint32_t (&neg)[R]) {
+  auto quad = [&](int q) {
+    uint4 v[R];
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      v[i] = *reinterpret_cast<const uint4*>(box + swz128(rows[i], q));
+      neg[i] |= v[i].x | v[i].y | v[i].z | v[i].w;
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      double2 t[CP];
+#pragma unroll
+      for (int c = 0; c < CP; ++c)
+        t[c] = *reinterpret_cast<const double2*>(tab + 2 * ((4 * q + e) * CP + c));
+#pragma unroll
+      for (int i = 0; i < R; ++i) {
+        const uint32_t x = e == 0 ? v[i].x : e == 1 ? v[i].y : e == 2 ? v[i].z : v[i].w;
+#pragma unroll
+        for (int c = 0; c < CP; ++c) acc[i][c] = __dadd_rn(acc[i][c], exact_product(x, t[c].x, t[c].y));
+      }
+    }
+  };
+  if (nq == 8) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) quad(q);
+  } else {
+#pragma unroll 1
+    for (int q = 0; q < nq; ++q) quad(q);
+  }
+}
+
+// Mixed tile: every row reads its own slot's table through L1.
+template <int CP, int R>
+__device__ __forceinline__ void score_chunk_mixed(double (&acc)[R][CP], const uint8_t* box,
+                                                  const uint32_t (&rows)[R], const int (&slot)[R],
+                                                  const double* tab_all, int NCH, int ch, int nq,
+                                                  uint32_t (&neg)[R]) {
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    const GlobalTab<CP> tab{tab_all + (static_cast<int64_t>(max(slot[i], 0)) * NCH + ch) *
+                                          (kChunkCols * CP * 2)};
+    double a[CP];
+#pragma unroll
+    for (int c = 0; c < CP; ++c) a[c] = acc[i][c];
+    score_chunk<CP>(a, box, rows[i], tab, nq, neg[i]);
+#pragma unroll
+    for (int c = 0; c < CP; ++c) acc[i][c] = a[c];
+  }
+}
+
+template <int CP, int R, int NW, int STAGES>
 __global__ void __launch_bounds__((NW + 1) * 32)
     predict_tma_kernel(const __grid_constant__ CUtensorMap xmap, const PredictParams p) {
-  using L = PredictSmem<CP, NW, STAGES>;
+  using L = PredictSmem<CP, R, NW, STAGES>;
   constexpr int ROWS = L::kRows;
   extern __shared__ uint8_t smem_raw[];
   // 1024-B alignment for SWIZZLE_128B, keeping the pointer in the shared window
@@ -189,7 +248,7 @@ __global__ void __launch_bounds__((NW + 1) * 32)
 
   if (warp == NW) {
     // ---------------------------------------------------------- producer
-    const uint64_t pol_x = policy_evict_first();
+    const uint64_t pol_x = p.x_policy == 1 ? policy_evict_first() : policy_evict_normal();
     const uint64_t pol_t = policy_evict_last();
     int stage = 0;
     uint32_t phase = 0;
@@ -245,36 +304,40 @@ __global__ void __launch_bounds__((NW + 1) * 32)
     }
   } else {
     // ---------------------------------------------------------- consumers
-    const uint32_t t = threadIdx.x;  // row within the tile
+    uint32_t rows[R];
+#pragma unroll
+    for (int i = 0; i < R; ++i) rows[i] = lane + 32 * (warp + NW * i);
     int stage = 0;
     uint32_t phase = 0;
     for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-      const int64_t r = tile * ROWS + t;
-      double acc[CP];
-      int slot = -1;
-      uint32_t neg = 0;
+      double acc[R][CP];
+      int slot[R];
+      uint32_t neg[R];
+#pragma unroll
+      for (int i = 0; i < R; ++i) neg[i] = 0;
       for (int ch = 0; ch < NCH; ++ch) {
         mbar_wait(&full[stage], phase);
         const StageHdr* hdr =
             reinterpret_cast<const StageHdr*>(smem + L::kHdr + stage * L::kHdrBytes);
         const int ts = hdr->tile_slot;
         if (ch == 0) {
-          slot = hdr->row_slot[t];
-          const int s = ts >= 0 ? ts : max(slot, 0);
 #pragma unroll
-          for (int c = 0; c < CP; ++c) acc[c] = __ldg(p.prior + s * CP + c);
+          for (int i = 0; i < R; ++i) {
+            slot[i] = hdr->row_slot[rows[i]];
+            const int s = ts >= 0 ? ts : max(slot[i], 0);
+#pragma unroll
+            for (int c = 0; c < CP; ++c) acc[i][c] = __ldg(p.prior + s * CP + c);
+          }
         }
         const int nf = min(kChunkCols, p.n_features - ch * kChunkCols);
         const int nq = (nf + 3) >> 2;
         const uint8_t* box = smem + L::kX + stage * L::kXBytes;
         if (ts >= 0) {
-          const SmemTab<CP> tab{
-              reinterpret_cast<const double*>(smem + L::kTab + stage * L::kTabBytes)};
-          score_chunk<CP>(acc, box, t, tab, nq, neg);
+          score_chunk_uniform<CP, R>(
+              acc, box, rows, reinterpret_cast<const double*>(smem + L::kTab + stage * L::kTabBytes),
+              nq, neg);
         } else {
-          const GlobalTab<CP> tab{
-              p.tab + (static_cast<int64_t>(max(slot, 0)) * NCH + ch) * (kChunkCols * CP * 2)};
-          score_chunk<CP>(acc, box, t, tab, nq, neg);
+          score_chunk_mixed<CP, R>(acc, box, rows, slot, p.tab, NCH, ch, nq, neg);
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[stage]);
@@ -283,7 +346,11 @@ __global__ void __launch_bounds__((NW + 1) * 32)
           phase ^= 1;
         }
       }
-      if (r < p.n_rows) write_row<CP>(p, r, slot, neg, acc);
+#pragma unroll
+      for (int i = 0; i < R; ++i) {
+        const int64_t r = tile * ROWS + rows[i];
+        if (r < p.n_rows) write_row<CP>(p, r, slot[i], neg[i], acc[i]);
+      }
     }
   }
 }
@@ -321,11 +388,11 @@ __global__ void __launch_bounds__(256) predict_generic_kernel(const PredictParam
 }
 
 // ------------------------------------------------------------------ launchers
-template <int CP, int NW, int STAGES>
-static cudaError_t launch_tma(const CUtensorMap& map, const PredictParams& p,
-                              cudaStream_t stream) {
-  using L = PredictSmem<CP, NW, STAGES>;
-  auto kern = predict_tma_kernel<CP, NW, STAGES>;
+template <int CP, int R, int NW, int STAGES>
+static cudaError_t launch_tma(const CUtensorMap& map, PredictParams p, cudaStream_t stream) {
+  using L = PredictSmem<CP, R, NW, STAGES>;
+  auto kern = predict_tma_kernel<CP, R, NW, STAGES>;
+  p.n_tiles = (p.n_rows + L::kRows - 1) / L::kRows;
   static int per_sm = 0;  // resident CTAs per SM for this instantiation
   static int sms = 0;
   if (per_sm == 0) {
@@ -377,20 +444,59 @@ cudaError_t pack_tables(const double* log_prior, const double* log_lik, int S, i
   return cudaGetLastError();
 }
 
+// K-PRED geometry per class pad: rows per thread (R), consumer warps (NW),
+// ring stages.  CP=2 keeps a few tuned variants selectable with
+// GNB_PRED_VARIANT (profiling only); the default is variant 0, measured best
+// on B200 (profiles/r01_tuning.md): 16-KB stages, 2 deep, 6 CTAs per SM.
+struct PredVariant {
+  int R, NW, STAGES;
+};
+static const PredVariant kCp2Variants[] = {
+    {1, 4, 2}, {1, 4, 3}, {2, 2, 2}, {2, 4, 2}};
+
+static int cp2_variant() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("GNB_PRED_VARIANT");
+    v = e ? atoi(e) : 0;
+    if (v < 0 || v >= static_cast<int>(sizeof(kCp2Variants) / sizeof(kCp2Variants[0]))) v = 0;
+  }
+  return v;
+}
+
+int predict_box_rows(int n_classes) {
+  const int CP = class_pad(n_classes);
+  if (CP == 2) {
+    const PredVariant& v = kCp2Variants[cp2_variant()];
+    return v.R * v.NW * 32;
+  }
+  return CP == 4 ? 2 * 4 * 32 : 128;
+}
+
 cudaError_t predict_launch(const CUtensorMap* map, PredictParams p, cudaStream_t stream,
                            int force_generic) {
   const int CP = class_pad(p.n_classes);
   p.n_chunks = (p.n_features + kChunkCols - 1) / kChunkCols;
+  static int x_policy = -1;  // GNB_X_POLICY=1: X loads evict_first (profiling; default normal)
+  if (x_policy < 0) {
+    const char* e = getenv("GNB_X_POLICY");
+    x_policy = e ? atoi(e) : 0;
+  }
+  p.x_policy = x_policy;
   const double* prior = p.prior;
   p.tab = prior + static_cast<int64_t>(p.n_slots) * CP;
   if (map != nullptr && !force_generic) {
-    constexpr int NW = 4;
-    p.n_tiles = (p.n_rows + NW * 32 - 1) / (NW * 32);
     switch (CP) {
-      case 2: return launch_tma<2, NW, 8>(*map, p, stream);
-      case 4: return launch_tma<4, NW, 6>(*map, p, stream);
-      case 8: return launch_tma<8, NW, 6>(*map, p, stream);
-      default: return launch_tma<16, NW, 4>(*map, p, stream);
+      case 2:
+        switch (cp2_variant()) {
+          case 1: return launch_tma<2, 1, 4, 3>(*map, p, stream);
+          case 2: return launch_tma<2, 2, 2, 2>(*map, p, stream);
+          case 3: return launch_tma<2, 2, 4, 2>(*map, p, stream);
+          default: return launch_tma<2, 1, 4, 2>(*map, p, stream);
+        }
+      case 4: return launch_tma<4, 2, 4, 3>(*map, p, stream);
+      case 8: return launch_tma<8, 1, 4, 4>(*map, p, stream);
+      default: return launch_tma<16, 1, 4, 4>(*map, p, stream);
     }
   }
   switch (CP) {
