@@ -53,6 +53,10 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-logpost", action="store_true")
+    ap.add_argument("--fit-rows", type=int, default=1_000_000_000)
+    ap.add_argument("--workload", choices=("predict", "sweep", "ragged", "fit"), default="predict",
+                    help="predict = cfg4 (driver default); sweep = cfg2 F sweep at 1M rows; "
+                         "ragged = cfg3 32 size groups in one launch; fit = cfg5 1B x 128, C=16")
     return ap.parse_args()
 
 
@@ -185,6 +189,7 @@ def run_ours(args, world, rank, local):
 
     from paper_1905_13746_b200 import _native as N
     from paper_1905_13746_b200 import dense
+    from paper_1905_13746_b200.sharding import allreduce_stats
 
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
@@ -198,10 +203,7 @@ def run_ours(args, world, rank, local):
                                   row_offset=offset, device=dev)
     st = dense.fit_stats(x, size, lab, n_classes=2, group_size_bytes=width,
                          max_size_bytes=width)
-    if world > 1:
-        flat = st.packed()
-        dist.all_reduce(flat)               # NCCL over NVLink: the fit's only exchange
-        st.unpack_(flat)
+    allreduce_stats(st)                     # NCCL over NVLink: the fit's only exchange
     fin = dense.fin_train(st.sums.cpu().numpy(), st.counts.cpu().numpy(), k=V, alpha=1.0,
                           min_per_class=6)
     assert fin.state[0] == 1, "synthetic group must be trainable"
@@ -400,11 +402,188 @@ def run_reference(args, world, rank):
     }
 
 
+# ---------------------------------------------------------------- secondary workloads
+def _timed_launches(fn, steps, warmup, flush_bytes=512 << 20):
+    """Mean device time (ms) of fn() over `steps` launches, L2 flushed before each
+    (a 512 MB write, > 126 MB L2), CUDA events on the launching stream."""
+    import torch
+    flush = torch.empty(flush_bytes // 4, dtype=torch.int32, device="cuda")
+    for _ in range(warmup):
+        fn()
+    times = []
+    s = torch.cuda.current_stream()
+    for _ in range(steps):
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(s)
+        fn()
+        b.record(s)
+        b.synchronize()
+        times.append(a.elapsed_time(b))
+    return sum(times) / len(times), statistics.median(times)
+
+
+def run_sweep(args, world, rank, local):
+    """cfg2: F = 50/100/200/500/1000 at 1M samples, 2 classes, 1 B200."""
+    import numpy as np
+    import torch
+    from paper_1905_13746_b200 import dense
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    n = 1_000_000
+    peak, kind = peaks()
+    rows = []
+    for F in (50, 100, 200, 500, 1000):
+        x, size, lab = dense.generate(n, F, divergence=0.8, seed=0, device=dev)
+        st = dense.fit_stats(x, size, lab, n_classes=2, group_size_bytes=5120,
+                             max_size_bytes=5120)
+        fin = dense.fin_train(st.sums.cpu().numpy(), st.counts.cpu().numpy(), k=F, alpha=1.0,
+                              min_per_class=6)
+        nf = int(fin.n_features[0])
+        feats = fin.features[0, :nf].copy()
+        dense.generate(n, nf, divergence=0.8, seed=0, col_map=feats,
+                       out=(x[:, :nf], size, lab), device=dev)
+        t = dense.DeviceTables.build(fin.log_prior[:1], fin.log_lik[:1, :, :nf],
+                                     np.zeros(1, np.int32), group_size_bytes=5120,
+                                     max_size_bytes=5120, device=dev)
+        label = torch.empty(n, dtype=torch.int32, device=dev)
+        lp = torch.empty((n, 2), dtype=torch.float64, device=dev)
+        mean_ms, med_ms = _timed_launches(
+            lambda: dense.predict(x[:, :nf], size, t, label_out=label, logpost_out=lp),
+            args.steps, max(args.warmup, 3))
+        bps = 4 * nf + 24
+        rows.append({"F": nf, "ldx": int(x.stride(0)), "ms": round(mean_ms, 4),
+                     "samples_per_s": round(n / (mean_ms / 1e3), 1),
+                     "achieved_gbs": round(n * bps / (mean_ms / 1e3) / 1e9, 1),
+                     "frac": round(n * bps / (mean_ms / 1e3) / 1e9 / peak, 4)})
+        del x, size, lab, label, lp
+    return {"metric": METRIC, "workload": "cfg2: F sweep at 1M samples, 2 classes, L2 flushed "
+            "before every launch", "unit": UNIT, "peak_gbs": peak, "peak_source": kind,
+            "bytes_per_sample": "4F+24", "rows": rows, "steps": args.steps}
+
+
+def run_ragged(args, world, rank, local):
+    """cfg3: 4,194,304 samples in 32 ragged size groups (n_g ~ 0.9^g), F=200, groups
+    {5, 8, 17} untrained (routed), one K-PRED launch for all groups."""
+    import numpy as np
+    import torch
+    from oracle import oracle as O
+    from paper_1905_13746_b200 import dense
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    G, V, N = 32, 200, 4_194_304
+    w = 0.9 ** np.arange(G)
+    counts = np.floor(N * w / w.sum()).astype(np.int64)
+    counts[0] += N - counts.sum()
+    width, limit = 5120, G * 5120
+    x, size, lab = dense.generate(N, V, group_rows=counts, divergence=0.8, seed=0, device=dev)
+    st = dense.fit_stats(x, size, lab, n_classes=2, group_size_bytes=width, max_size_bytes=limit)
+    fin = dense.fin_train(st.sums.cpu().numpy(), st.counts.cpu().numpy(), k=V, alpha=1.0,
+                          min_per_class=6)
+    trained = [g for g in range(G) if fin.state[g] == 1 and g not in (5, 8, 17)]
+    slot = {g: i for i, g in enumerate(trained)}
+    route = np.array([slot[int(g)] for g in O.route_table(trained, G)], np.int32)
+    F = int(max(fin.n_features[g] for g in trained))
+    prior = fin.log_prior[trained]
+    lik = fin.log_lik[trained][:, :, :F]
+    feats = fin.features[trained][:, :F].astype(np.int32)
+    nfeat = fin.n_features[trained].astype(np.int32)
+    t = dense.DeviceTables.build(prior, lik, route, group_size_bytes=width, max_size_bytes=limit,
+                                 device=dev)
+    xg = dense.gather_features(x, size, t, feats, nfeat)
+    label = torch.empty(N, dtype=torch.int32, device=dev)
+    lp = torch.empty((N, 2), dtype=torch.float64, device=dev)
+    mean_ms, med_ms = _timed_launches(
+        lambda: dense.predict(xg, size, t, label_out=label, logpost_out=lp),
+        args.steps, max(args.warmup, 3))
+    # parity spot check against the C oracle on a strided subsample
+    idx = np.arange(0, N, 97)
+    xs, ss = xg.cpu().numpy()[idx], size.cpu().numpy()[idx]
+    want, wlp = O.c_predict(xs, ss, route, prior, lik, width=width, limit=limit, threads=8)
+    ok = bool((label.cpu().numpy()[idx] == want).all() and
+              lp.cpu().numpy()[idx].tobytes() == wlp.tobytes())
+    peak, kind = peaks()
+    bps = 4 * F + 24
+    perm = torch.randperm(N, device=dev)
+    xs_, ss_ = xg[perm].contiguous(), size[perm].contiguous()
+    mix_ms, _ = _timed_launches(
+        lambda: dense.predict(xs_, ss_, t, label_out=label, logpost_out=lp), args.steps, 3)
+    return {"metric": METRIC, "workload": "cfg3: 4,194,304 samples, 32 ragged size groups "
+            "(0.9^g), F=200, groups 5/8/17 untrained -> routed, single launch",
+            "unit": UNIT, "value": round(N / (mean_ms / 1e3), 1), "ms": round(mean_ms, 4),
+            "achieved_gbs": round(N * bps / (mean_ms / 1e3) / 1e9, 1),
+            "frac": round(N * bps / (mean_ms / 1e3) / 1e9 / peak, 4), "peak_gbs": peak,
+            "trained_groups": len(trained), "bit_exact_subsample_vs_oracle": ok,
+            "shuffled_rows": {"ms": round(mix_ms, 4),
+                              "value": round(N / (mix_ms / 1e3), 1),
+                              "note": "rows in random group order: mixed tiles, L1 table path"}}
+
+
+def run_fit(args, world, rank, local):
+    """cfg5: fit statistics (S, Q, n) over 1B samples x 128 features, 16 classes,
+    rows sharded over the ranks, generated in 100M-row chunks (512 GB total does
+    not fit one GPU), fit kernel timed per chunk, one NCCL all-reduce at the end."""
+    import torch
+    from paper_1905_13746_b200 import dense
+    from paper_1905_13746_b200.sharding import allreduce_stats, shard_bounds
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    total, V, C = args.fit_rows, 128, 16
+    lo, hi = shard_bounds(total, world, rank)
+    chunk = min(100_000_000, hi - lo)
+    x, size, lab = dense.generate(chunk, V, n_classes=C, group_rows=[total], divergence=0.8,
+                                  seed=0, row_offset=lo, device=dev)
+    # warm-up launch (module load, tensor-map path) outside the timed region
+    dense.fit_stats(x[:1024], size[:1024], lab[:1024], n_classes=C, group_size_bytes=5120,
+                    max_size_bytes=5120)
+    st = None
+    ms = 0.0
+    s = torch.cuda.current_stream()
+    for r0 in range(lo, hi, chunk):
+        n = min(chunk, hi - r0)
+        dense.generate(n, V, n_classes=C, group_rows=[total], divergence=0.8, seed=0,
+                       row_offset=r0, out=(x[:n], size[:n], lab[:n]), device=dev)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(s)
+        st = dense.fit_stats(x[:n], size[:n], lab[:n], n_classes=C, group_size_bytes=5120,
+                             max_size_bytes=5120, out=st, accumulate=st is not None)
+        b.record(s)
+        b.synchronize()
+        ms += a.elapsed_time(b)
+    if world > 1:
+        torch.distributed.barrier()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(s)
+    allreduce_stats(st)
+    b.record(s)
+    b.synchronize()
+    ar_ms = a.elapsed_time(b)
+    ms = barrier_max(ms, world, dev)
+    peak, kind = peaks()
+    bps = 4 * V + 8
+    rows_here = hi - lo
+    n_total = float(st.counts.sum().item())
+    return {"metric": "samples fitted/sec (sums, sums of squares, counts)", "unit": UNIT,
+            "workload": "cfg5: fit 1B samples x 128 features, 16 classes, 1 size group",
+            "value": round(total / ((ms + ar_ms) / 1e3), 1), "fit_kernel_ms": round(ms, 3),
+            "allreduce_ms": round(ar_ms, 4), "n_gpus": world,
+            "achieved_gbs_per_gpu": round(rows_here * bps / (ms / 1e3) / 1e9, 1),
+            "frac": round(rows_here * bps / (ms / 1e3) / 1e9 / peak, 4), "peak_gbs": peak,
+            "bytes_per_sample": "4V+8", "rows_counted": n_total,
+            "stats_bytes_allreduced": int(st.packed().numel() * 8)}
+
+
 def main():
     args = parse()
     world, rank, local = dist_init(args)
     if args.impl == "reference":
         out = run_reference(args, world, rank)
+    elif args.workload == "sweep":
+        out = run_sweep(args, world, rank, local)
+    elif args.workload == "ragged":
+        out = run_ragged(args, world, rank, local)
+    elif args.workload == "fit":
+        out = run_fit(args, world, rank, local)
     else:
         out = run_ours(args, world, rank, local)
     if rank == 0 and out is not None:

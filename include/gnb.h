@@ -98,6 +98,18 @@ int gnb_predict_host(const int32_t* x, int64_t n_rows, int32_t n_features, int64
                      int32_t* label_out, double* logpost_out, int32_t device,
                      int64_t* elapsed_ns);
 
+/* Route + FeatureSet gather (device): x_out[n][j] = x_vocab[n][features[s][j]]
+ * for j < n_features[s], s = route[size/width]; 0 elsewhere and for rows with
+ * size out of range.  Turns a full-vocabulary matrix into the gnb_predict
+ * input layout.  Replaces the per-sample route + `histogram.get(op)` walk of
+ * engine._classify_slice / classifier.log_posterior (engine.py:198-202,
+ * classifier.py:142-147).  features: [n_slots][max_features] vocab columns. */
+int gnb_gather_features(const int32_t* x_vocab, int64_t n_rows, int32_t n_vocab, int64_t ldx,
+                        const int32_t* size_bytes, int32_t group_size_bytes,
+                        int32_t max_size_bytes, const int32_t* route, const int32_t* features,
+                        const int32_t* n_features, int32_t n_slots, int32_t max_features,
+                        int32_t* x_out, int64_t ldo, uintptr_t stream);
+
 /* ------------------------------------------------------------------ fit
  * Replaces: the sample x histogram count loops of features.class_frequency
  *           (pkg/src/groupnb/features.py:48-53) and classifier.train_group

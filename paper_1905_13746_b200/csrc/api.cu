@@ -255,7 +255,7 @@ int gnb_fit_stats(const int32_t* x, int64_t n_rows, int32_t n_cols, int64_t ldx,
   for (int64_t r0 = 0; r0 < n_rows; r0 += kMaxRowsPerLaunch) {
     const int64_t n = std::min(kMaxRowsPerLaunch, n_rows - r0);
     CUtensorMap map;
-    if (!encode_map(&map, x + r0 * ldx, n, n_cols, ldx, 64, false))
+    if (!encode_map(&map, x + r0 * ldx, n, n_cols, ldx, fit_box_rows(), false))
       return fail(GNB_ECUDA, "fit_stats: cuTensorMapEncodeTiled failed");
     FitParams p{};
     p.n_rows = n;
@@ -305,6 +305,25 @@ int gnb_generate(int32_t* x, int64_t n_rows, int32_t n_cols, int64_t ldx, int32_
   p.vocab_cols = vocab_cols;
   for (int g = 0; g < n_groups; ++g) p.group_end[g] = group_row_end[g];
   GNB_CUDA(generate_launch(p, reinterpret_cast<cudaStream_t>(stream)), "generate launch");
+  return GNB_OK;
+}
+
+int gnb_gather_features(const int32_t* x_vocab, int64_t n_rows, int32_t n_vocab, int64_t ldx,
+                        const int32_t* size_bytes, int32_t group_size_bytes,
+                        int32_t max_size_bytes, const int32_t* route, const int32_t* features,
+                        const int32_t* n_features, int32_t n_slots, int32_t max_features,
+                        int32_t* x_out, int64_t ldo, uintptr_t stream) {
+  if (n_rows < 0 || n_vocab < 1 || ldx < n_vocab || max_features < 1 || ldo < max_features ||
+      n_slots < 1 || group_size_bytes <= 0 || max_size_bytes <= 0 ||
+      max_size_bytes % group_size_bytes)
+    return fail(GNB_EINVAL, "gather_features: bad geometry");
+  if (n_rows > 0 && (!x_vocab || !size_bytes || !x_out))
+    return fail(GNB_EINVAL, "gather_features: null pointer");
+  if (!route || !features || !n_features) return fail(GNB_EINVAL, "gather_features: null table");
+  GNB_CUDA(gather_launch(x_vocab, n_rows, n_vocab, ldx, size_bytes, group_size_bytes,
+                         max_size_bytes, route, features, n_features, max_features, x_out, ldo,
+                         reinterpret_cast<cudaStream_t>(stream)),
+           "gather launch");
   return GNB_OK;
 }
 

@@ -6,30 +6,40 @@
 // corpus.trainable_groups (pkg/src/groupnb/corpus.py:302-305).
 //
 // Segmented reduction keyed by key = group * C + label:
-//   * X [N, V] is streamed once by TMA in boxes of 32 columns x 64 rows
-//     (no swizzle: a warp reads one 128-B box row per step, conflict-free).  Column chunk c of every tile goes to consumer warp
-//     c mod NW, so a warp always owns the same columns and its shared-memory
-//     partials need no atomics.
+//   * X [N, V] is streamed once by TMA.  A stage is one tile of kFitRows rows
+//     x one 64-column group (two 32-column boxes, unswizzled), so a warp reads
+//     a whole 256-B row segment per step: lane l owns columns 2l, 2l+1 (one
+//     LDS.64, conflict-free per half warp).
 //   * the producer warp routes the tile's rows (size -> group, label ->
-//     class), drops out-of-range / unlabeled rows, and groups the rest by key
-//     with warp ballots (a counting sort without a histogram).  It publishes
-//     the permutation and the key runs with every stage.
-//   * a consumer lane owns one column: for each key run it accumulates
-//     sum x and sum x^2 in 64-bit integer registers (IMAD.WIDE, no FP64),
-//     then adds the run into the CTA's shared partial [key][col].  Integer
-//     arithmetic is exact and associative, so the result does not depend on
-//     the tiling, the grid, or how rows are sharded across GPUs.
+//     class), drops out-of-range / unlabeled rows, and counting-sorts the rest
+//     by key through a shared histogram (match_any leaders reserve places for
+//     their lanes).  The next tile's sizes/labels are prefetched while the
+//     current one sorts.  It publishes the permutation and the key runs with
+//     every stage.
+//   * every consumer warp reads every stage but only accumulates the runs of
+//     the keys it owns (key mod NW == warp), so its shared-memory partials
+//     [key][column] are private to it: no atomics, no replicas.  Within a run
+//     the sums of x and x^2 stay in 64-bit integer registers (IMAD.WIDE, no
+//     FP64); the run is then added into the partial (one read-modify-write
+//     per run, not per row).  Integer arithmetic is exact and associative, so
+//     the result does not depend on tiling, grid, or GPU sharding.
 //   * at exit every CTA adds its partials into the fp64 outputs with
-//     RED.ADD.F64 (exact: integer values < 2^53).
+//     RED.ADD.F64 (exact: integer values < 2^53).  Keys beyond the shared
+//     memory capacity go straight to global RED per run.
+#include <climits>
 #include <cstdint>
+#include <cstdlib>
 
 #include "gnb_device.cuh"
 #include "gnb_internal.h"
 
 namespace gnb {
 
-constexpr int kFitRows = 64;  // rows per tile (u8 permutation)
-constexpr int kFitSPW = 3;    // ring stages per consumer warp
+constexpr int kFitRows = 128;        // rows per tile (u8 permutation, 4 keys per lane)
+constexpr int kKeysPerLane = kFitRows / 32;
+constexpr int kGroupCols = 64;       // columns per stage: 2 boxes of 32
+constexpr int kBoxesPerStage = kGroupCols / kChunkCols;
+constexpr int kMaxHistKeys = 4096;   // keys sorted by the shared-memory histogram
 
 struct FitHdr {
   int n_runs;
@@ -38,126 +48,214 @@ struct FitHdr {
   int2 runs[kFitRows];  // {key, start | len << 16}
 };
 
-template <int NW>
+template <int NW, int STAGES>
 struct FitSmem {
-  static constexpr int kBox = kFitRows * kChunkBytesPerRow;  // 8 KB
-  static constexpr int kStages = NW * kFitSPW;
+  static constexpr int kBox = kFitRows * kChunkBytesPerRow;  // 16 KB
+  static constexpr int kStage = kBoxesPerStage * kBox;        // 32 KB
   static constexpr int kX = 0;
-  static constexpr int kHdr = kX + kStages * kBox;
-  static constexpr int kScratch = kHdr + kStages * static_cast<int>(sizeof(FitHdr));
+  static constexpr int kHdr = kX + STAGES * kStage;
+  static constexpr int kScratch = kHdr + STAGES * static_cast<int>(sizeof(FitHdr));
   static constexpr int kBar = kScratch + static_cast<int>(sizeof(FitHdr));
-  static constexpr int kPart = kBar + 2 * kStages * 8;  // 8-B aligned
-  static constexpr int kFixed = kPart + 1024;           // + alignment slack
+  static constexpr int kPart = (kBar + 2 * STAGES * 8 + 15) / 16 * 16;
+  static constexpr int kFixed = kPart + 1024;  // + alignment slack
 };
 
-template <int NW>
+__device__ __forceinline__ void add_u64x2(unsigned long long* p, unsigned long long a,
+                                          unsigned long long b) {
+  ulonglong2 v = *reinterpret_cast<ulonglong2*>(p);
+  v.x += a;
+  v.y += b;
+  *reinterpret_cast<ulonglong2*>(p) = v;
+}
+
+template <int NW, int STAGES>
 __global__ void __launch_bounds__((NW + 1) * 32)
     fit_tma_kernel(const __grid_constant__ CUtensorMap xmap, const FitParams p) {
-  using L = FitSmem<NW>;
+  using L = FitSmem<NW, STAGES>;
   extern __shared__ uint8_t smem_raw[];
-  // 1024-B alignment for SWIZZLE_128B, keeping the pointer in the shared window
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::kBar);
-  uint64_t* empty = full + L::kStages;
-  const int Fp = p.n_chunks * kChunkCols;
+  uint64_t* empty = full + STAGES;
+  const int NG = p.n_chunks;         // 64-column groups
+  const int Vp = NG * kGroupCols;
   const int KS = p.smem_keys;
   unsigned long long* part_s = reinterpret_cast<unsigned long long*>(smem + L::kPart);
-  unsigned long long* part_q = part_s + static_cast<int64_t>(KS) * Fp;  // if sumsq
-  unsigned long long* part_n = part_q + (p.sumsq ? static_cast<int64_t>(KS) * Fp : 0);
+  unsigned long long* part_q = part_s + static_cast<int64_t>(KS) * Vp;  // if sumsq
+  unsigned long long* part_n = part_q + (p.sumsq ? static_cast<int64_t>(KS) * Vp : 0);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nthreads = blockDim.x;
-  const int64_t part_words = static_cast<int64_t>(KS) * Fp * (p.sumsq ? 2 : 1) + KS;
+  const int64_t part_words = static_cast<int64_t>(KS) * Vp * (p.sumsq ? 2 : 1) + KS;
   for (int64_t i = threadIdx.x; i < part_words; i += nthreads) part_s[i] = 0ull;
+  // histogram sort scratch after the partials: hist[HK], kstart[HK]
+  const int HK = p.n_keys <= kMaxHistKeys ? p.n_keys : 0;
+  int* hist = reinterpret_cast<int*>(part_n + KS);
+  int* kstart = hist + HK;
+  for (int i = threadIdx.x; i < HK; i += nthreads) hist[i] = 0;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < L::kStages; ++s) {
+    for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 32);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], NW);
     }
     mbar_fence_init();
   }
   __syncthreads();
 
-  const int NCH = p.n_chunks;
   if (warp == NW) {
     // ------------------------------------------------------------ producer
-    const uint64_t pol_x = policy_evict_first();
+    const uint64_t pol_x = policy_evict_normal();
     FitHdr* scratch = reinterpret_cast<FitHdr*>(smem + L::kScratch);
-    int stage_of[NW];
-    uint32_t phase_of[NW];
-#pragma unroll
-    for (int w = 0; w < NW; ++w) {
-      stage_of[w] = 0;
-      phase_of[w] = 0;
-    }
+    int stage = 0;
+    uint32_t phase = 0;
     unsigned long long bad_label = 0, out_of_range = 0;
     const uint32_t lt = (1u << lane) - 1u;
+    const bool hist_sort = HK > 0;
+    // Sizes/labels of the NEXT tile are loaded while this tile sorts; they are
+    // only turned into keys (and status counts) one iteration later, so the
+    // global-load latency never stalls the producer.
+    auto load_raw = [&](int64_t tile, int (&sz)[kKeysPerLane], int (&lab)[kKeysPerLane]) {
+#pragma unroll
+      for (int i = 0; i < kKeysPerLane; ++i) {
+        const int64_t r = tile * kFitRows + lane + 32 * i;
+        const bool in = tile < p.n_tiles && r < p.n_rows;
+        sz[i] = in ? __ldg(p.size + r) : INT_MIN;  // INT_MIN: no row
+        lab[i] = in ? __ldg(p.labels + r) : 0;
+      }
+    };
+    int nsz[kKeysPerLane], nlab[kKeysPerLane];
+    load_raw(blockIdx.x, nsz, nlab);
     for (int64_t tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
       const int64_t r0 = tile * kFitRows;
-      int key[2];
+      int key[kKeysPerLane];
 #pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        const int64_t r = r0 + lane + 32 * i;
+      for (int i = 0; i < kKeysPerLane; ++i) {
+        const int sz = nsz[i], lab = nlab[i];
         key[i] = -1;
-        if (r < p.n_rows) {
-          const int sz = __ldg(p.size + r);
-          if (sz >= 0 && sz < p.limit) {
-            const int lab = __ldg(p.labels + r);
-            if (lab >= 0 && lab < p.n_classes)
-              key[i] = (sz / p.width) * p.n_classes + lab;
-            else
-              ++bad_label;
-          } else {
-            ++out_of_range;
+        if (sz == INT_MIN) continue;
+        if (sz >= 0 && sz < p.limit) {
+          if (lab >= 0 && lab < p.n_classes)
+            key[i] = (sz / p.width) * p.n_classes + lab;
+          else
+            ++bad_label;
+        } else {
+          ++out_of_range;
+        }
+      }
+      load_raw(tile + gridDim.x, nsz, nlab);  // prefetch
+      int n_runs = 0;
+      if (hist_sort) {
+        // counting sort through a shared histogram: per key slot, lanes with
+        // equal keys elect a leader that reserves popc(lanes) places at once
+        int rank[kKeysPerLane];
+        uint32_t mine = 0;  // bit i: this lane's slot-i key is new in the tile
+#pragma unroll
+        for (int i = 0; i < kKeysPerLane; ++i) {
+          const uint32_t m = __match_any_sync(~0u, key[i]);
+          const int leader = __ffs(m) - 1;
+          int base = 0;
+          if (key[i] >= 0 && lane == leader) base = atomicAdd(&hist[key[i]], __popc(m));
+          base = __shfl_sync(~0u, base, leader);
+          rank[i] = base + __popc(m & lt);
+          if (key[i] >= 0 && lane == leader && base == 0) mine |= 1u << i;
+        }
+        __syncwarp();
+        // list the tile's keys, exclusive-scan their counts into run starts
+        int cnt[kKeysPerLane], kk[kKeysPerLane];
+        int total = 0;
+#pragma unroll
+        for (int i = 0; i < kKeysPerLane; ++i) {
+          const bool is_new = (mine >> i) & 1u;
+          const uint32_t b = __ballot_sync(~0u, is_new);
+          const int slot = n_runs + __popc(b & lt);
+          kk[i] = is_new ? key[i] : -1;
+          cnt[i] = is_new ? hist[key[i]] : 0;
+          // inclusive warp scan of cnt[i] in run order (slot order)
+          int v = cnt[i];
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(~0u, v, o);
+            if (lane >= o) v += t;
+          }
+          const int start = total + v - cnt[i];
+          if (is_new) {
+            kstart[key[i]] = start;
+            scratch->runs[slot] = make_int2(key[i], start | (cnt[i] << 16));
+          }
+          total += __shfl_sync(~0u, v, 31);
+          n_runs += __popc(b);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < kKeysPerLane; ++i)
+          if (key[i] >= 0)
+            scratch->perm[kstart[key[i]] + rank[i]] = static_cast<uint8_t>(lane + 32 * i);
+        // counts + reset the histogram entries this tile touched
+#pragma unroll
+        for (int i = 0; i < kKeysPerLane; ++i) {
+          if (kk[i] >= 0) {
+            if (kk[i] < KS) part_n[kk[i]] += static_cast<unsigned long long>(cnt[i]);
+            else atomicAdd(p.counts + kk[i], static_cast<double>(cnt[i]));
+            hist[kk[i]] = 0;
           }
         }
-      }
-      // group rows by key: repeatedly take the first remaining row's key
-      uint32_t rem0 = __ballot_sync(~0u, key[0] >= 0);
-      uint32_t rem1 = __ballot_sync(~0u, key[1] >= 0);
-      int pos = 0, n_runs = 0;
-      while (rem0 | rem1) {
-        const int src = rem0 ? __ffs(rem0) - 1 : __ffs(rem1) - 1;
-        const int k = rem0 ? __shfl_sync(~0u, key[0], src) : __shfl_sync(~0u, key[1], src);
-        const uint32_t m0 = __ballot_sync(~0u, key[0] == k) & rem0;
-        const uint32_t m1 = __ballot_sync(~0u, key[1] == k) & rem1;
-        const int c0 = __popc(m0), len = c0 + __popc(m1);
-        if (m0 & (1u << lane)) scratch->perm[pos + __popc(m0 & lt)] = static_cast<uint8_t>(lane);
-        if (m1 & (1u << lane))
-          scratch->perm[pos + c0 + __popc(m1 & lt)] = static_cast<uint8_t>(lane + 32);
-        if (lane == 0) {
-          scratch->runs[n_runs] = make_int2(k, pos | (len << 16));
-          if (k < KS) part_n[k] += static_cast<unsigned long long>(len);
-          else atomicAdd(p.counts + k, static_cast<double>(len));
+      } else {
+        // huge key spaces: take the first remaining row's key, ballot its rows
+        uint32_t rem[kKeysPerLane];
+#pragma unroll
+        for (int i = 0; i < kKeysPerLane; ++i) rem[i] = __ballot_sync(~0u, key[i] >= 0);
+        int pos = 0;
+        while (true) {
+          int src_i = -1;
+#pragma unroll
+          for (int i = kKeysPerLane - 1; i >= 0; --i)
+            if (rem[i]) src_i = i;
+          if (src_i < 0) break;
+          int k = 0;
+#pragma unroll
+          for (int i = 0; i < kKeysPerLane; ++i)
+            if (i == src_i) k = __shfl_sync(~0u, key[i], __ffs(rem[i]) - 1);
+          int len = 0;
+#pragma unroll
+          for (int i = 0; i < kKeysPerLane; ++i) {
+            const uint32_t m = __ballot_sync(~0u, key[i] == k) & rem[i];
+            if (m & (1u << lane))
+              scratch->perm[pos + len + __popc(m & lt)] = static_cast<uint8_t>(lane + 32 * i);
+            len += __popc(m);
+            rem[i] &= ~m;
+          }
+          if (lane == 0) {
+            scratch->runs[n_runs] = make_int2(k, pos | (len << 16));
+            if (k < KS) part_n[k] += static_cast<unsigned long long>(len);
+            else atomicAdd(p.counts + k, static_cast<double>(len));
+          }
+          pos += len;
+          ++n_runs;
         }
-        pos += len;
-        ++n_runs;
-        rem0 &= ~m0;
-        rem1 &= ~m1;
       }
       __syncwarp();
-      // copy perm + runs, then ship each column chunk to its owner warp
       const int hdr_words = (16 + kFitRows + n_runs * 8 + 15) / 16;  // 16-B units
-      for (int ch = 0; ch < NCH; ++ch) {
-        const int w = ch % NW;
-        const int st = w * kFitSPW + stage_of[w];
-        mbar_wait(&empty[st], phase_of[w] ^ 1);
-        FitHdr* hdr = reinterpret_cast<FitHdr*>(smem + L::kHdr + st * sizeof(FitHdr));
+      for (int cg = 0; cg < NG; ++cg) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        FitHdr* hdr = reinterpret_cast<FitHdr*>(smem + L::kHdr + stage * sizeof(FitHdr));
         const int4* src4 = reinterpret_cast<const int4*>(scratch);
         int4* dst4 = reinterpret_cast<int4*>(hdr);
         for (int i = lane; i < hdr_words; i += 32) dst4[i] = src4[i];
         if (lane == 0) hdr->n_runs = n_runs;
         __syncwarp();
         if (lane == 0) {
-          mbar_arrive_expect_tx(&full[st], L::kBox);
-          tma_load_2d(smem + L::kX + st * L::kBox, &xmap, ch * kChunkCols,
-                      static_cast<int32_t>(r0), &full[st], pol_x);
+          const int boxes = min(kBoxesPerStage,
+                                (p.n_cols - cg * kGroupCols + kChunkCols - 1) / kChunkCols);
+          mbar_arrive_expect_tx(&full[stage], boxes * L::kBox);
+          for (int b = 0; b < boxes; ++b)
+            tma_load_2d(smem + L::kX + stage * L::kStage + b * L::kBox, &xmap,
+                        cg * kGroupCols + b * kChunkCols, static_cast<int32_t>(r0), &full[stage],
+                        pol_x);
         } else {
-          mbar_arrive(&full[st]);
+          mbar_arrive(&full[stage]);
         }
-        if (++stage_of[w] == kFitSPW) {
-          stage_of[w] = 0;
-          phase_of[w] ^= 1;
+        if (++stage == STAGES) {
+          stage = 0;
+          phase ^= 1;
         }
       }
       __syncwarp();
@@ -173,54 +271,72 @@ __global__ void __launch_bounds__((NW + 1) * 32)
     }
   } else {
     // ------------------------------------------------------------ consumers
-    const uint32_t lane4 = static_cast<uint32_t>(lane) * 4u;  // unswizzled box: row r at r*128
+    // lane owns columns 2*lane, 2*lane+1 of the group: box lane/16, bytes (lane%16)*8
+    const uint32_t lane_off = static_cast<uint32_t>(lane >> 4) * L::kBox + (lane & 15) * 8;
     int stage = 0;
     uint32_t phase = 0;
     for (int64_t tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
-      for (int ch = warp; ch < NCH; ch += NW) {
-        const int st = warp * kFitSPW + stage;
-        mbar_wait(&full[st], phase);
-        const FitHdr* hdr = reinterpret_cast<const FitHdr*>(smem + L::kHdr + st * sizeof(FitHdr));
-        const uint8_t* box = smem + L::kX + st * L::kBox;
-        const int col = ch * kChunkCols + lane;
+      for (int cg = 0; cg < NG; ++cg) {
+        mbar_wait(&full[stage], phase);
+        const FitHdr* hdr =
+            reinterpret_cast<const FitHdr*>(smem + L::kHdr + stage * sizeof(FitHdr));
+        const uint8_t* xs = smem + L::kX + stage * L::kStage + lane_off;
+        const int col0 = cg * kGroupCols + 2 * lane;
         const int n_runs = hdr->n_runs;
-        for (int ri = 0; ri < n_runs; ++ri) {
-          const int2 run = hdr->runs[ri];
-          const int start = run.y & 0xffff, len = run.y >> 16;
-          unsigned long long s = 0, s2 = 0;
-          int i = 0;
-          for (; i + 4 <= len; i += 4) {
-            uint32_t x[4];
+        for (int rb = 0; rb < n_runs; rb += 32) {
+          // lane j holds run rb+j; the warp walks only the runs of its keys
+          int2 mine = make_int2(-1, 0);
+          if (rb + lane < n_runs) mine = hdr->runs[rb + lane];
+          uint32_t todo = __ballot_sync(~0u, mine.x >= 0 && mine.x % NW == warp);
+          while (todo) {
+            const int j = __ffs(todo) - 1;
+            todo &= todo - 1;
+            const int k = __shfl_sync(~0u, mine.x, j);
+            const int packed = __shfl_sync(~0u, mine.y, j);
+            const int start = packed & 0xffff, len = packed >> 16;
+            unsigned long long s0 = 0, s1 = 0, q0 = 0, q1 = 0;
+            int i = 0;
+            for (; i + 4 <= len; i += 4) {
+              uint2 v[4];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              const uint32_t r = hdr->perm[start + i + u];
-              x[u] = *reinterpret_cast<const uint32_t*>(box + (r << 7) + lane4);
-            }
+              for (int u = 0; u < 4; ++u) {
+                const uint32_t r = hdr->perm[start + i + u];
+                v[u] = *reinterpret_cast<const uint2*>(xs + (r << 7));
+              }
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              s += x[u];
-              s2 += static_cast<unsigned long long>(x[u]) * x[u];
+              for (int u = 0; u < 4; ++u) {
+                s0 += v[u].x;
+                s1 += v[u].y;
+                q0 += static_cast<unsigned long long>(v[u].x) * v[u].x;
+                q1 += static_cast<unsigned long long>(v[u].y) * v[u].y;
+              }
             }
-          }
-          for (; i < len; ++i) {
-            const uint32_t r = hdr->perm[start + i];
-            const uint32_t x = *reinterpret_cast<const uint32_t*>(box + (r << 7) + lane4);
-            s += x;
-            s2 += static_cast<unsigned long long>(x) * x;
-          }
-          const int k = run.x;
-          if (k < KS) {
-            part_s[static_cast<int64_t>(k) * Fp + col] += s;
-            if (p.sumsq) part_q[static_cast<int64_t>(k) * Fp + col] += s2;
-          } else if (col < p.n_cols) {
-            if (s) atomicAdd(p.sums + static_cast<int64_t>(k) * p.n_cols + col, static_cast<double>(s));
-            if (p.sumsq && s2)
-              atomicAdd(p.sumsq + static_cast<int64_t>(k) * p.n_cols + col, static_cast<double>(s2));
+            for (; i < len; ++i) {
+              const uint32_t r = hdr->perm[start + i];
+              const uint2 v = *reinterpret_cast<const uint2*>(xs + (r << 7));
+              s0 += v.x;
+              s1 += v.y;
+              q0 += static_cast<unsigned long long>(v.x) * v.x;
+              q1 += static_cast<unsigned long long>(v.y) * v.y;
+            }
+            if (k < KS) {
+              add_u64x2(part_s + static_cast<int64_t>(k) * Vp + col0, s0, s1);
+              if (p.sumsq) add_u64x2(part_q + static_cast<int64_t>(k) * Vp + col0, q0, q1);
+            } else {
+              const unsigned long long sv[2] = {s0, s1}, qv[2] = {q0, q1};
+#pragma unroll
+              for (int e = 0; e < 2; ++e) {
+                if (col0 + e >= p.n_cols) break;
+                const int64_t o = static_cast<int64_t>(k) * p.n_cols + col0 + e;
+                if (sv[e]) atomicAdd(p.sums + o, static_cast<double>(sv[e]));
+                if (p.sumsq && qv[e]) atomicAdd(p.sumsq + o, static_cast<double>(qv[e]));
+              }
+            }
           }
         }
         __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[st]);
-        if (++stage == kFitSPW) {
+        if (lane == 0) mbar_arrive(&empty[stage]);
+        if (++stage == STAGES) {
           stage = 0;
           phase ^= 1;
         }
@@ -229,8 +345,8 @@ __global__ void __launch_bounds__((NW + 1) * 32)
   }
   __syncthreads();
   // ------------------------------------------------------------ flush partials
-  for (int64_t i = threadIdx.x; i < static_cast<int64_t>(KS) * Fp; i += nthreads) {
-    const int k = static_cast<int>(i / Fp), col = static_cast<int>(i % Fp);
+  for (int64_t i = threadIdx.x; i < static_cast<int64_t>(KS) * Vp; i += nthreads) {
+    const int k = static_cast<int>(i / Vp), col = static_cast<int>(i % Vp);
     if (col >= p.n_cols) continue;
     const int64_t o = static_cast<int64_t>(k) * p.n_cols + col;
     if (part_s[i]) atomicAdd(p.sums + o, static_cast<double>(part_s[i]));
@@ -240,23 +356,27 @@ __global__ void __launch_bounds__((NW + 1) * 32)
     if (part_n[k]) atomicAdd(p.counts + k, static_cast<double>(part_n[k]));
 }
 
-template <int NW>
-static cudaError_t launch_fit(const CUtensorMap& map, FitParams p, cudaStream_t stream) {
-  using L = FitSmem<NW>;
-  auto kern = fit_tma_kernel<NW>;
+template <int NW, int STAGES>
+static cudaError_t launch_fit(const CUtensorMap& map, FitParams p, cudaStream_t stream,
+                              int ctas_per_sm) {
+  using L = FitSmem<NW, STAGES>;
+  auto kern = fit_tma_kernel<NW, STAGES>;
   int dev = 0, sms = 0, max_smem = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  const int Fp = p.n_chunks * kChunkCols;
-  const int per_key = Fp * 8 * (p.sumsq ? 2 : 1) + 8;
-  // keep partials modest so two CTAs fit per SM when keys are few
-  const int budget = max_smem - L::kFixed;
-  int ks = budget / per_key;
+  const int Vp = p.n_chunks * kGroupCols;
+  const int per_key = Vp * 8 * (p.sumsq ? 2 : 1) + 8;
+  const int hist_bytes = p.n_keys <= kMaxHistKeys ? 8 * p.n_keys : 0;
+  // Partials sized so `ctas_per_sm` CTAs share an SM; keys beyond the cap
+  // (large group counts) accumulate per run in global memory.
+  const int budget = (max_smem + 1024) / ctas_per_sm - 1024 - L::kFixed - hist_bytes;
+  int ks = budget > 0 ? budget / per_key : 0;
+  if (ks < 1) ks = (max_smem - L::kFixed - hist_bytes) / per_key;
   if (ks > p.n_keys) ks = p.n_keys;
   if (ks < 0) ks = 0;
   p.smem_keys = ks;
-  const int smem = L::kFixed + ks * per_key;
+  const int smem = L::kFixed + ks * per_key + hist_bytes;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   int per_sm = 0;
@@ -270,12 +390,38 @@ static cudaError_t launch_fit(const CUtensorMap& map, FitParams p, cudaStream_t 
   return cudaGetLastError();
 }
 
+int fit_box_rows() { return kFitRows; }
+
+// GNB_FIT_VARIANT (profiling only): 0 = 2 stages x 2 CTAs/SM (default; measured
+// best on B200, profiles/r01_tuning.md), 1 = 4 stages x 1 CTA/SM,
+// 2 = 5 stages x 1 CTA/SM, 3 = 3 stages x 1 CTA/SM.
+static int fit_variant() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("GNB_FIT_VARIANT");
+    v = e ? atoi(e) : 0;
+    if (v < 0 || v > 3) v = 0;
+  }
+  return v;
+}
+
+template <int NW>
+static cudaError_t launch_fit_nw(const CUtensorMap& map, const FitParams& p, cudaStream_t stream) {
+  switch (fit_variant()) {
+    case 1: return launch_fit<NW, 4>(map, p, stream, 1);
+    case 2: return launch_fit<NW, 5>(map, p, stream, 1);
+    case 3: return launch_fit<NW, 3>(map, p, stream, 1);
+    default: return launch_fit<NW, 2>(map, p, stream, 2);
+  }
+}
+
 cudaError_t fit_launch(const CUtensorMap& map, FitParams p, cudaStream_t stream) {
-  p.n_chunks = (p.n_cols + kChunkCols - 1) / kChunkCols;
+  p.n_chunks = (p.n_cols + kGroupCols - 1) / kGroupCols;  // 64-column groups
   p.n_tiles = (p.n_rows + kFitRows - 1) / kFitRows;
-  if (p.n_chunks >= 4) return launch_fit<4>(map, p, stream);
-  if (p.n_chunks >= 2) return launch_fit<2>(map, p, stream);
-  return launch_fit<1>(map, p, stream);
+  // keys are dealt to warps round-robin: no more warps than keys
+  if (p.n_keys >= 4) return launch_fit_nw<4>(map, p, stream);
+  if (p.n_keys >= 2) return launch_fit_nw<2>(map, p, stream);
+  return launch_fit_nw<1>(map, p, stream);
 }
 
 }  // namespace gnb

@@ -48,8 +48,14 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
   return ok != 0;
 }
 
+// Spin on try_wait (which itself suspends in hardware).  A phase that never
+// completes is a bug (e.g. expect_tx bytes that the copies never deliver):
+// after ~2^34 cycles (~9 s) trap instead of hanging the GPU.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  if (mbar_try_wait(bar, parity)) return;
+  const long long t0 = clock64();
   while (!mbar_try_wait(bar, parity)) {
+    if (clock64() - t0 > (1ll << 34)) __trap();
   }
 }
 

@@ -56,6 +56,7 @@ cudaError_t pack_tables(const double* log_prior, const double* log_lik, int S, i
 int predict_box_rows(int n_classes);  // TMA box height of the K-PRED variant
 cudaError_t predict_launch(const CUtensorMap* map, PredictParams p, cudaStream_t stream,
                            int force_generic);
+int fit_box_rows();  // TMA box height of K-FIT tiles
 cudaError_t fit_launch(const CUtensorMap& map, FitParams p, cudaStream_t stream);
 
 struct GenParams {
@@ -76,6 +77,12 @@ struct GenParams {
   long long group_end[128];
 };
 cudaError_t generate_launch(const GenParams& p, cudaStream_t stream);
+
+cudaError_t gather_launch(const int32_t* x, int64_t n_rows, int32_t V, int64_t ldx,
+                          const int32_t* size, int32_t width, int32_t limit,
+                          const int32_t* route, const int32_t* features,
+                          const int32_t* n_features, int32_t F, int32_t* out, int64_t ldo,
+                          cudaStream_t stream);
 
 // Host helpers (api.cu)
 bool encode_rows_map(CUtensorMap* map, const void* base, int64_t n_rows, int32_t n_cols,

@@ -116,6 +116,31 @@ def predict(x: torch.Tensor, size_bytes: torch.Tensor, tables: DeviceTables, *,
     return label, lp
 
 
+def gather_features(x_vocab: torch.Tensor, size_bytes: torch.Tensor, tables: DeviceTables,
+                    features, n_features, *, out=None, stream=None) -> torch.Tensor:
+    """[N, V] full-vocabulary counts -> [N, F] predict layout (routed FeatureSet order).
+
+    features: [S, F] vocabulary column per (slot, feature); n_features: [S]."""
+    xp, n, V, ldx = _rows(x_vocab, "x_vocab")
+    dev = x_vocab.device
+    feats = torch.as_tensor(features, dtype=torch.int32).to(dev).contiguous()
+    nf = torch.as_tensor(n_features, dtype=torch.int32).to(dev).contiguous()
+    F = tables.n_features
+    if feats.shape != (tables.n_slots, F) or nf.shape != (tables.n_slots,):
+        raise InvalidConfigError("features must be [n_slots, F] and n_features [n_slots]")
+    if out is None:
+        ld = (F + 3) // 4 * 4
+        out = torch.empty((n, ld), dtype=torch.int32, device=dev)[:, :F]
+    op, _, Fo, ldo = _rows(out, "out")
+    if Fo != F:
+        raise InvalidConfigError("out must have F columns")
+    N.check(N.lib.gnb_gather_features(
+        xp, n, V, ldx, _vec(size_bytes, n, "size_bytes"), tables.group_size_bytes,
+        tables.max_size_bytes, tables.route.data_ptr(), feats.data_ptr(), nf.data_ptr(),
+        tables.n_slots, F, op, ldo, _stream(stream)), "gnb_gather_features")
+    return out
+
+
 # ---------------------------------------------------------------- fit
 @dataclass
 class FitStats:

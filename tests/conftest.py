@@ -32,3 +32,10 @@ def cuda_ok():
         return torch.cuda.is_available()
     except Exception:
         return False
+
+
+def pytest_collection_modifyitems(config, items):
+    # a GPU test that hangs is a bug; fail it instead of holding the box
+    for item in items:
+        if item.get_closest_marker("gpu") and not item.get_closest_marker("timeout"):
+            item.add_marker(pytest.mark.timeout(120))

@@ -160,3 +160,36 @@ def test_large_counts_and_values_exact():
     x = rng.integers(0, 2**31 - 1, size=(257, F))
     x[::3] = rng.integers(0, 3, size=(86, F))
     _check(x, np.zeros(257, np.int64), prior, ll, np.zeros(1, np.int32), 1, 1, ldx=36)
+
+
+def test_gather_features_matches_oracle():
+    """Device route + FeatureSet gather == oracle.gather_rows; then predict on it."""
+    rng = np.random.default_rng(21)
+    G, V, F, N = 12, 90, 40, 20000
+    trained = [0, 1, 2, 4, 5, 6, 8, 10]
+    models = {}
+    for g in trained:
+        nf = int(rng.integers(5, F + 1))
+        feats = rng.choice(V, size=nf, replace=False)
+        models[g] = O.GroupTables(g, feats, np.log(np.array([0.4, 0.6])),
+                                  np.log(rng.dirichlet(np.ones(nf), size=2)), np.array([6, 6]))
+    ids, route, prior, ll = O.pack_models(models, G, F)
+    featmat = np.full((len(ids), F), -1, np.int32)
+    nfeat = np.zeros(len(ids), np.int32)
+    for i, g in enumerate(ids):
+        featmat[i, :len(models[g].features)] = models[g].features
+        nfeat[i] = len(models[g].features)
+    xv = rng.poisson(1.0, size=(N, V)).astype(np.int32)
+    size = rng.integers(-10, G * 100 + 10, size=N).astype(np.int32)
+    dev = torch.device("cuda")
+    t = dense.DeviceTables.build(prior, ll, route, group_size_bytes=100, max_size_bytes=G * 100)
+    sd = torch.from_numpy(size).to(dev)
+    xg = dense.gather_features(torch.from_numpy(xv).to(dev), sd, t, featmat, nfeat)
+    lab, lp = dense.predict(xg, sd, t)
+    torch.cuda.synchronize()
+    want_x = O.gather_rows(xv, size, models, width=100, limit=G * 100, n_features=F)
+    assert np.array_equal(xg.cpu().numpy(), want_x)
+    want, wlp = O.predict_dense(want_x, size, route, prior, ll, width=100, limit=G * 100)
+    assert lab.cpu().numpy().tolist() == want.tolist()
+    ok = want >= 0
+    assert lp.cpu().numpy()[ok].tobytes() == wlp[ok].tobytes()
