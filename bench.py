@@ -54,6 +54,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-logpost", action="store_true")
     ap.add_argument("--fit-rows", type=int, default=1_000_000_000)
+    ap.add_argument("--x-dtype", choices=("int32", "uint16", "uint8"), default="int32",
+                    help="storage of the predict matrix (same counts; narrower = fewer bytes)")
     ap.add_argument("--workload", choices=("predict", "sweep", "ragged", "fit"), default="predict",
                     help="predict = cfg4 (driver default); sweep = cfg2 F sweep at 1M rows; "
                          "ragged = cfg3 32 size groups in one launch; fit = cfg5 1B x 128, C=16")
@@ -213,6 +215,11 @@ def run_ours(args, world, rank, local):
     dense.generate(n, F, group_rows=group_rows, divergence=0.8, seed=0, row_offset=offset,
                    col_map=feats, out=(x[:, :F], size, lab), device=dev)
     xg = x[:, :F]
+    if args.x_dtype != "int32":
+        assert int(xg.max()) < (256 if args.x_dtype == "uint8" else 65536), "counts do not fit"
+        xg = xg.to(getattr(torch, args.x_dtype))   # lossless: every count fits
+        del x
+        torch.cuda.empty_cache()
     tables = dense.DeviceTables.build(fin.log_prior[:1], fin.log_lik[:1, :, :F],
                                       np.zeros(1, np.int32), group_size_bytes=width,
                                       max_size_bytes=width, device=dev)
@@ -261,7 +268,8 @@ def run_ours(args, world, rank, local):
 
     # ---- roofline of the dominant (only) kernel
     out_bytes = 4 + (16 if logpost is not None else 0)
-    bytes_per_sample = 4 * F + 4 + out_bytes
+    eb = xg.element_size()
+    bytes_per_sample = eb * F + 4 + out_bytes
     achieved = n * bytes_per_sample / (mean_launch_ms / 1e3) / 1e9
     peak, peak_kind = peaks()
     tps, ncu = ncu_traffic()
@@ -269,7 +277,7 @@ def run_ours(args, world, rank, local):
                 "frac": round(achieved / peak, 4), "peak_source": peak_kind,
                 "traffic": round(tps * n) if tps else None,
                 "algorithmic_bytes_per_launch": n * bytes_per_sample,
-                "bytes_per_sample": f"4F+4+{out_bytes} = {bytes_per_sample}",
+                "bytes_per_sample": f"{eb}F+4+{out_bytes} = {bytes_per_sample}",
                 "kernel": "gnb::predict_tma_kernel<2,1,4,2>"}
     if ncu:
         roofline["traffic_source"] = ncu.get("source")
@@ -322,7 +330,7 @@ def run_ours(args, world, rank, local):
         "config": {"workload": "cfg4: predict 100M samples x 256 features per GPU, 2 classes, "
                                "1 size group" if (n == DEFAULT_ROWS and V == DEFAULT_F)
                    else f"predict {n} samples x {V} features per GPU, 2 classes",
-                   "rows_per_gpu": n, "features": F, "classes": 2, "x_dtype": "int32",
+                   "rows_per_gpu": n, "features": F, "classes": 2, "x_dtype": args.x_dtype,
                    "outputs": "label int32 + log-posterior fp64 x2" if logpost is not None
                    else "label int32", "parity": "bit-exact vs reference (exact mode)",
                    "l2": "inputs (%.1f GB/GPU) >> 126 MB L2; no flush needed" % (n * 4 * F / 1e9),

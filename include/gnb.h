@@ -51,6 +51,10 @@ enum {
 
 #define GNB_MAX_CLASSES 16
 
+/* element type of X for the typed entry points: the same non-negative
+ * integer counts, stored in fewer bytes when they fit */
+enum { GNB_X_I32 = 0, GNB_X_U16 = 1, GNB_X_U8 = 2 };
+
 int gnb_abi_version(void);
 const char* gnb_strerror(int code);
 const char* gnb_last_error(void);
@@ -78,6 +82,15 @@ int gnb_predict(const int32_t* x, int64_t n_rows, int32_t n_features, int64_t ld
                 const int32_t* size_bytes, int32_t group_size_bytes, int32_t max_size_bytes,
                 const int32_t* route, int32_t n_slots, int32_t n_classes, const void* packed,
                 int32_t* label_out, double* logpost_out, uintptr_t stream);
+
+/* gnb_predict for X stored as x_type (GNB_X_I32 / GNB_X_U16 / GNB_X_U8); ldx
+ * in elements.  uint8/uint16 rows move 4x/2x fewer bytes; results are
+ * identical for the same counts. */
+int gnb_predict_typed(const void* x, int32_t x_type, int64_t n_rows, int32_t n_features,
+                      int64_t ldx, const int32_t* size_bytes, int32_t group_size_bytes,
+                      int32_t max_size_bytes, const int32_t* route, int32_t n_slots,
+                      int32_t n_classes, const void* packed, int32_t* label_out,
+                      double* logpost_out, uintptr_t stream);
 
 /* Same as gnb_predict but always uses the L1 (non-TMA) kernel; parity tests. */
 int gnb_predict_generic(const int32_t* x, int64_t n_rows, int32_t n_features, int64_t ldx,

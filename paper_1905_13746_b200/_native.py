@@ -14,13 +14,15 @@ import re
 from .errors import EmptyBundleError, InvalidConfigError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libgnb.so")
+# GNB_LIB: load an alternative in-tree build (kernel experiments / profiling)
+LIB_PATH = os.path.join(_HERE, os.environ.get("GNB_LIB", "libgnb.so"))
 HEADER = os.path.join(os.path.dirname(_HERE), "include", "gnb.h")
 
 GNB_OK, GNB_EINVAL, GNB_ECUDA, GNB_EUNSUPPORTED, GNB_ENOMEM = 0, 1, 2, 3, 4
 ROW_OUT_OF_RANGE = -1
 ROW_NEGATIVE_COUNT = -2
 MAX_CLASSES = 16
+X_I32, X_U16, X_U8 = 0, 1, 2
 
 
 class NativeError(RuntimeError):
@@ -48,6 +50,8 @@ _SIGS = {
     "gnb_pack_tables": ([_p, _p, _i32, _i32, _i32, _p, _up], C.c_int),
     "gnb_predict": ([_p, _i64, _i32, _i64, _p, _i32, _i32, _p, _i32, _i32, _p, _p, _p, _up],
                     C.c_int),
+    "gnb_predict_typed": ([_p, _i32, _i64, _i32, _i64, _p, _i32, _i32, _p, _i32, _i32, _p, _p,
+                           _p, _up], C.c_int),
     "gnb_predict_generic": ([_p, _i64, _i32, _i64, _p, _i32, _i32, _p, _i32, _i32, _p, _p, _p,
                              _up], C.c_int),
     "gnb_predict_host": ([_p, _i64, _i32, _i64, _p, _i32, _i32, _p, _i32, _i32, _p, _p, _p, _p,

@@ -64,8 +64,10 @@ CUtensorMapL2promotion l2_promotion() {
   return static_cast<CUtensorMapL2promotion>(v);
 }
 
-bool tma_ok(const void* base, int64_t ldx) {
-  return (reinterpret_cast<uintptr_t>(base) & 15u) == 0 && (ldx % 4) == 0;
+int elem_bytes(int x_type) { return x_type == GNB_X_U8 ? 1 : x_type == GNB_X_U16 ? 2 : 4; }
+
+bool tma_ok(const void* base, int64_t ldx, int x_type = GNB_X_I32) {
+  return (reinterpret_cast<uintptr_t>(base) & 15u) == 0 && (ldx * elem_bytes(x_type)) % 16 == 0;
 }
 
 }  // namespace
@@ -76,14 +78,19 @@ namespace gnb {
 // boxes of 32 columns x box_rows rows.  swizzle128: SWIZZLE_128B (predict)
 // or none (fit).
 static bool encode_map(CUtensorMap* map, const void* base, int64_t n_rows, int32_t n_cols,
-                       int64_t ldx, int box_rows, bool swizzle128) {
+                       int64_t ldx, int box_rows, bool swizzle128, int x_type = GNB_X_I32) {
   auto fn = encode_fn();
   if (fn == nullptr) return false;
+  const int eb = elem_bytes(x_type);
+  const CUtensorMapDataType dt = x_type == GNB_X_U8    ? CU_TENSOR_MAP_DATA_TYPE_UINT8
+                                 : x_type == GNB_X_U16 ? CU_TENSOR_MAP_DATA_TYPE_UINT16
+                                                       : CU_TENSOR_MAP_DATA_TYPE_INT32;
   cuuint64_t dims[2] = {static_cast<cuuint64_t>(n_cols), static_cast<cuuint64_t>(n_rows)};
-  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ldx) * 4};
-  cuuint32_t box[2] = {static_cast<cuuint32_t>(kChunkCols), static_cast<cuuint32_t>(box_rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ldx) * eb};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(kChunkBytesPerRow / eb),
+                       static_cast<cuuint32_t>(box_rows)};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_INT32, 2, const_cast<void*>(base), dims, strides,
+  CUresult r = fn(map, dt, 2, const_cast<void*>(base), dims, strides,
                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                   swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
                   l2_promotion(), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -154,15 +161,18 @@ static int check_predict(const int32_t* x, int64_t n_rows, int32_t F, int64_t ld
   return GNB_OK;
 }
 
-static int predict_device(const int32_t* x, int64_t n_rows, int32_t F, int64_t ldx,
+static int predict_device(const void* x, int x_type, int64_t n_rows, int32_t F, int64_t ldx,
                           const int32_t* size, int32_t width, int32_t limit,
                           const int32_t* route, int32_t S, int32_t C, const void* packed,
-                          int32_t* label, double* logpost, cudaStream_t stream) {
-  const bool use_tma = tma_ok(x, ldx) && encode_fn() != nullptr;
+                          int32_t* label, double* logpost, cudaStream_t stream,
+                          int force_generic = 0) {
+  const bool use_tma = !force_generic && tma_ok(x, ldx, x_type) && encode_fn() != nullptr;
+  const int eb = elem_bytes(x_type);
   for (int64_t r0 = 0; r0 < n_rows; r0 += kMaxRowsPerLaunch) {
     const int64_t n = std::min(kMaxRowsPerLaunch, n_rows - r0);
     PredictParams p{};
-    p.x = x + r0 * ldx;
+    p.x = static_cast<const uint8_t*>(x) + r0 * ldx * eb;
+    p.x_type = x_type;
     p.ldx = ldx;
     p.n_rows = n;
     p.n_features = F;
@@ -178,11 +188,11 @@ static int predict_device(const int32_t* x, int64_t n_rows, int32_t F, int64_t l
     CUtensorMap map;
     const CUtensorMap* mp = nullptr;
     if (use_tma) {
-      if (!encode_map(&map, p.x, n, F, ldx, predict_box_rows(C), true))
+      if (!encode_map(&map, p.x, n, F, ldx, predict_box_rows(C), true, x_type))
         return fail(GNB_ECUDA, "predict: cuTensorMapEncodeTiled failed");
       mp = &map;
     }
-    GNB_CUDA(predict_launch(mp, p, stream, 0), "predict launch");
+    GNB_CUDA(predict_launch(mp, p, stream, force_generic), "predict launch");
   }
   return GNB_OK;
 }
@@ -194,7 +204,23 @@ int gnb_predict(const int32_t* x, int64_t n_rows, int32_t n_features, int64_t ld
   int rc = check_predict(x, n_rows, n_features, ldx, size_bytes, group_size_bytes,
                          max_size_bytes, route, n_slots, n_classes, packed, label_out);
   if (rc) return rc;
-  return predict_device(x, n_rows, n_features, ldx, size_bytes, group_size_bytes,
+  return predict_device(x, GNB_X_I32, n_rows, n_features, ldx, size_bytes, group_size_bytes,
+                        max_size_bytes, route, n_slots, n_classes, packed, label_out,
+                        logpost_out, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int gnb_predict_typed(const void* x, int32_t x_type, int64_t n_rows, int32_t n_features,
+                      int64_t ldx, const int32_t* size_bytes, int32_t group_size_bytes,
+                      int32_t max_size_bytes, const int32_t* route, int32_t n_slots,
+                      int32_t n_classes, const void* packed, int32_t* label_out,
+                      double* logpost_out, uintptr_t stream) {
+  if (x_type != GNB_X_I32 && x_type != GNB_X_U16 && x_type != GNB_X_U8)
+    return fail(GNB_EINVAL, "predict: unknown x_type %d", x_type);
+  int rc = check_predict(static_cast<const int32_t*>(x), n_rows, n_features, ldx, size_bytes,
+                         group_size_bytes, max_size_bytes, route, n_slots, n_classes, packed,
+                         label_out);
+  if (rc) return rc;
+  return predict_device(x, x_type, n_rows, n_features, ldx, size_bytes, group_size_bytes,
                         max_size_bytes, route, n_slots, n_classes, packed, label_out,
                         logpost_out, reinterpret_cast<cudaStream_t>(stream));
 }
@@ -208,23 +234,9 @@ int gnb_predict_generic(const int32_t* x, int64_t n_rows, int32_t n_features, in
   int rc = check_predict(x, n_rows, n_features, ldx, size_bytes, group_size_bytes,
                          max_size_bytes, route, n_slots, n_classes, packed, label_out);
   if (rc) return rc;
-  PredictParams p{};
-  p.x = x;
-  p.ldx = ldx;
-  p.n_rows = n_rows;
-  p.n_features = n_features;
-  p.size = size_bytes;
-  p.width = group_size_bytes;
-  p.limit = max_size_bytes;
-  p.route = route;
-  p.n_slots = n_slots;
-  p.n_classes = n_classes;
-  p.prior = static_cast<const double*>(packed);
-  p.label = label_out;
-  p.logpost = logpost_out;
-  GNB_CUDA(predict_launch(nullptr, p, reinterpret_cast<cudaStream_t>(stream), 1),
-           "predict_generic launch");
-  return GNB_OK;
+  return predict_device(x, GNB_X_I32, n_rows, n_features, ldx, size_bytes, group_size_bytes,
+                        max_size_bytes, route, n_slots, n_classes, packed, label_out,
+                        logpost_out, reinterpret_cast<cudaStream_t>(stream), 1);
 }
 
 int gnb_fit_stats(const int32_t* x, int64_t n_rows, int32_t n_cols, int64_t ldx,
@@ -437,7 +449,7 @@ int gnb_predict_host(const int32_t* x, int64_t n_rows, int32_t n_features, int64
     GNB_CUDA(cudaMemcpyAsync(c->size[lane].p, size_bytes + r0, size_t(n) * 4,
                              cudaMemcpyHostToDevice, s),
              "H2D");
-    rc = predict_device(dx, n, n_features, ld, static_cast<int32_t*>(c->size[lane].p),
+    rc = predict_device(dx, GNB_X_I32, n, n_features, ld, static_cast<int32_t*>(c->size[lane].p),
                         group_size_bytes, max_size_bytes, static_cast<int32_t*>(c->route.p),
                         n_slots, n_classes, c->packed.p, static_cast<int32_t*>(c->label[lane].p),
                         logpost_out ? static_cast<double*>(c->logpost[lane].p) : nullptr, s);

@@ -1,7 +1,6 @@
 // Device-side building blocks for the sm_100a group-wise Naive Bayes kernels:
-// mbarrier / TMA (cp.async.bulk[.tensor]) inline PTX and the fp64 helpers
-// that keep the predict accumulation bit-identical to the reference's
-// Python loop (pkg/src/groupnb/classifier.py:143-147).
+// mbarrier / TMA (cp.async.bulk[.tensor]) inline PTX, L2 cache policies and
+// the SWIZZLE_128B address helper.
 #pragma once
 
 #include <cstdint>
@@ -106,16 +105,6 @@ __device__ __forceinline__ void prefetch_tensormap(const CUtensorMap* map) {
 // are 128 B: chunk index XOR (row mod 8).  Base must be 1024-B aligned.
 __device__ __forceinline__ uint32_t swz128(uint32_t r, uint32_t q) {
   return (r << 7) | (((q ^ r) & 7u) << 4);
-}
-
-// ------------------------------------------------------------ exact fp64
-// fl(x * ll) for 0 <= x < 2^32 with ONE FP64 op:  d = 2^52 + x is built by
-// bit-pasting (no conversion instruction); cc = -2^52 * ll is exact (power of
-// two scale), so fma(d, ll, cc) = round((2^52 + x) ll - 2^52 ll) = round(x ll),
-// i.e. exactly the reference's `n * ll` (a Python float multiply).
-__device__ __forceinline__ double exact_product(uint32_t x, double ll, double cc) {
-  const double d = __hiloint2double(0x43300000, static_cast<int>(x));
-  return __fma_rn(d, ll, cc);
 }
 
 }  // namespace gnb

@@ -11,11 +11,13 @@
 namespace gnb {
 
 struct PredictParams {
-  const int32_t* x;  // generic kernel only (TMA path reads through the tensor map)
-  int64_t ldx;
+  const void* x;     // generic kernel only (TMA path reads through the tensor map)
+  int32_t x_type;    // GNB_X_I32 / GNB_X_U16 / GNB_X_U8
+  int64_t ldx;       // row pitch in elements
   int64_t n_rows;
   int32_t n_features;
-  int32_t n_chunks;  // ceil(F / 32), set by predict_launch
+  int32_t n_chunks;  // ceil(F / features per 128-B box row), set by predict_launch
+  int32_t n_tab_blocks;  // 32-feature table blocks per slot, set by predict_launch
   const int32_t* size;
   int32_t width;
   int32_t limit;
@@ -23,7 +25,7 @@ struct PredictParams {
   int32_t n_slots;
   int32_t n_classes;
   const double* prior;  // packed: [S][CP]
-  const double* tab;    // packed: [S][NCH][32][CP][2], set by predict_launch
+  const double* tab;    // packed: [S][NB][32][CP][2], set by predict_launch
   int32_t* label;
   double* logpost;  // nullable, [N][C]
   int64_t n_tiles;  // set by predict_launch

@@ -5,19 +5,20 @@
 // (pkg/src/groupnb/classifier.py:132-158).
 //
 // Data path:
-//   * X [N, F] int32 is streamed from HBM exactly once by TMA: 2-D boxes of
-//     32 columns (128 B) x ROWS rows, SWIZZLE_128B, through a STAGES-deep
-//     mbarrier ring filled by one producer warp.
+//   * X [N, F] counts (int32, or uint16 / uint8 when the counts fit -- the same
+//     integers, fewer bytes) are streamed from HBM exactly once by TMA: 2-D
+//     boxes of 128 B (32/64/128 features) x ROWS rows, SWIZZLE_128B, through a
+//     STAGES-deep mbarrier ring filled by one producer warp.
 //   * each consumer thread owns one row and walks its features in FeatureSet
-//     order: acc_c = acc_c + x * ll_c with the product computed by one DFMA
-//     (exact_product) and the add by one DADD -- the same two roundings as the
-//     reference's `score += n * ll`, so log-posteriors are bit-identical.
+//     order: acc_c = acc_c + x * ll_c as one DMUL (x converted exactly by
+//     I2F.F64) and one DADD -- the same two roundings as the reference's
+//     `score += n * ll`, so log-posteriors are bit-identical.
 //   * the producer routes the tile's rows (size -> group -> slot, the whole
 //     route table lookup of engine.py:202) and, when every valid row of the tile
 //     shares a slot (G=1, or rows grouped by size group as the reference's
-//     GroupedCorpus orders them), also bulk-copies that slot's 32-feature table
-//     slice next to the X box, so table reads are smem broadcasts.  Mixed tiles
-//     read per-row tables through L1 instead.  All groups: one launch.
+//     GroupedCorpus orders them), also bulk-copies that slot's table slice for
+//     the chunk next to the X box, so table reads are smem broadcasts.  Mixed
+//     tiles read per-row tables through L1 instead.  All groups: one launch.
 //   * argmax (ties -> lowest class index = benign) and the out-of-range status
 //     are fused into the epilogue; label (+ optional log-posteriors) written
 //     once, coalesced.
@@ -32,13 +33,24 @@
 namespace gnb {
 
 // ------------------------------------------------------------------ tables
-// packed = [prior: S][CP] | [tab: S][NCH][32 features][CP][{ll, -2^52 ll}]
+// packed = [prior: S][CP] | [tab: S][NB][32 features][CP] log-likelihoods.
+// NB = ceil(F/32) rounded up to a multiple of 4, so a 128-feature chunk (uint8
+// X) of any slot is one in-bounds contiguous block; padding entries are 0.
+constexpr int kTabBlockFeatures = 32;
+constexpr int kTabBlockAlign = 4;
+
+int table_blocks(int F) {
+  const int nb = (F + kTabBlockFeatures - 1) / kTabBlockFeatures;
+  return (nb + kTabBlockAlign - 1) / kTabBlockAlign * kTabBlockAlign;
+}
+
 __global__ void pack_tables_kernel(const double* __restrict__ log_prior,
                                    const double* __restrict__ log_lik, int S, int C, int F,
-                                   int CP, int NCH, double* __restrict__ prior_out,
+                                   int CP, int NB, double* __restrict__ prior_out,
                                    double* __restrict__ tab_out) {
   const int64_t total_prior = static_cast<int64_t>(S) * CP;
-  const int64_t total_tab = static_cast<int64_t>(S) * NCH * kChunkCols * CP;
+  const int64_t per_slot = static_cast<int64_t>(NB) * kTabBlockFeatures * CP;
+  const int64_t total_tab = S * per_slot;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
        i < total_prior + total_tab; i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     if (i < total_prior) {
@@ -47,63 +59,80 @@ __global__ void pack_tables_kernel(const double* __restrict__ log_prior,
     } else {
       const int64_t k = i - total_prior;
       const int c = static_cast<int>(k % CP);
-      const int j = static_cast<int>((k / CP) % (NCH * kChunkCols));  // feature
-      const int s = static_cast<int>(k / (static_cast<int64_t>(CP) * NCH * kChunkCols));
+      const int j = static_cast<int>((k / CP) % (NB * kTabBlockFeatures));  // feature
+      const int s = static_cast<int>(k / per_slot);
       double ll = 0.0;
       if (c < C && j < F) ll = log_lik[(static_cast<int64_t>(s) * C + c) * F + j];
-      tab_out[2 * k] = ll;
-      tab_out[2 * k + 1] = -0x1p52 * ll;  // exact: power-of-two scale
+      tab_out[k] = ll;
     }
+  }
+}
+
+// ------------------------------------------------------------------ element types
+template <typename T>
+struct Elem {
+  static constexpr int kPerQuad = 16 / static_cast<int>(sizeof(T));   // per 16-B chunk
+  static constexpr int kPerRow = 128 / static_cast<int>(sizeof(T));   // per 128-B box row
+  static constexpr bool kSigned = false;
+};
+template <>
+struct Elem<int32_t> {
+  static constexpr int kPerQuad = 4, kPerRow = 32;
+  static constexpr bool kSigned = true;  // negative counts are flagged, not scored
+};
+
+// Element e (0 <= e < kPerQuad) of a 16-B chunk as a double.  The conversion
+// is exact (counts < 2^32) and runs on the conversion unit (I2F.F64; for
+// uint8/uint16 with a byte/half-word source select), so the product below is
+// ONE DMUL rounding, exactly the reference's `n * ll` (a Python float multiply).
+template <typename T>
+__device__ __forceinline__ double converted(const uint4& v, int e) {
+  constexpr int sz = static_cast<int>(sizeof(T));
+  const uint32_t w = (e * sz) < 4 ? v.x : (e * sz) < 8 ? v.y : (e * sz) < 12 ? v.z : v.w;
+  if constexpr (sz == 4) {
+    return __uint2double_rn(w);
+  } else {
+    constexpr int bits = 8 * sz;
+    return __uint2double_rn((w >> ((e * bits) & 31)) & ((1u << bits) - 1u));
   }
 }
 
 // ------------------------------------------------------------------ inner loops
-template <int CP>
-struct SmemTab {
-  const double* p;
-  __device__ __forceinline__ double2 get(int idx) const {
-    return *reinterpret_cast<const double2*>(p + 2 * idx);
-  }
-};
-template <int CP>
 struct GlobalTab {
   const double* p;
-  __device__ __forceinline__ double2 get(int idx) const {
-    return __ldg(reinterpret_cast<const double2*>(p + 2 * idx));
-  }
+  __device__ __forceinline__ double get(int idx) const { return __ldg(p + idx); }
 };
 
-// 4 consecutive features (one 16-B smem chunk) of one row, all classes.
-template <int CP, typename Tab>
+// One 16-B chunk (kPerQuad consecutive features) of one row, all classes.
+template <int CP, typename T, typename Tab>
 __device__ __forceinline__ void score_quad(double (&acc)[CP], const uint4 v, const Tab& tab,
                                            int feat0) {
-  const uint32_t xs[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-  for (int e = 0; e < 4; ++e) {
+  for (int e = 0; e < Elem<T>::kPerQuad; ++e) {
+    const double xd = converted<T>(v, e);
 #pragma unroll
-    for (int c = 0; c < CP; ++c) {
-      const double2 t = tab.get((feat0 + e) * CP + c);
-      acc[c] = __dadd_rn(acc[c], exact_product(xs[e], t.x, t.y));
-    }
+    for (int c = 0; c < CP; ++c)
+      acc[c] = __dadd_rn(acc[c], __dmul_rn(xd, tab.get((feat0 + e) * CP + c)));
   }
 }
 
-template <int CP, typename Tab>
+template <int CP, typename T, typename Tab>
 __device__ __forceinline__ void score_chunk(double (&acc)[CP], const uint8_t* box, uint32_t row,
                                             const Tab& tab, int nq, uint32_t& neg) {
+  constexpr int EQ = Elem<T>::kPerQuad;
   if (nq == 8) {
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
       const uint4 v = *reinterpret_cast<const uint4*>(box + swz128(row, q));
-      neg |= v.x | v.y | v.z | v.w;
-      score_quad<CP>(acc, v, tab, 4 * q);
+      if (Elem<T>::kSigned) neg |= v.x | v.y | v.z | v.w;
+      score_quad<CP, T>(acc, v, tab, EQ * q);
     }
   } else {
 #pragma unroll 1
     for (int q = 0; q < nq; ++q) {
       const uint4 v = *reinterpret_cast<const uint4*>(box + swz128(row, q));
-      neg |= v.x | v.y | v.z | v.w;
-      score_quad<CP>(acc, v, tab, 4 * q);
+      if (Elem<T>::kSigned) neg |= v.x | v.y | v.z | v.w;
+      score_quad<CP, T>(acc, v, tab, EQ * q);
     }
   }
 }
@@ -129,29 +158,27 @@ __device__ __forceinline__ void write_row(const PredictParams& p, int64_t r, int
   }
   p.label[r] = lab;
   if (p.logpost != nullptr) {
+    const double nan = __longlong_as_double(0x7ff8000000000000ll);
     double* out = p.logpost + r * p.n_classes;
     if (p.n_classes == 2 && CP == 2) {
-      const double2 v = slot < 0 ? make_double2(__longlong_as_double(0x7ff8000000000000ll),
-                                                __longlong_as_double(0x7ff8000000000000ll))
-                                 : make_double2(acc[0], acc[CP > 1 ? 1 : 0]);
+      const double2 v = slot < 0 ? make_double2(nan, nan) : make_double2(acc[0], acc[CP - 1]);
       *reinterpret_cast<double2*>(out) = v;
     } else {
 #pragma unroll
       for (int c = 0; c < CP; ++c)
-        if (c < p.n_classes) out[c] = slot < 0 ? __longlong_as_double(0x7ff8000000000000ll) : acc[c];
+        if (c < p.n_classes) out[c] = slot < 0 ? nan : acc[c];
     }
   }
 }
 
 // ------------------------------------------------------------------ TMA kernel
 // A consumer thread owns R rows of the tile (rows lane + 32*(w + NW*i)), so one
-// broadcast table read feeds R*CP independent accumulator chains and the
-// DADD latency of each chain is hidden behind the others.
-template <int CP, int R, int NW, int STAGES>
+// broadcast table read feeds R*CP independent accumulator chains.
+template <int CP, typename T, int R, int NW, int STAGES>
 struct PredictSmem {
-  static constexpr int kRows = NW * 32 * R;                      // rows per tile (<= 256)
-  static constexpr int kXBytes = kRows * kChunkBytesPerRow;        // one box
-  static constexpr int kTabBytes = kChunkCols * CP * 2 * 8;         // one table slice
+  static constexpr int kRows = NW * 32 * R;                          // rows per tile (<= 256)
+  static constexpr int kXBytes = kRows * kChunkBytesPerRow;            // one box
+  static constexpr int kTabBytes = Elem<T>::kPerRow * CP * 8;          // one table slice
   static constexpr int kHdrBytes = ((4 + kRows * 4) + 15) / 16 * 16;
   static constexpr int kX = 0;
   static constexpr int kTab = kX + STAGES * kXBytes;
@@ -167,29 +194,41 @@ struct StageHdr {
   int row_slot[1];
 };
 
+// Table of slot s, chunk ch (kPerRow features per chunk).
+template <int CP, typename T>
+__device__ __forceinline__ const double* chunk_table(const PredictParams& p, int s, int ch) {
+  constexpr int blocks_per_chunk = Elem<T>::kPerRow / kTabBlockFeatures;
+  return p.tab + (static_cast<int64_t>(s) * p.n_tab_blocks + ch * blocks_per_chunk) *
+                     (kTabBlockFeatures * CP);
+}
+
 // Uniform tile: the chunk's table slice is in smem and shared by all R rows.
-template <int CP, int R>
+template <int CP, typename T, int R>
 __device__ __forceinline__ void score_chunk_uniform(double (&acc)[R][CP], const uint8_t* box,
                                                     const uint32_t (&rows)[R], const double* tab,
                                                     int nq, uint32_t (&neg)[R]) {
+  constexpr int EQ = Elem<T>::kPerQuad;
   auto quad = [&](int q) {
     uint4 v[R];
 #pragma unroll
     for (int i = 0; i < R; ++i) {
       v[i] = *reinterpret_cast<const uint4*>(box + swz128(rows[i], q));
-      neg[i] |= v[i].x | v[i].y | v[i].z | v[i].w;
+      if (Elem<T>::kSigned) neg[i] |= v[i].x | v[i].y | v[i].z | v[i].w;
     }
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      double2 t[CP];
+    for (int e = 0; e < EQ; ++e) {
+      double t[CP];  // one broadcast LDS.128 per 2 classes
 #pragma unroll
-      for (int c = 0; c < CP; ++c)
-        t[c] = *reinterpret_cast<const double2*>(tab + 2 * ((4 * q + e) * CP + c));
+      for (int c = 0; c < CP; c += 2) {
+        const double2 t2 = *reinterpret_cast<const double2*>(tab + (EQ * q + e) * CP + c);
+        t[c] = t2.x;
+        t[c + 1] = t2.y;
+      }
 #pragma unroll
       for (int i = 0; i < R; ++i) {
-        const uint32_t x = e == 0 ? v[i].x : e == 1 ? v[i].y : e == 2 ? v[i].z : v[i].w;
+        const double xd = converted<T>(v[i], e);
 #pragma unroll
-        for (int c = 0; c < CP; ++c) acc[i][c] = __dadd_rn(acc[i][c], exact_product(x, t[c].x, t[c].y));
+        for (int c = 0; c < CP; ++c) acc[i][c] = __dadd_rn(acc[i][c], __dmul_rn(xd, t[c]));
       }
     }
   };
@@ -203,29 +242,30 @@ __device__ __forceinline__ void score_chunk_uniform(double (&acc)[R][CP], const 
 }
 
 // Mixed tile: every row reads its own slot's table through L1.
-template <int CP, int R>
-__device__ __forceinline__ void score_chunk_mixed(double (&acc)[R][CP], const uint8_t* box,
-                                                  const uint32_t (&rows)[R], const int (&slot)[R],
-                                                  const double* tab_all, int NCH, int ch, int nq,
+template <int CP, typename T, int R>
+__device__ __forceinline__ void score_chunk_mixed(const PredictParams& p, double (&acc)[R][CP],
+                                                  const uint8_t* box, const uint32_t (&rows)[R],
+                                                  const int (&slot)[R], int ch, int nq,
                                                   uint32_t (&neg)[R]) {
 #pragma unroll
   for (int i = 0; i < R; ++i) {
-    const GlobalTab<CP> tab{tab_all + (static_cast<int64_t>(max(slot[i], 0)) * NCH + ch) *
-                                          (kChunkCols * CP * 2)};
+    const GlobalTab tab{chunk_table<CP, T>(p, max(slot[i], 0), ch)};
     double a[CP];
 #pragma unroll
     for (int c = 0; c < CP; ++c) a[c] = acc[i][c];
-    score_chunk<CP>(a, box, rows[i], tab, nq, neg[i]);
+    score_chunk<CP, T>(a, box, rows[i], tab, nq, neg[i]);
 #pragma unroll
     for (int c = 0; c < CP; ++c) acc[i][c] = a[c];
   }
 }
 
-template <int CP, int R, int NW, int STAGES>
+template <int CP, typename T, int R, int NW, int STAGES>
 __global__ void __launch_bounds__((NW + 1) * 32)
     predict_tma_kernel(const __grid_constant__ CUtensorMap xmap, const PredictParams p) {
-  using L = PredictSmem<CP, R, NW, STAGES>;
+  using L = PredictSmem<CP, T, R, NW, STAGES>;
   constexpr int ROWS = L::kRows;
+  constexpr int CF = Elem<T>::kPerRow;
+  constexpr int EQ = Elem<T>::kPerQuad;
   extern __shared__ uint8_t smem_raw[];
   // 1024-B alignment for SWIZZLE_128B, keeping the pointer in the shared window
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -285,14 +325,11 @@ __global__ void __launch_bounds__((NW + 1) * 32)
         if (lane == 0) {
           const uint32_t bytes = L::kXBytes + (tile_slot >= 0 ? L::kTabBytes : 0);
           mbar_arrive_expect_tx(&full[stage], bytes);
-          tma_load_2d(smem + L::kX + stage * L::kXBytes, &xmap, ch * kChunkCols,
+          tma_load_2d(smem + L::kX + stage * L::kXBytes, &xmap, ch * CF,
                       static_cast<int32_t>(r0), &full[stage], pol_x);
-          if (tile_slot >= 0) {
-            const double* src =
-                p.tab + (static_cast<int64_t>(tile_slot) * NCH + ch) * (kChunkCols * CP * 2);
-            bulk_load(smem + L::kTab + stage * L::kTabBytes, src, L::kTabBytes, &full[stage],
-                      pol_t);
-          }
+          if (tile_slot >= 0)
+            bulk_load(smem + L::kTab + stage * L::kTabBytes, chunk_table<CP, T>(p, tile_slot, ch),
+                      L::kTabBytes, &full[stage], pol_t);
         } else {
           mbar_arrive(&full[stage]);
         }
@@ -329,15 +366,15 @@ __global__ void __launch_bounds__((NW + 1) * 32)
             for (int c = 0; c < CP; ++c) acc[i][c] = __ldg(p.prior + s * CP + c);
           }
         }
-        const int nf = min(kChunkCols, p.n_features - ch * kChunkCols);
-        const int nq = (nf + 3) >> 2;
+        const int nf = min(CF, p.n_features - ch * CF);
+        const int nq = (nf + EQ - 1) / EQ;
         const uint8_t* box = smem + L::kX + stage * L::kXBytes;
         if (ts >= 0) {
-          score_chunk_uniform<CP, R>(
+          score_chunk_uniform<CP, T, R>(
               acc, box, rows, reinterpret_cast<const double*>(smem + L::kTab + stage * L::kTabBytes),
               nq, neg);
         } else {
-          score_chunk_mixed<CP, R>(acc, box, rows, slot, p.tab, NCH, ch, nq, neg);
+          score_chunk_mixed<CP, T, R>(p, acc, box, rows, slot, ch, nq, neg);
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[stage]);
@@ -356,11 +393,11 @@ __global__ void __launch_bounds__((NW + 1) * 32)
 }
 
 // ------------------------------------------------------------------ generic kernel
-// Any layout (ldx not a multiple of 4, unaligned X): one thread per row,
-// loads through L1.  Same arithmetic, same results; slower.
-template <int CP>
+// Any layout (unaligned X, row pitch not a multiple of 16 B): one thread per
+// row, loads through L1.  Same arithmetic, same results; slower.
+template <int CP, typename T>
 __global__ void __launch_bounds__(256) predict_generic_kernel(const PredictParams p) {
-  const int NCH = p.n_chunks;
+  const T* xbase = static_cast<const T*>(p.x);
   for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r < p.n_rows;
        r += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int sz = p.size[r];
@@ -369,30 +406,28 @@ __global__ void __launch_bounds__(256) predict_generic_kernel(const PredictParam
     double acc[CP];
 #pragma unroll
     for (int c = 0; c < CP; ++c) acc[c] = p.prior[s * CP + c];
-    const int32_t* row = p.x + r * p.ldx;
+    const T* row = xbase + r * p.ldx;
     uint32_t neg = 0;
+    const GlobalTab tab{p.tab + static_cast<int64_t>(s) * p.n_tab_blocks *
+                                    (kTabBlockFeatures * CP)};
     for (int j = 0; j < p.n_features; ++j) {
       const uint32_t x = static_cast<uint32_t>(__ldg(row + j));
-      neg |= x;
-      const GlobalTab<CP> tab{p.tab +
-                              (static_cast<int64_t>(s) * NCH + j / kChunkCols) *
-                                  (kChunkCols * CP * 2)};
+      if (Elem<T>::kSigned) neg |= x;
+      const double xd = __uint2double_rn(x);
 #pragma unroll
-      for (int c = 0; c < CP; ++c) {
-        const double2 t = tab.get((j % kChunkCols) * CP + c);
-        acc[c] = __dadd_rn(acc[c], exact_product(x, t.x, t.y));
-      }
+      for (int c = 0; c < CP; ++c) acc[c] = __dadd_rn(acc[c], __dmul_rn(xd, tab.get(j * CP + c)));
     }
     write_row<CP>(p, r, slot, neg, acc);
   }
 }
 
 // ------------------------------------------------------------------ launchers
-template <int CP, int R, int NW, int STAGES>
+template <int CP, typename T, int R, int NW, int STAGES>
 static cudaError_t launch_tma(const CUtensorMap& map, PredictParams p, cudaStream_t stream) {
-  using L = PredictSmem<CP, R, NW, STAGES>;
-  auto kern = predict_tma_kernel<CP, R, NW, STAGES>;
+  using L = PredictSmem<CP, T, R, NW, STAGES>;
+  auto kern = predict_tma_kernel<CP, T, R, NW, STAGES>;
   p.n_tiles = (p.n_rows + L::kRows - 1) / L::kRows;
+  p.n_chunks = (p.n_features + Elem<T>::kPerRow - 1) / Elem<T>::kPerRow;
   static int per_sm = 0;  // resident CTAs per SM for this instantiation
   static int sms = 0;
   if (per_sm == 0) {
@@ -413,12 +448,12 @@ static cudaError_t launch_tma(const CUtensorMap& map, PredictParams p, cudaStrea
   return cudaGetLastError();
 }
 
-template <int CP>
+template <int CP, typename T>
 static cudaError_t launch_generic(const PredictParams& p, cudaStream_t stream) {
   const int64_t blocks64 = (p.n_rows + 255) / 256;
   const int blocks = static_cast<int>(blocks64 < 148 * 16 ? blocks64 : 148 * 16);
   if (blocks == 0) return cudaSuccess;
-  predict_generic_kernel<CP><<<blocks, 256, 0, stream>>>(p);
+  predict_generic_kernel<CP, T><<<blocks, 256, 0, stream>>>(p);
   return cudaGetLastError();
 }
 
@@ -426,33 +461,31 @@ int class_pad(int C) { return C <= 2 ? 2 : C <= 4 ? 4 : C <= 8 ? 8 : 16; }
 
 size_t packed_bytes(int S, int C, int F) {
   const int CP = class_pad(C);
-  const int NCH = (F + kChunkCols - 1) / kChunkCols;
   return static_cast<size_t>(S) * CP * 8 +
-         static_cast<size_t>(S) * NCH * kChunkCols * CP * 2 * 8;
+         static_cast<size_t>(S) * table_blocks(F) * kTabBlockFeatures * CP * 8;
 }
 
 cudaError_t pack_tables(const double* log_prior, const double* log_lik, int S, int C, int F,
                         void* packed, cudaStream_t stream) {
   const int CP = class_pad(C);
-  const int NCH = (F + kChunkCols - 1) / kChunkCols;
+  const int NB = table_blocks(F);
   double* prior = static_cast<double*>(packed);
   double* tab = prior + static_cast<int64_t>(S) * CP;
-  const int64_t total = static_cast<int64_t>(S) * CP * (1 + NCH * kChunkCols);
+  const int64_t total = static_cast<int64_t>(S) * CP * (1 + NB * kTabBlockFeatures);
   const int blocks = static_cast<int>((total + 255) / 256 < 4096 ? (total + 255) / 256 : 4096);
   pack_tables_kernel<<<blocks > 0 ? blocks : 1, 256, 0, stream>>>(log_prior, log_lik, S, C, F,
-                                                                   CP, NCH, prior, tab);
+                                                                   CP, NB, prior, tab);
   return cudaGetLastError();
 }
 
-// K-PRED geometry per class pad: rows per thread (R), consumer warps (NW),
-// ring stages.  CP=2 keeps a few tuned variants selectable with
-// GNB_PRED_VARIANT (profiling only); the default is variant 0, measured best
-// on B200 (profiles/r01_tuning.md): 16-KB stages, 2 deep, 6 CTAs per SM.
+// K-PRED geometry for C = 2: rows per thread (R), consumer warps (NW), ring
+// stages; a few variants selectable with GNB_PRED_VARIANT (profiling only).
+// Default (variant 0) measured best on B200 for int32 X
+// (profiles/r01_tuning.md): 16-KB stages, 2 deep, 6 CTAs per SM.
 struct PredVariant {
   int R, NW, STAGES;
 };
-static const PredVariant kCp2Variants[] = {
-    {1, 4, 2}, {1, 4, 3}, {2, 2, 2}, {2, 4, 2}};
+static const PredVariant kCp2Variants[] = {{1, 4, 2}, {1, 4, 3}, {2, 2, 2}, {2, 4, 2}};
 
 static int cp2_variant() {
   static int v = -1;
@@ -473,37 +506,47 @@ int predict_box_rows(int n_classes) {
   return CP == 4 ? 2 * 4 * 32 : 128;
 }
 
+template <typename T>
+static cudaError_t launch_typed(const CUtensorMap* map, const PredictParams& p, int CP,
+                                cudaStream_t stream) {
+  if (map != nullptr) {
+    switch (CP) {
+      case 2:
+        switch (cp2_variant()) {
+          case 1: return launch_tma<2, T, 1, 4, 3>(*map, p, stream);
+          case 2: return launch_tma<2, T, 2, 2, 2>(*map, p, stream);
+          case 3: return launch_tma<2, T, 2, 4, 2>(*map, p, stream);
+          default: return launch_tma<2, T, 1, 4, 2>(*map, p, stream);
+        }
+      case 4: return launch_tma<4, T, 2, 4, 3>(*map, p, stream);
+      case 8: return launch_tma<8, T, 1, 4, 4>(*map, p, stream);
+      default: return launch_tma<16, T, 1, 4, 4>(*map, p, stream);
+    }
+  }
+  switch (CP) {
+    case 2: return launch_generic<2, T>(p, stream);
+    case 4: return launch_generic<4, T>(p, stream);
+    case 8: return launch_generic<8, T>(p, stream);
+    default: return launch_generic<16, T>(p, stream);
+  }
+}
+
 cudaError_t predict_launch(const CUtensorMap* map, PredictParams p, cudaStream_t stream,
                            int force_generic) {
   const int CP = class_pad(p.n_classes);
-  p.n_chunks = (p.n_features + kChunkCols - 1) / kChunkCols;
   static int x_policy = -1;  // GNB_X_POLICY=1: X loads evict_first (profiling; default normal)
   if (x_policy < 0) {
     const char* e = getenv("GNB_X_POLICY");
     x_policy = e ? atoi(e) : 0;
   }
   p.x_policy = x_policy;
-  const double* prior = p.prior;
-  p.tab = prior + static_cast<int64_t>(p.n_slots) * CP;
-  if (map != nullptr && !force_generic) {
-    switch (CP) {
-      case 2:
-        switch (cp2_variant()) {
-          case 1: return launch_tma<2, 1, 4, 3>(*map, p, stream);
-          case 2: return launch_tma<2, 2, 2, 2>(*map, p, stream);
-          case 3: return launch_tma<2, 2, 4, 2>(*map, p, stream);
-          default: return launch_tma<2, 1, 4, 2>(*map, p, stream);
-        }
-      case 4: return launch_tma<4, 2, 4, 3>(*map, p, stream);
-      case 8: return launch_tma<8, 1, 4, 4>(*map, p, stream);
-      default: return launch_tma<16, 1, 4, 4>(*map, p, stream);
-    }
-  }
-  switch (CP) {
-    case 2: return launch_generic<2>(p, stream);
-    case 4: return launch_generic<4>(p, stream);
-    case 8: return launch_generic<8>(p, stream);
-    default: return launch_generic<16>(p, stream);
+  p.n_tab_blocks = table_blocks(p.n_features);
+  p.tab = p.prior + static_cast<int64_t>(p.n_slots) * CP;
+  if (force_generic) map = nullptr;
+  switch (p.x_type) {
+    case GNB_X_U16: return launch_typed<uint16_t>(map, p, CP, stream);
+    case GNB_X_U8: return launch_typed<uint8_t>(map, p, CP, stream);
+    default: return launch_typed<int32_t>(map, p, CP, stream);
   }
 }
 

@@ -35,8 +35,14 @@ def _dev(t: torch.Tensor, name: str, dtype) -> int:
     return t.data_ptr()
 
 
-def _rows(x: torch.Tensor, name: str = "x"):
-    ptr = _dev(x, name, torch.int32)
+_X_TYPES = {torch.int32: N.X_I32, torch.uint16: N.X_U16, torch.uint8: N.X_U8}
+
+
+def _rows(x: torch.Tensor, name: str = "x", dtypes=(torch.int32,)):
+    if isinstance(x, torch.Tensor) and x.dtype in dtypes:
+        ptr = _dev(x, name, x.dtype)
+    else:
+        ptr = _dev(x, name, dtypes[0])
     if x.dim() != 2 or (x.numel() > 0 and x.shape[1] > 1 and x.stride(1) != 1):
         raise InvalidConfigError(f"{name} must be a row-major [N, F] int32 matrix")
     return ptr, x.shape[0], x.shape[1], max(x.stride(0), x.shape[1])
@@ -97,8 +103,9 @@ def predict(x: torch.Tensor, size_bytes: torch.Tensor, tables: DeviceTables, *,
     -2 negative count) and, if requested, log-posteriors [N, C] fp64.
 
     Row n of x holds its routed model's feature counts in FeatureSet order
-    (extra columns beyond the model's features must be 0)."""
-    xp, n, F, ldx = _rows(x)
+    (extra columns beyond the model's features must be 0).  x may be int32,
+    uint16 or uint8 (the same counts in fewer bytes; identical results)."""
+    xp, n, F, ldx = _rows(x, dtypes=tuple(_X_TYPES))
     if F != tables.n_features:
         raise InvalidConfigError(f"x has {F} columns, tables have {tables.n_features} features")
     sp = _vec(size_bytes, n, "size_bytes")
@@ -108,12 +115,32 @@ def predict(x: torch.Tensor, size_bytes: torch.Tensor, tables: DeviceTables, *,
     if logpost:
         lp = logpost_out if logpost_out is not None else torch.empty(
             (n, tables.n_classes), dtype=torch.float64, device=dev)
-    fn = N.lib.gnb_predict_generic if generic else N.lib.gnb_predict
-    N.check(fn(xp, n, F, ldx, sp, tables.group_size_bytes, tables.max_size_bytes,
-               tables.route.data_ptr(), tables.n_slots, tables.n_classes,
-               tables.packed.data_ptr(), _vec(label, n, "label_out"),
-               lp.data_ptr() if lp is not None else None, _stream(stream)), "gnb_predict")
+    args = (n, F, ldx, sp, tables.group_size_bytes, tables.max_size_bytes,
+            tables.route.data_ptr(), tables.n_slots, tables.n_classes, tables.packed.data_ptr(),
+            _vec(label, n, "label_out"), lp.data_ptr() if lp is not None else None,
+            _stream(stream))
+    if generic:
+        if x.dtype != torch.int32:
+            raise InvalidConfigError("generic=True is the int32 L1 test path")
+        N.check(N.lib.gnb_predict_generic(xp, *args), "gnb_predict_generic")
+    else:
+        N.check(N.lib.gnb_predict_typed(xp, _X_TYPES[x.dtype], *args), "gnb_predict_typed")
     return label, lp
+
+
+def narrowest(x: torch.Tensor) -> torch.Tensor:
+    """The same non-negative counts in the narrowest lossless dtype (uint8 /
+    uint16 / int32) -- 4x / 2x fewer bytes for K-PRED to stream."""
+    if x.numel() == 0:
+        return x
+    lo, hi = int(x.min()), int(x.max())
+    if lo < 0:
+        return x
+    if hi < 256:
+        return x.to(torch.uint8)
+    if hi < 65536:
+        return x.to(torch.uint16)
+    return x
 
 
 def gather_features(x_vocab: torch.Tensor, size_bytes: torch.Tensor, tables: DeviceTables,

@@ -31,7 +31,9 @@ def test_predict_rejects_bad_geometry(F, ldx, width, limit, S, C):
 
 
 def test_packed_table_bytes():
-    assert N.lib.gnb_packed_table_bytes(1, 2, 32) == 1 * 2 * 8 + 1 * 1 * 32 * 2 * 2 * 8
+    # prior [S][CP] + log-lik [S][NB][32][CP], NB = ceil(F/32) padded to a multiple of 4
+    assert N.lib.gnb_packed_table_bytes(1, 2, 32) == 1 * 2 * 8 + 1 * 4 * 32 * 2 * 8
+    assert N.lib.gnb_packed_table_bytes(3, 5, 200) == 3 * 8 * 8 + 3 * 8 * 32 * 8 * 8
     assert N.lib.gnb_packed_table_bytes(0, 2, 32) == 0
     assert N.lib.gnb_packed_table_bytes(1, 17, 32) == 0
 

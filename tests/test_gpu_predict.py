@@ -193,3 +193,38 @@ def test_gather_features_matches_oracle():
     assert lab.cpu().numpy().tolist() == want.tolist()
     ok = want >= 0
     assert lp.cpu().numpy()[ok].tobytes() == wlp[ok].tobytes()
+
+
+@pytest.mark.parametrize("dtype,hi", [(torch.uint8, 256), (torch.uint16, 65536)])
+@pytest.mark.parametrize("F", [1, 16, 31, 64, 100, 128, 129, 256, 300])
+@pytest.mark.parametrize("C", [2, 5])
+def test_narrow_dtypes_bit_exact(dtype, hi, F, C):
+    """uint8 / uint16 X: same counts, fewer bytes, identical results (TMA and L1 paths)."""
+    rng = np.random.default_rng(F * 7 + C)
+    prior, ll, route = _tables(rng, 3, C, F, 4)
+    N = 2000
+    x = rng.integers(0, hi, size=(N, F))
+    x[::5] = rng.poisson(1.0, size=(len(x[::5]), F))
+    size = rng.integers(-5, 4 * 100 + 5, size=N)
+    want, wlp = O.predict_dense(x, size, route, prior, ll, width=100, limit=400)
+    dev = torch.device("cuda")
+    t = dense.DeviceTables.build(prior, ll, route, group_size_bytes=100, max_size_bytes=400)
+    sd = torch.from_numpy(size.astype(np.int32)).to(dev)
+    esz = torch.tensor([], dtype=dtype).element_size()
+    ld_tma = (F * esz + 15) // 16 * 16 // esz
+    for ld in (ld_tma, F):                     # aligned pitch -> TMA; F may force the L1 path
+        base = torch.zeros((N, ld), dtype=torch.int32, device=dev)
+        base[:, :F] = torch.from_numpy(x.astype(np.int32)).to(dev)
+        xd = base.to(dtype)[:, :F]
+        lab, lp = dense.predict(xd, sd, t)
+        torch.cuda.synchronize()
+        assert lab.cpu().numpy().tolist() == want.tolist()
+        ok = want >= 0
+        assert lp.cpu().numpy()[ok].tobytes() == wlp[ok].tobytes()
+
+
+def test_narrowest_roundtrip():
+    x = torch.tensor([[0, 5, 255]], dtype=torch.int32, device="cuda")
+    assert dense.narrowest(x).dtype == torch.uint8
+    assert dense.narrowest(x * 100).dtype == torch.uint16
+    assert dense.narrowest(x * 1000).dtype == torch.int32
