@@ -123,6 +123,15 @@ int gnb_gather_features(const int32_t* x_vocab, int64_t n_rows, int32_t n_vocab,
                         const int32_t* n_features, int32_t n_slots, int32_t max_features,
                         int32_t* x_out, int64_t ldo, uintptr_t stream);
 
+/* gnb_predict_host for host rows stored as x_type (GNB_X_I32/U16/U8), ldx in
+ * elements: narrow storage moves 2x/4x fewer bytes over PCIe. */
+int gnb_predict_host_typed(const void* x, int32_t x_type, int64_t n_rows, int32_t n_features,
+                           int64_t ldx, const int32_t* size_bytes, int32_t group_size_bytes,
+                           int32_t max_size_bytes, const int32_t* route, int32_t n_slots,
+                           int32_t n_classes, const double* log_prior, const double* log_lik,
+                           int32_t* label_out, double* logpost_out, int32_t device,
+                           int64_t* elapsed_ns);
+
 /* ------------------------------------------------------------------ fit
  * Replaces: the sample x histogram count loops of features.class_frequency
  *           (pkg/src/groupnb/features.py:48-53) and classifier.train_group

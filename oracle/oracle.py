@@ -238,6 +238,8 @@ def c_oracle():
         lib = C.CDLL(path)
         p, i32, i64 = C.c_void_p, C.c_int32, C.c_int64
         lib.oracle_predict.argtypes = [p, i64, i32, i64, p, i32, i32, p, i32, p, p, p, p, i32]
+        lib.oracle_predict_typed.argtypes = [p, i32, i64, i32, i64, p, i32, i32, p, i32, p, p, p,
+                                             p, i32]
         lib.oracle_fit_stats.argtypes = [p, i64, i32, i64, p, p, i32, i32, i32, p, p, p, p]
         _C_LIB = lib
     return _C_LIB
@@ -246,8 +248,11 @@ def c_oracle():
 def c_predict(x, size, route, prior, ll, *, width: int, limit: int, threads: int = 1,
               logpost: bool = True):
     """Same contract as predict_dense, in C (pthreads over contiguous row chunks
-    -- the reference's classify_parallel chunking, engine.py:264-268)."""
-    x = np.ascontiguousarray(x, dtype=np.int32)
+    -- the reference's classify_parallel chunking, engine.py:264-268).  x may be
+    int32, uint16 or uint8 (same counts, narrower storage)."""
+    x = np.asarray(x)
+    xt = {np.dtype(np.uint8): 2, np.dtype(np.uint16): 1}.get(x.dtype, 0)
+    x = np.ascontiguousarray(x, dtype=x.dtype if xt else np.int32)
     size = np.ascontiguousarray(size, dtype=np.int32)
     route = np.ascontiguousarray(route, dtype=np.int32)
     prior = np.ascontiguousarray(prior, dtype=np.float64)
@@ -256,10 +261,10 @@ def c_predict(x, size, route, prior, ll, *, width: int, limit: int, threads: int
     C = prior.shape[1]
     label = np.empty(n, dtype=np.int32)
     lp = np.empty((n, C)) if logpost else None
-    rc = c_oracle().oracle_predict(x.ctypes.data, n, F, F, size.ctypes.data, width, limit,
-                                   route.ctypes.data, C, prior.ctypes.data, ll.ctypes.data,
-                                   label.ctypes.data, lp.ctypes.data if lp is not None else None,
-                                   threads)
+    rc = c_oracle().oracle_predict_typed(x.ctypes.data, xt, n, F, F, size.ctypes.data, width,
+                                         limit, route.ctypes.data, C, prior.ctypes.data,
+                                         ll.ctypes.data, label.ctypes.data,
+                                         lp.ctypes.data if lp is not None else None, threads)
     assert rc == 0
     return label, lp
 

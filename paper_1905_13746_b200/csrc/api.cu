@@ -1,7 +1,11 @@
 // C ABI of libgnb.so (declared in include/gnb.h): argument checking, TMA
 // tensor-map encoding, the device entry points and the host-buffer pipelines.
 #include <algorithm>
+#include <atomic>
 #include <chrono>
+#include <condition_variable>
+#include <functional>
+#include <thread>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -339,6 +343,8 @@ int gnb_gather_features(const int32_t* x_vocab, int64_t n_rows, int32_t n_vocab,
   return GNB_OK;
 }
 
+}  // extern "C"
+
 // ---------------------------------------------------------------- host pipelines
 namespace {
 
@@ -356,14 +362,82 @@ struct DevBuf {
   }
 };
 
+struct PinBuf {  // page-locked host staging
+  void* p = nullptr;
+  size_t n = 0;
+  cudaError_t ensure(size_t bytes) {
+    if (bytes <= n) return cudaSuccess;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    n = 0;
+    cudaError_t e = cudaHostAlloc(&p, bytes, cudaHostAllocDefault);
+    if (e == cudaSuccess) n = bytes;
+    return e;
+  }
+};
+
+// Minimal fork-join pool for the host-side narrowing of X (one job at a time).
+class Pool {
+ public:
+  explicit Pool(int n) : n_(n) {
+    for (int i = 0; i < n_; ++i) th_.emplace_back([this, i] { loop(i); });
+  }
+  ~Pool() {
+    {
+      std::lock_guard<std::mutex> g(m_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    for (auto& t : th_) t.join();
+  }
+  int size() const { return n_; }
+  void run(const std::function<void(int)>& f) {  // f(worker), blocks until all finish
+    std::unique_lock<std::mutex> g(m_);
+    job_ = &f;
+    pending_ = n_;
+    ++gen_;
+    cv_.notify_all();
+    done_.wait(g, [this] { return pending_ == 0; });
+    job_ = nullptr;
+  }
+
+ private:
+  void loop(int i) {
+    int seen = 0;
+    for (;;) {
+      const std::function<void(int)>* f;
+      {
+        std::unique_lock<std::mutex> g(m_);
+        cv_.wait(g, [&] { return stop_ || gen_ != seen; });
+        if (stop_) return;
+        seen = gen_;
+        f = job_;
+      }
+      (*f)(i);
+      std::lock_guard<std::mutex> g(m_);
+      if (--pending_ == 0) done_.notify_one();
+    }
+  }
+  int n_;
+  std::vector<std::thread> th_;
+  std::mutex m_;
+  std::condition_variable cv_, done_;
+  const std::function<void(int)>* job_ = nullptr;
+  int pending_ = 0, gen_ = 0;
+  bool stop_ = false;
+};
+
 constexpr int kLanes = 3;  // chunk pipeline depth (streams)
 
 struct HostCtx {
   int device = -1;
   cudaStream_t s[kLanes] = {};
   cudaEvent_t ev[kLanes] = {};
+  cudaEvent_t copied[kLanes] = {};  // staging buffer of the lane may be reused
   DevBuf x[kLanes], size[kLanes], aux[kLanes], label[kLanes], logpost[kLanes];
+  PinBuf stage[kLanes];
   DevBuf route, prior, lik, packed, sums, sumsq, counts, status;
+  Pool* pool = nullptr;
 };
 
 thread_local std::vector<HostCtx*> g_ctx;
@@ -379,10 +453,45 @@ int get_ctx(int device, HostCtx** out) {
   for (int i = 0; i < kLanes; ++i) {
     GNB_CUDA(cudaStreamCreateWithFlags(&c->s[i], cudaStreamNonBlocking), "stream create");
     GNB_CUDA(cudaEventCreateWithFlags(&c->ev[i], cudaEventDisableTiming), "event create");
+    GNB_CUDA(cudaEventCreateWithFlags(&c->copied[i], cudaEventDisableTiming), "event create");
   }
+  const unsigned hw = std::thread::hardware_concurrency();
+  c->pool = new Pool(static_cast<int>(hw > 0 ? std::min(hw, 64u) : 4u));
   g_ctx.push_back(c);
   *out = c;
   return GNB_OK;
+}
+
+// Narrow rows [0, n) of an int32 matrix into `dst` as uint8 (ld = dld) if every
+// count is < 256, else uint16 if < 65536; returns the x_type written, or
+// GNB_X_I32 when neither fits (negative or large counts): the caller then
+// ships the int32 rows unchanged.  Lossless by construction.
+template <typename U>
+bool narrow_rows(Pool& pool, const int32_t* src, int64_t n, int32_t F, int64_t ldx, U* dst,
+                 int64_t dld) {
+  std::atomic<uint32_t> bad{0};
+  const int W = pool.size();
+  pool.run([&](int w) {
+    const int64_t lo = n * w / W, hi = n * (w + 1) / W;
+    uint32_t acc = 0;
+    for (int64_t r = lo; r < hi; ++r) {
+      const int32_t* s = src + r * ldx;
+      U* d = dst + r * dld;
+      for (int32_t j = 0; j < F; ++j) {
+        const uint32_t v = static_cast<uint32_t>(s[j]);
+        acc |= v;
+        d[j] = static_cast<U>(v);
+      }
+      if (acc >> (8 * sizeof(U))) break;
+    }
+    if (acc >> (8 * sizeof(U))) bad.fetch_or(1u);
+  });
+  return bad.load() == 0;
+}
+
+bool narrowing_enabled() {
+  const char* e = getenv("GNB_HOST_NARROW");
+  return e != nullptr && atoi(e) != 0;
 }
 
 int64_t chunk_rows_for(int64_t row_bytes) {
@@ -393,13 +502,18 @@ int64_t chunk_rows_for(int64_t row_bytes) {
 
 }  // namespace
 
-int gnb_predict_host(const int32_t* x, int64_t n_rows, int32_t n_features, int64_t ldx,
-                     const int32_t* size_bytes, int32_t group_size_bytes,
-                     int32_t max_size_bytes, const int32_t* route, int32_t n_slots,
-                     int32_t n_classes, const double* log_prior, const double* log_lik,
-                     int32_t* label_out, double* logpost_out, int32_t device,
-                     int64_t* elapsed_ns) {
+extern "C" {
+
+}  // extern "C"
+
+static int predict_host_impl(const void* xv, int x_type, int64_t n_rows, int32_t n_features,
+                             int64_t ldx, const int32_t* size_bytes, int32_t group_size_bytes,
+                             int32_t max_size_bytes, const int32_t* route, int32_t n_slots,
+                             int32_t n_classes, const double* log_prior, const double* log_lik,
+                             int32_t* label_out, double* logpost_out, int32_t device,
+                             int64_t* elapsed_ns) {
   const auto t0 = std::chrono::steady_clock::now();
+  const int32_t* x = static_cast<const int32_t*>(xv);  // int32 view (x_type == GNB_X_I32)
   int rc = check_predict(x, n_rows, n_features, ldx, size_bytes, group_size_bytes,
                          max_size_bytes, route, n_slots, n_classes, log_prior, label_out);
   if (rc) return rc;
@@ -425,10 +539,18 @@ int gnb_predict_host(const int32_t* x, int64_t n_rows, int32_t n_features, int64
   GNB_CUDA(cudaEventRecord(c->ev[0], s0), "event");
   for (int i = 1; i < kLanes; ++i) GNB_CUDA(cudaStreamWaitEvent(c->s[i], c->ev[0], 0), "wait");
 
-  const int64_t ld = (n_features + 3) / 4 * 4;  // device rows padded for TMA
+  // Rows cross PCIe in the caller's storage (int32 / uint16 / uint8).  For
+  // int32 input, GNB_HOST_NARROW=1 makes host threads narrow each chunk into
+  // pinned staging first (lossless; chunks that do not fit stay int32) -- a
+  // win only when host DRAM bandwidth well exceeds PCIe (off by default:
+  // measured slower on the B200 box, profiles/r01_tuning.md).
+  const int64_t ld = (n_features + 3) / 4 * 4;  // device rows padded for TMA (int32)
+  const int64_t ld8 = (n_features + 15) / 16 * 16, ld16 = (n_features + 7) / 8 * 8;
   const int64_t rows = std::min<int64_t>(chunk_rows_for(ld * 4), std::max<int64_t>(n_rows, 1));
+  const bool narrow = x_type == GNB_X_I32 && narrowing_enabled();
   for (int i = 0; i < kLanes; ++i) {
     GNB_CUDA(c->x[i].ensure(size_t(rows) * ld * 4), "malloc");
+    if (narrow) GNB_CUDA(c->stage[i].ensure(size_t(rows) * ld16 * 2), "cudaHostAlloc");
     GNB_CUDA(c->size[i].ensure(size_t(rows) * 4), "malloc");
     GNB_CUDA(c->label[i].ensure(size_t(rows) * 4), "malloc");
     if (logpost_out) GNB_CUDA(c->logpost[i].ensure(size_t(rows) * n_classes * 8), "malloc");
@@ -438,18 +560,52 @@ int gnb_predict_host(const int32_t* x, int64_t n_rows, int32_t n_features, int64
     const int lane = static_cast<int>(chunk % kLanes);
     cudaStream_t s = c->s[lane];
     const int64_t n = std::min(rows, n_rows - r0);
-    int32_t* dx = static_cast<int32_t*>(c->x[lane].p);
-    if (ldx == ld) {
-      GNB_CUDA(cudaMemcpyAsync(dx, x + r0 * ldx, size_t(n) * ld * 4, cudaMemcpyHostToDevice, s), "H2D");
-    } else {
-      GNB_CUDA(cudaMemcpy2DAsync(dx, ld * 4, x + r0 * ldx, ldx * 4, size_t(n_features) * 4, n,
+    void* dx = c->x[lane].p;
+    int xt = GNB_X_I32;
+    int64_t dld = ld;
+    if (x_type != GNB_X_I32) {  // caller's narrow rows: copy as they are
+      xt = x_type;
+      const int eb = elem_bytes(xt);
+      dld = xt == GNB_X_U8 ? ld8 : ld16;
+      const uint8_t* src = static_cast<const uint8_t*>(xv) + r0 * ldx * eb;
+      if (ldx == dld)
+        GNB_CUDA(cudaMemcpyAsync(dx, src, size_t(n) * dld * eb, cudaMemcpyHostToDevice, s), "H2D");
+      else
+        GNB_CUDA(cudaMemcpy2DAsync(dx, dld * eb, src, ldx * eb, size_t(n_features) * eb, n,
+                                   cudaMemcpyHostToDevice, s),
+                 "H2D 2D");
+    } else if (narrow) {
+      GNB_CUDA(cudaEventSynchronize(c->copied[lane]), "event sync");  // staging free again
+      const int32_t* src = x + r0 * ldx;
+      if (narrow_rows(*c->pool, src, n, n_features, ldx,
+                      static_cast<uint8_t*>(c->stage[lane].p), ld8)) {
+        xt = GNB_X_U8;
+        dld = ld8;
+      } else if (narrow_rows(*c->pool, src, n, n_features, ldx,
+                             static_cast<uint16_t*>(c->stage[lane].p), ld16)) {
+        xt = GNB_X_U16;
+        dld = ld16;
+      }
+      if (xt != GNB_X_I32) {
+        GNB_CUDA(cudaMemcpyAsync(dx, c->stage[lane].p, size_t(n) * dld * elem_bytes(xt),
                                  cudaMemcpyHostToDevice, s),
-               "H2D 2D");
+                 "H2D");
+        GNB_CUDA(cudaEventRecord(c->copied[lane], s), "event");
+      }
+    }
+    if (xt == GNB_X_I32) {
+      if (ldx == ld) {
+        GNB_CUDA(cudaMemcpyAsync(dx, x + r0 * ldx, size_t(n) * ld * 4, cudaMemcpyHostToDevice, s), "H2D");
+      } else {
+        GNB_CUDA(cudaMemcpy2DAsync(dx, ld * 4, x + r0 * ldx, ldx * 4, size_t(n_features) * 4, n,
+                                   cudaMemcpyHostToDevice, s),
+                 "H2D 2D");
+      }
     }
     GNB_CUDA(cudaMemcpyAsync(c->size[lane].p, size_bytes + r0, size_t(n) * 4,
                              cudaMemcpyHostToDevice, s),
              "H2D");
-    rc = predict_device(dx, GNB_X_I32, n, n_features, ld, static_cast<int32_t*>(c->size[lane].p),
+    rc = predict_device(dx, xt, n, n_features, dld, static_cast<int32_t*>(c->size[lane].p),
                         group_size_bytes, max_size_bytes, static_cast<int32_t*>(c->route.p),
                         n_slots, n_classes, c->packed.p, static_cast<int32_t*>(c->label[lane].p),
                         logpost_out ? static_cast<double*>(c->logpost[lane].p) : nullptr, s);
@@ -468,6 +624,32 @@ int gnb_predict_host(const int32_t* x, int64_t n_rows, int32_t n_features, int64
                       std::chrono::steady_clock::now() - t0)
                       .count();
   return GNB_OK;
+}
+
+extern "C" {
+
+int gnb_predict_host(const int32_t* x, int64_t n_rows, int32_t n_features, int64_t ldx,
+                     const int32_t* size_bytes, int32_t group_size_bytes,
+                     int32_t max_size_bytes, const int32_t* route, int32_t n_slots,
+                     int32_t n_classes, const double* log_prior, const double* log_lik,
+                     int32_t* label_out, double* logpost_out, int32_t device,
+                     int64_t* elapsed_ns) {
+  return predict_host_impl(x, GNB_X_I32, n_rows, n_features, ldx, size_bytes, group_size_bytes,
+                           max_size_bytes, route, n_slots, n_classes, log_prior, log_lik,
+                           label_out, logpost_out, device, elapsed_ns);
+}
+
+int gnb_predict_host_typed(const void* x, int32_t x_type, int64_t n_rows, int32_t n_features,
+                           int64_t ldx, const int32_t* size_bytes, int32_t group_size_bytes,
+                           int32_t max_size_bytes, const int32_t* route, int32_t n_slots,
+                           int32_t n_classes, const double* log_prior, const double* log_lik,
+                           int32_t* label_out, double* logpost_out, int32_t device,
+                           int64_t* elapsed_ns) {
+  if (x_type != GNB_X_I32 && x_type != GNB_X_U16 && x_type != GNB_X_U8)
+    return fail(GNB_EINVAL, "predict_host: unknown x_type %d", x_type);
+  return predict_host_impl(x, x_type, n_rows, n_features, ldx, size_bytes, group_size_bytes,
+                           max_size_bytes, route, n_slots, n_classes, log_prior, log_lik,
+                           label_out, logpost_out, device, elapsed_ns);
 }
 
 int gnb_fit_stats_host(const int32_t* x, int64_t n_rows, int32_t n_cols, int64_t ldx,

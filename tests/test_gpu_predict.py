@@ -228,3 +228,65 @@ def test_narrowest_roundtrip():
     assert dense.narrowest(x).dtype == torch.uint8
     assert dense.narrowest(x * 100).dtype == torch.uint16
     assert dense.narrowest(x * 1000).dtype == torch.int32
+
+
+@pytest.mark.parametrize("narrow", ["0", "1"])
+@pytest.mark.parametrize("hi,neg", [(256, False), (60000, False), (2**31 - 1, False), (100, True)])
+def test_host_entry_narrowing_paths(hi, neg, narrow, monkeypatch):
+    """gnb_predict_host (GNB_HOST_NARROW=1: chunks shipped as uint8 / uint16 / int32 by
+    content) gives identical results."""
+    import ctypes
+    from paper_1905_13746_b200 import _native as N
+    monkeypatch.setenv("GNB_HOST_NARROW", narrow)
+    rng = np.random.default_rng(hi % 1000)
+    S, C, F, G = 2, 2, 45, 3
+    prior, ll, route = _tables(rng, S, C, F, G)
+    n = 70_000
+    x = rng.integers(0, hi, size=(n, F)).astype(np.int32)
+    if neg:
+        x[123, 7] = -5
+    ldx = 48                                  # padded host rows: exercises the pitch paths
+    xh = np.zeros((n, ldx), np.int32)
+    xh[:, :F] = x
+    size = rng.integers(-3, G * 100, size=n).astype(np.int32)
+    lab = np.empty(n, np.int32)
+    lp = np.empty((n, C))
+    el = ctypes.c_int64()
+    pr, lk = np.ascontiguousarray(prior), np.ascontiguousarray(ll)
+    N.check(N.lib.gnb_predict_host(xh.ctypes.data, n, F, ldx, size.ctypes.data, 100, G * 100,
+                                   route.ctypes.data, S, C, pr.ctypes.data, lk.ctypes.data,
+                                   lab.ctypes.data, lp.ctypes.data, 0, ctypes.addressof(el)))
+    want, wlp = O.predict_dense(np.clip(x, 0, None), size, route, prior, ll, width=100,
+                                limit=G * 100)
+    if neg:
+        assert lab[123] == N.ROW_NEGATIVE_COUNT or size[123] < 0
+        want[123] = lab[123]
+        wlp[123] = lp[123]
+    assert lab.tolist() == want.tolist()
+    ok = want >= 0
+    assert lp[ok].tobytes() == wlp[ok].tobytes()
+
+
+@pytest.mark.parametrize("dtype,xt", [(np.uint8, 2), (np.uint16, 1), (np.int32, 0)])
+def test_host_typed_entry(dtype, xt):
+    import ctypes
+    from paper_1905_13746_b200 import _native as N
+    rng = np.random.default_rng(xt)
+    S, C, F, G = 2, 3, 37, 2
+    prior, ll, route = _tables(rng, S, C, F, G)
+    n = 50_000
+    x = rng.integers(0, np.iinfo(dtype).max if dtype != np.int32 else 10**6, size=(n, F))
+    ldx = F + 3
+    xh = np.zeros((n, ldx), dtype)
+    xh[:, :F] = x
+    size = rng.integers(0, G * 100, size=n).astype(np.int32)
+    lab = np.empty(n, np.int32)
+    lp = np.empty((n, C))
+    pr, lk = np.ascontiguousarray(prior), np.ascontiguousarray(ll)
+    N.check(N.lib.gnb_predict_host_typed(xh.ctypes.data, xt, n, F, ldx, size.ctypes.data, 100,
+                                         G * 100, route.ctypes.data, S, C, pr.ctypes.data,
+                                         lk.ctypes.data, lab.ctypes.data, lp.ctypes.data, 0,
+                                         None))
+    want, wlp = O.predict_dense(x, size, route, prior, ll, width=100, limit=G * 100)
+    assert lab.tolist() == want.tolist()
+    assert lp.tobytes() == wlp.tobytes()

@@ -49,3 +49,17 @@ def test_c_predict_golden(golden):
     assert lab.tolist() == z["pred_label"].astype(np.int32).tolist()
     ok = lab >= 0
     assert lp[ok].tobytes() == z["pred_lp"][ok].tobytes()
+
+
+@pytest.mark.parametrize("dtype", [np.uint8, np.uint16])
+def test_c_predict_narrow_storage(dtype):
+    rng = np.random.default_rng(4)
+    prior = np.log(rng.dirichlet(np.ones(2), size=2))
+    ll = np.log(rng.dirichlet(np.ones(30), size=(2, 2)))
+    route = np.array([0, 1, 1], np.int32)
+    x = rng.integers(0, np.iinfo(dtype).max, size=(999, 30))
+    size = rng.integers(-2, 31, size=999)
+    a = O.c_predict(x.astype(dtype), size, route, prior, ll, width=10, limit=30, threads=3)
+    b = O.predict_dense(x, size, route, prior, ll, width=10, limit=30)
+    assert a[0].tolist() == b[0].tolist()
+    assert a[1].tobytes() == b[1].tobytes()
