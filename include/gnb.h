@@ -92,6 +92,23 @@ int gnb_predict_typed(const void* x, int32_t x_type, int64_t n_rows, int32_t n_f
                       int32_t n_classes, const void* packed, int32_t* label_out,
                       double* logpost_out, uintptr_t stream);
 
+/* Ragged batches in arbitrary row order.  gnb_slot_sort writes perm[n] = row
+ * indices grouped by routed model slot (device counting sort over the sizes;
+ * rows with size out of range last), using `workspace`
+ * (gnb_slot_sort_workspace_bytes).  gnb_predict_permuted then scores tiles of
+ * perm order -- rows fetched with TMA tile::gather4, one model per tile, tables
+ * in shared memory -- and writes every output at its ORIGINAL row index, so
+ * results equal gnb_predict's exactly.  n_rows <= 2^30, n_slots < 4096. */
+size_t gnb_slot_sort_workspace_bytes(int64_t n_rows, int32_t n_slots);
+int gnb_slot_sort(const int32_t* size_bytes, int64_t n_rows, int32_t group_size_bytes,
+                  int32_t max_size_bytes, const int32_t* route, int32_t n_slots, int32_t* perm,
+                  void* workspace, size_t workspace_bytes, uintptr_t stream);
+int gnb_predict_permuted(const void* x, int32_t x_type, int64_t n_rows, int32_t n_features,
+                         int64_t ldx, const int32_t* size_bytes, int32_t group_size_bytes,
+                         int32_t max_size_bytes, const int32_t* route, int32_t n_slots,
+                         int32_t n_classes, const void* packed, const int32_t* perm,
+                         int32_t* label_out, double* logpost_out, uintptr_t stream);
+
 /* Same as gnb_predict but always uses the L1 (non-TMA) kernel; parity tests. */
 int gnb_predict_generic(const int32_t* x, int64_t n_rows, int32_t n_features, int64_t ldx,
                         const int32_t* size_bytes, int32_t group_size_bytes,

@@ -52,6 +52,10 @@ _SIGS = {
                     C.c_int),
     "gnb_predict_typed": ([_p, _i32, _i64, _i32, _i64, _p, _i32, _i32, _p, _i32, _i32, _p, _p,
                            _p, _up], C.c_int),
+    "gnb_slot_sort_workspace_bytes": ([_i64, _i32], _sz),
+    "gnb_slot_sort": ([_p, _i64, _i32, _i32, _p, _i32, _p, _p, _sz, _up], C.c_int),
+    "gnb_predict_permuted": ([_p, _i32, _i64, _i32, _i64, _p, _i32, _i32, _p, _i32, _i32, _p, _p,
+                              _p, _p, _up], C.c_int),
     "gnb_predict_generic": ([_p, _i64, _i32, _i64, _p, _i32, _i32, _p, _i32, _i32, _p, _p, _p,
                              _up], C.c_int),
     "gnb_predict_host": ([_p, _i64, _i32, _i64, _p, _i32, _i32, _p, _i32, _i32, _p, _p, _p, _p,

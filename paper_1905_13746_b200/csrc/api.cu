@@ -169,8 +169,10 @@ static int predict_device(const void* x, int x_type, int64_t n_rows, int32_t F, 
                           const int32_t* size, int32_t width, int32_t limit,
                           const int32_t* route, int32_t S, int32_t C, const void* packed,
                           int32_t* label, double* logpost, cudaStream_t stream,
-                          int force_generic = 0) {
+                          int force_generic = 0, const int32_t* perm = nullptr) {
   const bool use_tma = !force_generic && tma_ok(x, ldx, x_type) && encode_fn() != nullptr;
+  if (perm != nullptr && n_rows > kMaxRowsPerLaunch)
+    return fail(GNB_EUNSUPPORTED, "predict: permuted batches are limited to 2^30 rows");
   const int eb = elem_bytes(x_type);
   for (int64_t r0 = 0; r0 < n_rows; r0 += kMaxRowsPerLaunch) {
     const int64_t n = std::min(kMaxRowsPerLaunch, n_rows - r0);
@@ -189,10 +191,12 @@ static int predict_device(const void* x, int x_type, int64_t n_rows, int32_t F, 
     p.prior = static_cast<const double*>(packed);
     p.label = label + r0;
     p.logpost = logpost ? logpost + r0 * C : nullptr;
+    p.perm = use_tma ? perm : nullptr;  // the L1 kernel walks rows in order
     CUtensorMap map;
     const CUtensorMap* mp = nullptr;
     if (use_tma) {
-      if (!encode_map(&map, p.x, n, F, ldx, predict_box_rows(C), true, x_type))
+      // gather mode: box height 1 (tile::gather4 loads 4 rows per instruction)
+      if (!encode_map(&map, p.x, n, F, ldx, perm ? 1 : predict_box_rows(C), true, x_type))
         return fail(GNB_ECUDA, "predict: cuTensorMapEncodeTiled failed");
       mp = &map;
     }
@@ -227,6 +231,44 @@ int gnb_predict_typed(const void* x, int32_t x_type, int64_t n_rows, int32_t n_f
   return predict_device(x, x_type, n_rows, n_features, ldx, size_bytes, group_size_bytes,
                         max_size_bytes, route, n_slots, n_classes, packed, label_out,
                         logpost_out, reinterpret_cast<cudaStream_t>(stream));
+}
+
+size_t gnb_slot_sort_workspace_bytes(int64_t n_rows, int32_t n_slots) {
+  if (n_rows < 0 || n_slots < 1) return 0;
+  return slot_sort_workspace(n_rows, n_slots);
+}
+
+int gnb_slot_sort(const int32_t* size_bytes, int64_t n_rows, int32_t group_size_bytes,
+                  int32_t max_size_bytes, const int32_t* route, int32_t n_slots, int32_t* perm,
+                  void* workspace, size_t workspace_bytes, uintptr_t stream) {
+  if (n_rows < 0 || n_rows > kMaxRowsPerLaunch || n_slots < 1 || n_slots >= 4096 ||
+      group_size_bytes <= 0 || max_size_bytes <= 0 || max_size_bytes % group_size_bytes)
+    return fail(GNB_EINVAL, "slot_sort: bad geometry (n_rows <= 2^30, n_slots < 4096)");
+  if (n_rows > 0 && (!size_bytes || !route || !perm || !workspace))
+    return fail(GNB_EINVAL, "slot_sort: null pointer");
+  if (workspace_bytes < slot_sort_workspace(n_rows, n_slots))
+    return fail(GNB_EINVAL, "slot_sort: workspace too small");
+  GNB_CUDA(slot_sort(size_bytes, n_rows, group_size_bytes, max_size_bytes, route, n_slots, perm,
+                     workspace, reinterpret_cast<cudaStream_t>(stream)),
+           "slot_sort");
+  return GNB_OK;
+}
+
+int gnb_predict_permuted(const void* x, int32_t x_type, int64_t n_rows, int32_t n_features,
+                         int64_t ldx, const int32_t* size_bytes, int32_t group_size_bytes,
+                         int32_t max_size_bytes, const int32_t* route, int32_t n_slots,
+                         int32_t n_classes, const void* packed, const int32_t* perm,
+                         int32_t* label_out, double* logpost_out, uintptr_t stream) {
+  if (x_type != GNB_X_I32 && x_type != GNB_X_U16 && x_type != GNB_X_U8)
+    return fail(GNB_EINVAL, "predict: unknown x_type %d", x_type);
+  int rc = check_predict(static_cast<const int32_t*>(x), n_rows, n_features, ldx, size_bytes,
+                         group_size_bytes, max_size_bytes, route, n_slots, n_classes, packed,
+                         label_out);
+  if (rc) return rc;
+  if (n_rows > 0 && !perm) return fail(GNB_EINVAL, "predict_permuted: null perm");
+  return predict_device(x, x_type, n_rows, n_features, ldx, size_bytes, group_size_bytes,
+                        max_size_bytes, route, n_slots, n_classes, packed, label_out,
+                        logpost_out, reinterpret_cast<cudaStream_t>(stream), 0, perm);
 }
 
 // Test hook: force the L1 (non-TMA) predict kernel.
@@ -435,6 +477,7 @@ struct HostCtx {
   cudaEvent_t ev[kLanes] = {};
   cudaEvent_t copied[kLanes] = {};  // staging buffer of the lane may be reused
   DevBuf x[kLanes], size[kLanes], aux[kLanes], label[kLanes], logpost[kLanes];
+  DevBuf perm[kLanes], sortws[kLanes];
   PinBuf stage[kLanes];
   DevBuf route, prior, lik, packed, sums, sumsq, counts, status;
   Pool* pool = nullptr;
@@ -605,10 +648,39 @@ static int predict_host_impl(const void* xv, int x_type, int64_t n_rows, int32_t
     GNB_CUDA(cudaMemcpyAsync(c->size[lane].p, size_bytes + r0, size_t(n) * 4,
                              cudaMemcpyHostToDevice, s),
              "H2D");
+    // Ragged batch not grouped by size group (more than 1 in 8 tiles would mix
+    // models): sort the chunk's rows by slot on the device, score via gather4.
+    const int32_t* perm = nullptr;
+    if (n_slots > 1) {
+      int64_t mixed = 0, tiles = 0;
+      for (int64_t t0 = 0; t0 < n; t0 += 128, ++tiles) {
+        int first = -2;
+        for (int64_t r = t0; r < std::min<int64_t>(t0 + 128, n); ++r) {
+          const int32_t sz = size_bytes[r0 + r];
+          if (sz < 0 || sz >= max_size_bytes) continue;
+          const int sl = route[sz / group_size_bytes];
+          if (first == -2) first = sl;
+          else if (sl != first) {
+            ++mixed;
+            break;
+          }
+        }
+      }
+      if (mixed * 8 > tiles) {
+        GNB_CUDA(c->perm[lane].ensure(size_t(n) * 4), "malloc");
+        GNB_CUDA(c->sortws[lane].ensure(slot_sort_workspace(n, n_slots)), "malloc");
+        GNB_CUDA(slot_sort(static_cast<int32_t*>(c->size[lane].p), n, group_size_bytes,
+                           max_size_bytes, static_cast<int32_t*>(c->route.p), n_slots,
+                           static_cast<int32_t*>(c->perm[lane].p), c->sortws[lane].p, s),
+                 "slot_sort");
+        perm = static_cast<int32_t*>(c->perm[lane].p);
+      }
+    }
     rc = predict_device(dx, xt, n, n_features, dld, static_cast<int32_t*>(c->size[lane].p),
                         group_size_bytes, max_size_bytes, static_cast<int32_t*>(c->route.p),
                         n_slots, n_classes, c->packed.p, static_cast<int32_t*>(c->label[lane].p),
-                        logpost_out ? static_cast<double*>(c->logpost[lane].p) : nullptr, s);
+                        logpost_out ? static_cast<double*>(c->logpost[lane].p) : nullptr, s, 0,
+                        perm);
     if (rc) return rc;
     GNB_CUDA(cudaMemcpyAsync(label_out + r0, c->label[lane].p, size_t(n) * 4,
                              cudaMemcpyDeviceToHost, s),

@@ -87,6 +87,18 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
       : "memory");
 }
 
+// TMA gather: 4 rows (arbitrary row coordinates) x one box width -> smem, laid
+// out as 4 consecutive box rows.  The tensor map's box height must be 1.
+__device__ __forceinline__ void tma_gather4(void* dst, const CUtensorMap* map, int32_t c0,
+                                            const int (&rows)[4], uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(rows[0]), "r"(rows[1]), "r"(rows[2]),
+      "r"(rows[3]), "r"(smem_u32(bar))
+      : "memory");
+}
+
 // 1-D bulk copy global -> smem (size multiple of 16, both ends 16-B aligned).
 __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes,
                                           uint64_t* bar, uint64_t policy) {

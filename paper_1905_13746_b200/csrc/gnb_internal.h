@@ -30,6 +30,7 @@ struct PredictParams {
   double* logpost;  // nullable, [N][C]
   int64_t n_tiles;  // set by predict_launch
   int32_t x_policy; // 0 evict_normal (default), 1 evict_first
+  const int32_t* perm;  // nullable: rows in routed-slot order (gather mode)
 };
 
 struct FitParams {
@@ -85,6 +86,10 @@ cudaError_t gather_launch(const int32_t* x, int64_t n_rows, int32_t V, int64_t l
                           const int32_t* route, const int32_t* features,
                           const int32_t* n_features, int32_t F, int32_t* out, int64_t ldo,
                           cudaStream_t stream);
+
+size_t slot_sort_workspace(int64_t n, int S);
+cudaError_t slot_sort(const int32_t* size, int64_t n, int width, int limit, const int32_t* route,
+                      int S, int32_t* perm, void* workspace, cudaStream_t stream);
 
 // Host helpers (api.cu)
 bool encode_rows_map(CUtensorMap* map, const void* base, int64_t n_rows, int32_t n_cols,

@@ -174,12 +174,13 @@ __device__ __forceinline__ void write_row(const PredictParams& p, int64_t r, int
 // ------------------------------------------------------------------ TMA kernel
 // A consumer thread owns R rows of the tile (rows lane + 32*(w + NW*i)), so one
 // broadcast table read feeds R*CP independent accumulator chains.
-template <int CP, typename T, int R, int NW, int STAGES>
+template <int CP, typename T, int R, int NW, int STAGES, bool GATHER = false>
 struct PredictSmem {
   static constexpr int kRows = NW * 32 * R;                          // rows per tile (<= 256)
   static constexpr int kXBytes = kRows * kChunkBytesPerRow;            // one box
   static constexpr int kTabBytes = Elem<T>::kPerRow * CP * 8;          // one table slice
-  static constexpr int kHdrBytes = ((4 + kRows * 4) + 15) / 16 * 16;
+  // tile_slot + row_slot[kRows] (+ row_id[kRows] in gather mode)
+  static constexpr int kHdrBytes = ((4 + kRows * 4 * (GATHER ? 2 : 1)) + 15) / 16 * 16;
   static constexpr int kX = 0;
   static constexpr int kTab = kX + STAGES * kXBytes;
   static constexpr int kHdr = kTab + STAGES * kTabBytes;
@@ -191,7 +192,7 @@ struct PredictSmem {
 
 struct StageHdr {
   int tile_slot;  // >= 0: every valid row uses this slot; table slice staged
-  int row_slot[1];
+  int row_slot[1];  // [kRows]; in gather mode followed by row_id[kRows]
 };
 
 // Table of slot s, chunk ch (kPerRow features per chunk).
@@ -259,10 +260,14 @@ __device__ __forceinline__ void score_chunk_mixed(const PredictParams& p, double
   }
 }
 
-template <int CP, typename T, int R, int NW, int STAGES>
+// GATHER: tile rows are perm[tile*ROWS ...] (rows sorted by routed slot by
+// slot_sort), loaded with TMA tile::gather4 (4 arbitrary rows per
+// instruction, one instruction per producer lane) into the same swizzled box
+// layout; outputs go back to the original row index.
+template <int CP, typename T, int R, int NW, int STAGES, bool GATHER>
 __global__ void __launch_bounds__((NW + 1) * 32)
     predict_tma_kernel(const __grid_constant__ CUtensorMap xmap, const PredictParams p) {
-  using L = PredictSmem<CP, T, R, NW, STAGES>;
+  using L = PredictSmem<CP, T, R, NW, STAGES, GATHER>;
   constexpr int ROWS = L::kRows;
   constexpr int CF = Elem<T>::kPerRow;
   constexpr int EQ = Elem<T>::kPerQuad;
@@ -294,13 +299,15 @@ __global__ void __launch_bounds__((NW + 1) * 32)
     uint32_t phase = 0;
     for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
       const int64_t r0 = tile * ROWS;
-      int slots[ROWS / 32];
+      int slots[ROWS / 32], ids[ROWS / 32];
       int lo = INT_MAX, hi = INT_MIN;
 #pragma unroll
       for (int i = 0; i < ROWS / 32; ++i) {
-        const int64_t r = r0 + lane + 32 * i;
+        int64_t r = r0 + lane + 32 * i;
         int s = -1;
-        if (r < p.n_rows) {
+        if (GATHER) r = r < p.n_rows ? __ldg(p.perm + r) : -1;
+        ids[i] = static_cast<int>(GATHER ? r : 0);
+        if (r >= 0 && r < p.n_rows) {
           const int sz = __ldg(p.size + r);
           if (sz >= 0 && sz < p.limit) {
             s = __ldg(p.route + sz / p.width);
@@ -318,21 +325,37 @@ __global__ void __launch_bounds__((NW + 1) * 32)
         StageHdr* hdr = reinterpret_cast<StageHdr*>(smem + L::kHdr + stage * L::kHdrBytes);
         if (ch == 0) {
 #pragma unroll
-          for (int i = 0; i < ROWS / 32; ++i) hdr->row_slot[lane + 32 * i] = slots[i];
+          for (int i = 0; i < ROWS / 32; ++i) {
+            hdr->row_slot[lane + 32 * i] = slots[i];
+            if (GATHER) hdr->row_slot[ROWS + lane + 32 * i] = ids[i];
+          }
         }
         if (lane == 0) hdr->tile_slot = tile_slot;
         __syncwarp();
+        uint8_t* box = smem + L::kX + stage * L::kXBytes;
         if (lane == 0) {
           const uint32_t bytes = L::kXBytes + (tile_slot >= 0 ? L::kTabBytes : 0);
           mbar_arrive_expect_tx(&full[stage], bytes);
-          tma_load_2d(smem + L::kX + stage * L::kXBytes, &xmap, ch * CF,
-                      static_cast<int32_t>(r0), &full[stage], pol_x);
+          if (!GATHER)
+            tma_load_2d(box, &xmap, ch * CF, static_cast<int32_t>(r0), &full[stage], pol_x);
           if (tile_slot >= 0)
             bulk_load(smem + L::kTab + stage * L::kTabBytes, chunk_table<CP, T>(p, tile_slot, ch),
                       L::kTabBytes, &full[stage], pol_t);
-        } else {
-          mbar_arrive(&full[stage]);
         }
+        if (GATHER) {
+          __syncwarp();  // expect_tx precedes every completion
+#pragma unroll
+          for (int g = lane; g < ROWS / 4; g += 32) {
+            int rr[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const int64_t pos = r0 + 4 * g + k;
+              rr[k] = __ldg(p.perm + (pos < p.n_rows ? pos : p.n_rows - 1));
+            }
+            tma_gather4(box + 4 * g * kChunkBytesPerRow, &xmap, ch * CF, rr, &full[stage]);
+          }
+        }
+        if (lane != 0) mbar_arrive(&full[stage]);
         if (++stage == STAGES) {
           stage = 0;
           phase ^= 1;
@@ -348,7 +371,7 @@ __global__ void __launch_bounds__((NW + 1) * 32)
     uint32_t phase = 0;
     for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
       double acc[R][CP];
-      int slot[R];
+      int slot[R], rid[R];
       uint32_t neg[R];
 #pragma unroll
       for (int i = 0; i < R; ++i) neg[i] = 0;
@@ -361,6 +384,7 @@ __global__ void __launch_bounds__((NW + 1) * 32)
 #pragma unroll
           for (int i = 0; i < R; ++i) {
             slot[i] = hdr->row_slot[rows[i]];
+            rid[i] = GATHER ? hdr->row_slot[ROWS + rows[i]] : 0;
             const int s = ts >= 0 ? ts : max(slot[i], 0);
 #pragma unroll
             for (int c = 0; c < CP; ++c) acc[i][c] = __ldg(p.prior + s * CP + c);
@@ -385,8 +409,12 @@ __global__ void __launch_bounds__((NW + 1) * 32)
       }
 #pragma unroll
       for (int i = 0; i < R; ++i) {
-        const int64_t r = tile * ROWS + rows[i];
-        if (r < p.n_rows) write_row<CP>(p, r, slot[i], neg[i], acc[i]);
+        if (GATHER) {
+          if (tile * ROWS + rows[i] < p.n_rows) write_row<CP>(p, rid[i], slot[i], neg[i], acc[i]);
+        } else {
+          const int64_t r = tile * ROWS + rows[i];
+          if (r < p.n_rows) write_row<CP>(p, r, slot[i], neg[i], acc[i]);
+        }
       }
     }
   }
@@ -422,10 +450,10 @@ __global__ void __launch_bounds__(256) predict_generic_kernel(const PredictParam
 }
 
 // ------------------------------------------------------------------ launchers
-template <int CP, typename T, int R, int NW, int STAGES>
-static cudaError_t launch_tma(const CUtensorMap& map, PredictParams p, cudaStream_t stream) {
-  using L = PredictSmem<CP, T, R, NW, STAGES>;
-  auto kern = predict_tma_kernel<CP, T, R, NW, STAGES>;
+template <int CP, typename T, int R, int NW, int STAGES, bool GATHER>
+static cudaError_t launch_tma_mode(const CUtensorMap& map, PredictParams p, cudaStream_t stream) {
+  using L = PredictSmem<CP, T, R, NW, STAGES, GATHER>;
+  auto kern = predict_tma_kernel<CP, T, R, NW, STAGES, GATHER>;
   p.n_tiles = (p.n_rows + L::kRows - 1) / L::kRows;
   p.n_chunks = (p.n_features + Elem<T>::kPerRow - 1) / Elem<T>::kPerRow;
   static int per_sm = 0;  // resident CTAs per SM for this instantiation
@@ -446,6 +474,13 @@ static cudaError_t launch_tma(const CUtensorMap& map, PredictParams p, cudaStrea
   if (grid == 0) return cudaSuccess;
   kern<<<grid, (NW + 1) * 32, L::kAlloc, stream>>>(map, p);
   return cudaGetLastError();
+}
+
+template <int CP, typename T, int R, int NW, int STAGES>
+static cudaError_t launch_tma(const CUtensorMap& map, const PredictParams& p,
+                              cudaStream_t stream) {
+  return p.perm != nullptr ? launch_tma_mode<CP, T, R, NW, STAGES, true>(map, p, stream)
+                           : launch_tma_mode<CP, T, R, NW, STAGES, false>(map, p, stream);
 }
 
 template <int CP, typename T>

@@ -96,15 +96,31 @@ class DeviceTables:
         return cls(rt, packed, S, Cn, F, group_size_bytes, max_size_bytes)
 
 
+def slot_sort(size_bytes: torch.Tensor, tables: DeviceTables, *, stream=None) -> torch.Tensor:
+    """perm[n]: row indices grouped by routed model slot (device counting sort)."""
+    n = size_bytes.shape[0]
+    sp = _vec(size_bytes, n, "size_bytes")
+    dev = size_bytes.device
+    perm = torch.empty(n, dtype=torch.int32, device=dev)
+    ws_bytes = N.lib.gnb_slot_sort_workspace_bytes(n, tables.n_slots)
+    ws = torch.empty(max(ws_bytes, 4), dtype=torch.uint8, device=dev)
+    N.check(N.lib.gnb_slot_sort(sp, n, tables.group_size_bytes, tables.max_size_bytes,
+                                tables.route.data_ptr(), tables.n_slots, perm.data_ptr(),
+                                ws.data_ptr(), ws.numel(), _stream(stream)), "gnb_slot_sort")
+    return perm
+
+
 def predict(x: torch.Tensor, size_bytes: torch.Tensor, tables: DeviceTables, *,
             logpost: bool = True, label_out=None, logpost_out=None, stream=None,
-            generic: bool = False):
+            generic: bool = False, perm: torch.Tensor | None = None):
     """Score every row: label[N] int32 (class index, or -1 size out of range,
     -2 negative count) and, if requested, log-posteriors [N, C] fp64.
 
     Row n of x holds its routed model's feature counts in FeatureSet order
     (extra columns beyond the model's features must be 0).  x may be int32,
-    uint16 or uint8 (the same counts in fewer bytes; identical results)."""
+    uint16 or uint8 (the same counts in fewer bytes; identical results).
+    perm (from slot_sort): score in slot-grouped order -- for ragged batches
+    whose rows are not grouped by size group; results are identical."""
     xp, n, F, ldx = _rows(x, dtypes=tuple(_X_TYPES))
     if F != tables.n_features:
         raise InvalidConfigError(f"x has {F} columns, tables have {tables.n_features} features")
@@ -123,6 +139,11 @@ def predict(x: torch.Tensor, size_bytes: torch.Tensor, tables: DeviceTables, *,
         if x.dtype != torch.int32:
             raise InvalidConfigError("generic=True is the int32 L1 test path")
         N.check(N.lib.gnb_predict_generic(xp, *args), "gnb_predict_generic")
+    elif perm is not None:
+        pp = _vec(perm, n, "perm")
+        a = list(args)
+        a.insert(10, pp)   # after packed
+        N.check(N.lib.gnb_predict_permuted(xp, _X_TYPES[x.dtype], *a), "gnb_predict_permuted")
     else:
         N.check(N.lib.gnb_predict_typed(xp, _X_TYPES[x.dtype], *args), "gnb_predict_typed")
     return label, lp

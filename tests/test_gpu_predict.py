@@ -290,3 +290,36 @@ def test_host_typed_entry(dtype, xt):
     want, wlp = O.predict_dense(x, size, route, prior, ll, width=100, limit=G * 100)
     assert lab.tolist() == want.tolist()
     assert lp.tobytes() == wlp.tobytes()
+
+
+@pytest.mark.parametrize("dtype", [torch.int32, torch.uint8])
+@pytest.mark.parametrize("N", [1, 127, 5000, 100_003])
+def test_slot_sort_and_permuted_predict(dtype, N):
+    """Shuffled ragged batch: slot_sort + gather4 predict == oracle, outputs in original order."""
+    rng = np.random.default_rng(N)
+    G, F = 32, 72
+    trained = [g for g in range(G) if g not in (5, 8, 17)]
+    prior, ll, _ = _tables(rng, len(trained), 2, F, G)
+    route = np.array([trained.index(t) for t in O.route_table(trained, G)], dtype=np.int32)
+    size = rng.integers(-20, G * 100 + 20, size=N)
+    x = rng.integers(0, 200, size=(N, F))
+    dev = torch.device("cuda")
+    t = dense.DeviceTables.build(prior, ll, route, group_size_bytes=100, max_size_bytes=G * 100)
+    sd = torch.from_numpy(size.astype(np.int32)).to(dev)
+    perm = dense.slot_sort(sd, t)
+    torch.cuda.synchronize()
+    pm = perm.cpu().numpy()
+    assert sorted(pm.tolist()) == list(range(N))           # a permutation
+    g = O.group_of(size, 100, G * 100)
+    key = np.where(g >= 0, route[np.maximum(g, 0)], len(trained))
+    assert (np.diff(key[pm]) >= 0).all()                    # grouped by slot, invalid last
+    ld = {torch.int32: (F + 3) // 4 * 4, torch.uint8: (F + 15) // 16 * 16}[dtype]
+    base = torch.zeros((N, ld), dtype=torch.int32, device=dev)
+    base[:, :F] = torch.from_numpy(x.astype(np.int32)).to(dev)
+    xd = base.to(dtype)[:, :F]
+    lab, lp = dense.predict(xd, sd, t, perm=perm)
+    torch.cuda.synchronize()
+    want, wlp = O.predict_dense(x, size, route, prior, ll, width=100, limit=G * 100)
+    assert lab.cpu().numpy().tolist() == want.tolist()
+    ok = want >= 0
+    assert lp.cpu().numpy()[ok].tobytes() == wlp[ok].tobytes()
