@@ -594,8 +594,10 @@ def run_fit(args, world, rank, local):
     chunk = min(100_000_000, hi - lo)
     x, size, lab = dense.generate(chunk, V, n_classes=C, group_rows=[total], divergence=0.8,
                                   seed=0, row_offset=lo, device=dev)
+    xt = getattr(torch, args.x_dtype)
+    xs = x if args.x_dtype == "int32" else torch.empty((chunk, V), dtype=xt, device=dev)
     # warm-up launch (module load, tensor-map path) outside the timed region
-    dense.fit_stats(x[:1024], size[:1024], lab[:1024], n_classes=C, group_size_bytes=5120,
+    dense.fit_stats(xs[:1024], size[:1024], lab[:1024], n_classes=C, group_size_bytes=5120,
                     max_size_bytes=5120)
     st = None
     ms = 0.0
@@ -604,9 +606,12 @@ def run_fit(args, world, rank, local):
         n = min(chunk, hi - r0)
         dense.generate(n, V, n_classes=C, group_rows=[total], divergence=0.8, seed=0,
                        row_offset=r0, out=(x[:n], size[:n], lab[:n]), device=dev)
+        if args.x_dtype != "int32":        # same counts, narrower storage (lossless check)
+            assert int(x[:n].max()) < (256 if args.x_dtype == "uint8" else 65536)
+            xs[:n].copy_(x[:n])
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(s)
-        st = dense.fit_stats(x[:n], size[:n], lab[:n], n_classes=C, group_size_bytes=5120,
+        st = dense.fit_stats(xs[:n], size[:n], lab[:n], n_classes=C, group_size_bytes=5120,
                              max_size_bytes=5120, out=st, accumulate=st is not None)
         b.record(s)
         b.synchronize()
@@ -621,7 +626,7 @@ def run_fit(args, world, rank, local):
     ar_ms = a.elapsed_time(b)
     ms = barrier_max(ms, world, dev)
     peak, kind = peaks()
-    bps = 4 * V + 8
+    bps = xs.element_size() * V + 8
     rows_here = hi - lo
     n_total = float(st.counts.sum().item())
     return {"metric": "samples fitted/sec (sums, sums of squares, counts)", "unit": UNIT,
@@ -630,7 +635,8 @@ def run_fit(args, world, rank, local):
             "allreduce_ms": round(ar_ms, 4), "n_gpus": world,
             "achieved_gbs_per_gpu": round(rows_here * bps / (ms / 1e3) / 1e9, 1),
             "frac": round(rows_here * bps / (ms / 1e3) / 1e9 / peak, 4), "peak_gbs": peak,
-            "bytes_per_sample": "4V+8", "rows_counted": n_total,
+            "bytes_per_sample": f"{xs.element_size()}V+8", "x_dtype": args.x_dtype,
+            "rows_counted": n_total,
             "stats_bytes_allreduced": int(st.packed().numel() * 8)}
 
 

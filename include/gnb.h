@@ -171,6 +171,13 @@ int gnb_fit_stats(const int32_t* x, int64_t n_rows, int32_t n_cols, int64_t ldx,
                   double* counts, unsigned long long* status, int32_t accumulate,
                   uintptr_t stream);
 
+/* gnb_fit_stats for X stored as x_type (GNB_X_I32 / GNB_X_U16 / GNB_X_U8). */
+int gnb_fit_stats_typed(const void* x, int32_t x_type, int64_t n_rows, int32_t n_cols,
+                        int64_t ldx, const int32_t* size_bytes, const int32_t* labels,
+                        int32_t group_size_bytes, int32_t max_size_bytes, int32_t n_classes,
+                        double* sums, double* sumsq, double* counts, unsigned long long* status,
+                        int32_t accumulate, uintptr_t stream);
+
 int gnb_fit_stats_host(const int32_t* x, int64_t n_rows, int32_t n_cols, int64_t ldx,
                        const int32_t* size_bytes, const int32_t* labels,
                        int32_t group_size_bytes, int32_t max_size_bytes, int32_t n_classes,

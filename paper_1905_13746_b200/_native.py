@@ -66,6 +66,8 @@ _SIGS = {
                                 _p, _p, _p, _i32, _p], C.c_int),
     "gnb_fit_stats": ([_p, _i64, _i32, _i64, _p, _p, _i32, _i32, _i32, _p, _p, _p, _p, _i32, _up],
                       C.c_int),
+    "gnb_fit_stats_typed": ([_p, _i32, _i64, _i32, _i64, _p, _p, _i32, _i32, _i32, _p, _p, _p,
+                             _p, _i32, _up], C.c_int),
     "gnb_fit_stats_host": ([_p, _i64, _i32, _i64, _p, _p, _i32, _i32, _i32, _p, _p, _p, _p, _i32],
                            C.c_int),
     "gnb_fin_train": ([_p, _p, _i32, _i32, _i32, _f64, _i32, _p, _p, _p, _p, _p], C.c_int),

@@ -285,22 +285,23 @@ int gnb_predict_generic(const int32_t* x, int64_t n_rows, int32_t n_features, in
                         logpost_out, reinterpret_cast<cudaStream_t>(stream), 1);
 }
 
-int gnb_fit_stats(const int32_t* x, int64_t n_rows, int32_t n_cols, int64_t ldx,
-                  const int32_t* size_bytes, const int32_t* labels, int32_t group_size_bytes,
-                  int32_t max_size_bytes, int32_t n_classes, double* sums, double* sumsq,
-                  double* counts, unsigned long long* status, int32_t accumulate,
-                  uintptr_t stream_) {
-  cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
+static int fit_stats_device(const void* x, int x_type, int64_t n_rows, int32_t n_cols,
+                            int64_t ldx, const int32_t* size_bytes, const int32_t* labels,
+                            int32_t group_size_bytes, int32_t max_size_bytes, int32_t n_classes,
+                            double* sums, double* sumsq, double* counts,
+                            unsigned long long* status, int32_t accumulate, cudaStream_t stream) {
   if (n_rows < 0 || n_cols < 1 || ldx < n_cols)
     return fail(GNB_EINVAL, "fit_stats: need n_rows>=0, n_cols>=1, ldx>=n_cols");
   if (group_size_bytes <= 0 || max_size_bytes <= 0 || max_size_bytes % group_size_bytes)
     return fail(GNB_EINVAL, "fit_stats: need 0 < group_size_bytes dividing max_size_bytes");
   if (n_classes < 2 || n_classes > GNB_MAX_CLASSES)
     return fail(GNB_EINVAL, "fit_stats: n_classes must be in [2, %d]", GNB_MAX_CLASSES);
+  if (x_type != GNB_X_I32 && x_type != GNB_X_U16 && x_type != GNB_X_U8)
+    return fail(GNB_EINVAL, "fit_stats: unknown x_type %d", x_type);
   if (!sums || !counts) return fail(GNB_EINVAL, "fit_stats: null output");
   if (n_rows > 0 && (!x || !size_bytes || !labels)) return fail(GNB_EINVAL, "fit_stats: null input");
-  if (n_rows > 0 && !tma_ok(x, ldx))
-    return fail(GNB_EUNSUPPORTED, "fit_stats: X must be 16-byte aligned with ldx %% 4 == 0");
+  if (n_rows > 0 && !tma_ok(x, ldx, x_type))
+    return fail(GNB_EUNSUPPORTED, "fit_stats: X must be 16-byte aligned with a 16-byte row pitch");
   const int64_t G = max_size_bytes / group_size_bytes;
   const int64_t keys = G * n_classes;
   if (keys > (int64_t(1) << 30)) return fail(GNB_EINVAL, "fit_stats: too many groups");
@@ -310,12 +311,15 @@ int gnb_fit_stats(const int32_t* x, int64_t n_rows, int32_t n_cols, int64_t ldx,
     GNB_CUDA(cudaMemsetAsync(counts, 0, keys * sizeof(double), stream), "memset");
     if (status) GNB_CUDA(cudaMemsetAsync(status, 0, 2 * sizeof(unsigned long long), stream), "memset");
   }
+  const int eb = elem_bytes(x_type);
   for (int64_t r0 = 0; r0 < n_rows; r0 += kMaxRowsPerLaunch) {
     const int64_t n = std::min(kMaxRowsPerLaunch, n_rows - r0);
     CUtensorMap map;
-    if (!encode_map(&map, x + r0 * ldx, n, n_cols, ldx, fit_box_rows(), false))
+    const void* xr = static_cast<const uint8_t*>(x) + r0 * ldx * eb;
+    if (!encode_map(&map, xr, n, n_cols, ldx, fit_box_rows(), false, x_type))
       return fail(GNB_ECUDA, "fit_stats: cuTensorMapEncodeTiled failed");
     FitParams p{};
+    p.x_type = x_type;
     p.n_rows = n;
     p.n_cols = n_cols;
     p.size = size_bytes + r0;
@@ -331,6 +335,26 @@ int gnb_fit_stats(const int32_t* x, int64_t n_rows, int32_t n_cols, int64_t ldx,
     GNB_CUDA(fit_launch(map, p, stream), "fit launch");
   }
   return GNB_OK;
+}
+
+int gnb_fit_stats(const int32_t* x, int64_t n_rows, int32_t n_cols, int64_t ldx,
+                  const int32_t* size_bytes, const int32_t* labels, int32_t group_size_bytes,
+                  int32_t max_size_bytes, int32_t n_classes, double* sums, double* sumsq,
+                  double* counts, unsigned long long* status, int32_t accumulate,
+                  uintptr_t stream) {
+  return fit_stats_device(x, GNB_X_I32, n_rows, n_cols, ldx, size_bytes, labels,
+                          group_size_bytes, max_size_bytes, n_classes, sums, sumsq, counts, status,
+                          accumulate, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int gnb_fit_stats_typed(const void* x, int32_t x_type, int64_t n_rows, int32_t n_cols,
+                        int64_t ldx, const int32_t* size_bytes, const int32_t* labels,
+                        int32_t group_size_bytes, int32_t max_size_bytes, int32_t n_classes,
+                        double* sums, double* sumsq, double* counts, unsigned long long* status,
+                        int32_t accumulate, uintptr_t stream) {
+  return fit_stats_device(x, x_type, n_rows, n_cols, ldx, size_bytes, labels, group_size_bytes,
+                          max_size_bytes, n_classes, sums, sumsq, counts, status, accumulate,
+                          reinterpret_cast<cudaStream_t>(stream));
 }
 
 int gnb_generate(int32_t* x, int64_t n_rows, int32_t n_cols, int64_t ldx, int32_t* size_bytes,

@@ -37,9 +37,20 @@ namespace gnb {
 
 constexpr int kFitRows = 128;        // rows per tile (u8 permutation, 4 keys per lane)
 constexpr int kKeysPerLane = kFitRows / 32;
-constexpr int kGroupCols = 64;       // columns per stage: 2 boxes of 32
-constexpr int kBoxesPerStage = kGroupCols / kChunkCols;
 constexpr int kMaxHistKeys = 4096;   // keys sorted by the shared-memory histogram
+
+// Stage geometry per X storage: a lane owns CPL consecutive columns.
+//   int32 : 2 boxes x 32 columns = 64 columns, CPL 2 (LDS.64)
+//   uint16: 1 box  x 64 columns  = 64 columns, CPL 2 (LDS.32)
+//   uint8 : 1 box  x 128 columns = 128 columns, CPL 4 (LDS.32)
+template <typename T>
+struct FitGeom {
+  static constexpr int kBoxCols = kChunkBytesPerRow / static_cast<int>(sizeof(T));
+  static constexpr int kBoxes = sizeof(T) == 4 ? 2 : 1;
+  static constexpr int kGroupCols = kBoxCols * kBoxes;
+  static constexpr int kCPL = kGroupCols / 32;
+  static constexpr int kLaneBytes = kCPL * static_cast<int>(sizeof(T));
+};
 
 struct FitHdr {
   int n_runs;
@@ -48,10 +59,10 @@ struct FitHdr {
   int2 runs[kFitRows];  // {key, start | len << 16}
 };
 
-template <int NW, int STAGES>
+template <typename T, int NW, int STAGES>
 struct FitSmem {
   static constexpr int kBox = kFitRows * kChunkBytesPerRow;  // 16 KB
-  static constexpr int kStage = kBoxesPerStage * kBox;        // 32 KB
+  static constexpr int kStage = FitGeom<T>::kBoxes * kBox;    // 32 / 16 KB
   static constexpr int kX = 0;
   static constexpr int kHdr = kX + STAGES * kStage;
   static constexpr int kScratch = kHdr + STAGES * static_cast<int>(sizeof(FitHdr));
@@ -68,15 +79,38 @@ __device__ __forceinline__ void add_u64x2(unsigned long long* p, unsigned long l
   *reinterpret_cast<ulonglong2*>(p) = v;
 }
 
-template <int NW, int STAGES>
+// column e (< CPL) of a lane's slice of one box row
+template <typename T>
+__device__ __forceinline__ void load_lane(const uint8_t* at, uint32_t (&x)[FitGeom<T>::kCPL]) {
+  if constexpr (sizeof(T) == 4) {
+    const uint2 v = *reinterpret_cast<const uint2*>(at);
+    x[0] = v.x;
+    x[1] = v.y;
+  } else if constexpr (sizeof(T) == 2) {
+    const uint32_t w = *reinterpret_cast<const uint32_t*>(at);
+    x[0] = w & 0xffffu;
+    x[1] = w >> 16;
+  } else {
+    const uint32_t w = *reinterpret_cast<const uint32_t*>(at);
+    x[0] = w & 0xffu;
+    x[1] = (w >> 8) & 0xffu;
+    x[2] = (w >> 16) & 0xffu;
+    x[3] = w >> 24;
+  }
+}
+
+template <typename T, int NW, int STAGES>
 __global__ void __launch_bounds__((NW + 1) * 32)
     fit_tma_kernel(const __grid_constant__ CUtensorMap xmap, const FitParams p) {
-  using L = FitSmem<NW, STAGES>;
+  using L = FitSmem<T, NW, STAGES>;
+  using Geo = FitGeom<T>;
+  constexpr int kGroupCols = Geo::kGroupCols;
+  constexpr int CPL = Geo::kCPL;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::kBar);
   uint64_t* empty = full + STAGES;
-  const int NG = p.n_chunks;         // 64-column groups
+  const int NG = p.n_chunks;         // column groups of kGroupCols
   const int Vp = NG * kGroupCols;
   const int KS = p.smem_keys;
   unsigned long long* part_s = reinterpret_cast<unsigned long long*>(smem + L::kPart);
@@ -243,13 +277,13 @@ __global__ void __launch_bounds__((NW + 1) * 32)
         if (lane == 0) hdr->n_runs = n_runs;
         __syncwarp();
         if (lane == 0) {
-          const int boxes = min(kBoxesPerStage,
-                                (p.n_cols - cg * kGroupCols + kChunkCols - 1) / kChunkCols);
+          const int boxes = min(Geo::kBoxes, (p.n_cols - cg * kGroupCols + Geo::kBoxCols - 1) /
+                                                 Geo::kBoxCols);
           mbar_arrive_expect_tx(&full[stage], boxes * L::kBox);
           for (int b = 0; b < boxes; ++b)
             tma_load_2d(smem + L::kX + stage * L::kStage + b * L::kBox, &xmap,
-                        cg * kGroupCols + b * kChunkCols, static_cast<int32_t>(r0), &full[stage],
-                        pol_x);
+                        cg * kGroupCols + b * Geo::kBoxCols, static_cast<int32_t>(r0),
+                        &full[stage], pol_x);
         } else {
           mbar_arrive(&full[stage]);
         }
@@ -271,8 +305,9 @@ __global__ void __launch_bounds__((NW + 1) * 32)
     }
   } else {
     // ------------------------------------------------------------ consumers
-    // lane owns columns 2*lane, 2*lane+1 of the group: box lane/16, bytes (lane%16)*8
-    const uint32_t lane_off = static_cast<uint32_t>(lane >> 4) * L::kBox + (lane & 15) * 8;
+    // lane owns columns CPL*lane .. CPL*lane+CPL-1 of the group
+    const uint32_t lane_byte = static_cast<uint32_t>(lane) * Geo::kLaneBytes;
+    const uint32_t lane_off = (lane_byte / kChunkBytesPerRow) * L::kBox + lane_byte % kChunkBytesPerRow;
     int stage = 0;
     uint32_t phase = 0;
     for (int64_t tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
@@ -281,7 +316,7 @@ __global__ void __launch_bounds__((NW + 1) * 32)
         const FitHdr* hdr =
             reinterpret_cast<const FitHdr*>(smem + L::kHdr + stage * sizeof(FitHdr));
         const uint8_t* xs = smem + L::kX + stage * L::kStage + lane_off;
-        const int col0 = cg * kGroupCols + 2 * lane;
+        const int col0 = cg * kGroupCols + CPL * lane;
         const int n_runs = hdr->n_runs;
         for (int rb = 0; rb < n_runs; rb += 32) {
           // lane j holds run rb+j; the warp walks only the runs of its keys
@@ -294,42 +329,48 @@ __global__ void __launch_bounds__((NW + 1) * 32)
             const int k = __shfl_sync(~0u, mine.x, j);
             const int packed = __shfl_sync(~0u, mine.y, j);
             const int start = packed & 0xffff, len = packed >> 16;
-            unsigned long long s0 = 0, s1 = 0, q0 = 0, q1 = 0;
+            unsigned long long sa[CPL], qa[CPL];
+#pragma unroll
+            for (int e = 0; e < CPL; ++e) sa[e] = qa[e] = 0;
             int i = 0;
             for (; i + 4 <= len; i += 4) {
-              uint2 v[4];
+              uint32_t v[4][CPL];
 #pragma unroll
               for (int u = 0; u < 4; ++u) {
                 const uint32_t r = hdr->perm[start + i + u];
-                v[u] = *reinterpret_cast<const uint2*>(xs + (r << 7));
+                load_lane<T>(xs + (r << 7), v[u]);
               }
 #pragma unroll
-              for (int u = 0; u < 4; ++u) {
-                s0 += v[u].x;
-                s1 += v[u].y;
-                q0 += static_cast<unsigned long long>(v[u].x) * v[u].x;
-                q1 += static_cast<unsigned long long>(v[u].y) * v[u].y;
-              }
+              for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int e = 0; e < CPL; ++e) {
+                  sa[e] += v[u][e];
+                  qa[e] += static_cast<unsigned long long>(v[u][e]) * v[u][e];
+                }
             }
             for (; i < len; ++i) {
-              const uint32_t r = hdr->perm[start + i];
-              const uint2 v = *reinterpret_cast<const uint2*>(xs + (r << 7));
-              s0 += v.x;
-              s1 += v.y;
-              q0 += static_cast<unsigned long long>(v.x) * v.x;
-              q1 += static_cast<unsigned long long>(v.y) * v.y;
+              uint32_t v[CPL];
+              load_lane<T>(xs + (static_cast<uint32_t>(hdr->perm[start + i]) << 7), v);
+#pragma unroll
+              for (int e = 0; e < CPL; ++e) {
+                sa[e] += v[e];
+                qa[e] += static_cast<unsigned long long>(v[e]) * v[e];
+              }
             }
             if (k < KS) {
-              add_u64x2(part_s + static_cast<int64_t>(k) * Vp + col0, s0, s1);
-              if (p.sumsq) add_u64x2(part_q + static_cast<int64_t>(k) * Vp + col0, q0, q1);
-            } else {
-              const unsigned long long sv[2] = {s0, s1}, qv[2] = {q0, q1};
 #pragma unroll
-              for (int e = 0; e < 2; ++e) {
+              for (int e = 0; e < CPL; e += 2) {
+                add_u64x2(part_s + static_cast<int64_t>(k) * Vp + col0 + e, sa[e], sa[e + 1]);
+                if (p.sumsq)
+                  add_u64x2(part_q + static_cast<int64_t>(k) * Vp + col0 + e, qa[e], qa[e + 1]);
+              }
+            } else {
+#pragma unroll
+              for (int e = 0; e < CPL; ++e) {
                 if (col0 + e >= p.n_cols) break;
                 const int64_t o = static_cast<int64_t>(k) * p.n_cols + col0 + e;
-                if (sv[e]) atomicAdd(p.sums + o, static_cast<double>(sv[e]));
-                if (p.sumsq && qv[e]) atomicAdd(p.sumsq + o, static_cast<double>(qv[e]));
+                if (sa[e]) atomicAdd(p.sums + o, static_cast<double>(sa[e]));
+                if (p.sumsq && qa[e]) atomicAdd(p.sumsq + o, static_cast<double>(qa[e]));
               }
             }
           }
@@ -356,11 +397,13 @@ __global__ void __launch_bounds__((NW + 1) * 32)
     if (part_n[k]) atomicAdd(p.counts + k, static_cast<double>(part_n[k]));
 }
 
-template <int NW, int STAGES>
+template <typename T, int NW, int STAGES>
 static cudaError_t launch_fit(const CUtensorMap& map, FitParams p, cudaStream_t stream,
                               int ctas_per_sm) {
-  using L = FitSmem<NW, STAGES>;
-  auto kern = fit_tma_kernel<NW, STAGES>;
+  using L = FitSmem<T, NW, STAGES>;
+  auto kern = fit_tma_kernel<T, NW, STAGES>;
+  constexpr int kGroupCols = FitGeom<T>::kGroupCols;
+  p.n_chunks = (p.n_cols + kGroupCols - 1) / kGroupCols;
   int dev = 0, sms = 0, max_smem = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -405,23 +448,32 @@ static int fit_variant() {
   return v;
 }
 
-template <int NW>
+template <typename T, int NW>
 static cudaError_t launch_fit_nw(const CUtensorMap& map, const FitParams& p, cudaStream_t stream) {
   switch (fit_variant()) {
-    case 1: return launch_fit<NW, 4>(map, p, stream, 1);
-    case 2: return launch_fit<NW, 5>(map, p, stream, 1);
-    case 3: return launch_fit<NW, 3>(map, p, stream, 1);
-    default: return launch_fit<NW, 2>(map, p, stream, 2);
+    case 1: return launch_fit<T, NW, 4>(map, p, stream, 1);
+    case 2: return launch_fit<T, NW, 5>(map, p, stream, 1);
+    case 3: return launch_fit<T, NW, 3>(map, p, stream, 1);
+    default: return launch_fit<T, NW, 2>(map, p, stream, 2);
   }
 }
 
-cudaError_t fit_launch(const CUtensorMap& map, FitParams p, cudaStream_t stream) {
-  p.n_chunks = (p.n_cols + kGroupCols - 1) / kGroupCols;  // 64-column groups
-  p.n_tiles = (p.n_rows + kFitRows - 1) / kFitRows;
+template <typename T>
+static cudaError_t launch_fit_typed(const CUtensorMap& map, const FitParams& p,
+                                   cudaStream_t stream) {
   // keys are dealt to warps round-robin: no more warps than keys
-  if (p.n_keys >= 4) return launch_fit_nw<4>(map, p, stream);
-  if (p.n_keys >= 2) return launch_fit_nw<2>(map, p, stream);
-  return launch_fit_nw<1>(map, p, stream);
+  if (p.n_keys >= 4) return launch_fit_nw<T, 4>(map, p, stream);
+  if (p.n_keys >= 2) return launch_fit_nw<T, 2>(map, p, stream);
+  return launch_fit_nw<T, 1>(map, p, stream);
+}
+
+cudaError_t fit_launch(const CUtensorMap& map, FitParams p, cudaStream_t stream) {
+  p.n_tiles = (p.n_rows + kFitRows - 1) / kFitRows;
+  switch (p.x_type) {
+    case GNB_X_U16: return launch_fit_typed<uint16_t>(map, p, stream);
+    case GNB_X_U8: return launch_fit_typed<uint8_t>(map, p, stream);
+    default: return launch_fit_typed<int32_t>(map, p, stream);
+  }
 }
 
 }  // namespace gnb

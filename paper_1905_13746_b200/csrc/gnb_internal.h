@@ -34,6 +34,7 @@ struct PredictParams {
 };
 
 struct FitParams {
+  int32_t x_type;  // GNB_X_I32 / GNB_X_U16 / GNB_X_U8
   int64_t n_rows;
   int32_t n_cols;
   int32_t n_chunks;

@@ -218,8 +218,9 @@ class FitStats:
 def fit_stats(x: torch.Tensor, size_bytes: torch.Tensor, labels: torch.Tensor, *,
               n_classes: int, group_size_bytes: int, max_size_bytes: int, sumsq: bool = True,
               out: FitStats | None = None, accumulate: bool = False, stream=None) -> FitStats:
-    """Per-(size group, class, column) sums / sums of squares / row counts."""
-    xp, n, V, ldx = _rows(x)
+    """Per-(size group, class, column) sums / sums of squares / row counts.
+    x may be int32, uint16 or uint8 (same counts, fewer bytes)."""
+    xp, n, V, ldx = _rows(x, dtypes=tuple(_X_TYPES))
     if max_size_bytes <= 0 or group_size_bytes <= 0 or max_size_bytes % group_size_bytes:
         raise InvalidConfigError("group_size_bytes must divide max_size_bytes")
     G = max_size_bytes // group_size_bytes
@@ -230,11 +231,12 @@ def fit_stats(x: torch.Tensor, size_bytes: torch.Tensor, labels: torch.Tensor, *
             torch.zeros((G, n_classes, V), dtype=torch.float64, device=dev) if sumsq else None,
             torch.zeros((G, n_classes), dtype=torch.float64, device=dev),
             torch.zeros(2, dtype=torch.int64, device=dev))
-    N.check(N.lib.gnb_fit_stats(
-        xp, n, V, ldx, _vec(size_bytes, n, "size_bytes"), _vec(labels, n, "labels"),
+    N.check(N.lib.gnb_fit_stats_typed(
+        xp, _X_TYPES[x.dtype], n, V, ldx, _vec(size_bytes, n, "size_bytes"),
+        _vec(labels, n, "labels"),
         group_size_bytes, max_size_bytes, n_classes, out.sums.data_ptr(),
         out.sumsq.data_ptr() if out.sumsq is not None else None, out.counts.data_ptr(),
-        out.status.data_ptr(), 1 if accumulate else 0, _stream(stream)), "gnb_fit_stats")
+        out.status.data_ptr(), 1 if accumulate else 0, _stream(stream)), "gnb_fit_stats_typed")
     return out
 
 

@@ -93,3 +93,30 @@ def test_accumulate_over_chunks_equals_one_pass():
     torch.cuda.synchronize()
     assert torch.equal(whole.sums, acc.sums) and torch.equal(whole.counts, acc.counts)
     assert torch.equal(whole.sumsq, acc.sumsq)
+
+
+@pytest.mark.parametrize("dtype,hi", [(torch.uint8, 256), (torch.uint16, 65536)])
+@pytest.mark.parametrize("V", [1, 33, 64, 100, 128, 129, 256, 300])
+@pytest.mark.parametrize("C", [2, 16])
+def test_narrow_storage_fit(dtype, hi, V, C):
+    """uint8 / uint16 X: identical statistics to the int32 oracle."""
+    rng = np.random.default_rng(V * 3 + C)
+    N, G = 4000, 3
+    x = rng.integers(0, hi, size=(N, V))
+    size = rng.integers(-10, G * 100 + 10, size=N)
+    label = rng.integers(-1, C + 1, size=N)
+    dev = torch.device("cuda")
+    esz = torch.tensor([], dtype=dtype).element_size()
+    ld = (V * esz + 15) // 16 * 16 // esz
+    base = torch.zeros((N, ld), dtype=torch.int32, device=dev)
+    base[:, :V] = torch.from_numpy(x.astype(np.int32)).to(dev)
+    xd = base.to(dtype)[:, :V]
+    st = dense.fit_stats(xd, torch.from_numpy(size.astype(np.int32)).to(dev),
+                         torch.from_numpy(label.astype(np.int32)).to(dev), n_classes=C,
+                         group_size_bytes=100, max_size_bytes=G * 100)
+    torch.cuda.synchronize()
+    S, Q, n, bad, oor = O.fit_stats(x, size, label, C, 100, G * 100)
+    assert np.array_equal(st.sums.cpu().numpy(), S.astype(np.float64))
+    assert np.array_equal(st.sumsq.cpu().numpy(), Q.astype(np.float64))
+    assert np.array_equal(st.counts.cpu().numpy(), n.astype(np.float64))
+    assert st.status.cpu().tolist() == [bad, oor]
