@@ -54,6 +54,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-logpost", action="store_true")
     ap.add_argument("--fit-rows", type=int, default=1_000_000_000)
+    ap.add_argument("--dist-backend", choices=("nccl", "gloo"), default="nccl",
+                    help="gloo: exercise the multi-rank path with ranks sharing one GPU "
+                         "(host-side collectives only; testing, not a bench number)")
     ap.add_argument("--x-dtype", choices=("int32", "uint16", "uint8"), default="int32",
                     help="storage of the predict matrix (same counts; narrower = fewer bytes)")
     ap.add_argument("--workload", choices=("predict", "sweep", "ragged", "fit"), default="predict",
@@ -156,11 +159,19 @@ def dist_init(args):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1 and not dist.is_initialized():
-        backend = "nccl" if args.impl == "ours" else "gloo"
+        backend = args.dist_backend if args.impl == "ours" else "gloo"
         if args.impl == "ours":
+            if backend == "gloo":          # test mode: every rank may share GPU 0
+                local = local % max(torch.cuda.device_count(), 1)
             torch.cuda.set_device(local)
         dist.init_process_group(backend=backend)
     return world, rank, local
+
+
+def _coll_device(device):
+    """Collectives run where the backend can: CUDA tensors for NCCL, CPU for gloo."""
+    import torch.distributed as dist
+    return device if dist.get_backend() == "nccl" else "cpu"
 
 
 def barrier_max(value: float, world: int, device=None) -> float:
@@ -168,7 +179,7 @@ def barrier_max(value: float, world: int, device=None) -> float:
         return value
     import torch
     import torch.distributed as dist
-    t = torch.tensor([value], dtype=torch.float64, device=device)
+    t = torch.tensor([value], dtype=torch.float64, device=_coll_device(device))
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -178,7 +189,7 @@ def barrier_sum(value: float, world: int, device=None) -> float:
         return value
     import torch
     import torch.distributed as dist
-    t = torch.tensor([value], dtype=torch.float64, device=device)
+    t = torch.tensor([value], dtype=torch.float64, device=_coll_device(device))
     dist.all_reduce(t, op=dist.ReduceOp.SUM)
     return float(t.item())
 
@@ -193,8 +204,7 @@ def run_ours(args, world, rank, local):
     from paper_1905_13746_b200 import dense
     from paper_1905_13746_b200.sharding import allreduce_stats
 
-    dev = torch.device("cuda", local)
-    torch.cuda.set_device(dev)
+    dev = torch.device("cuda", torch.cuda.current_device())
     n, V = args.rows, args.features
     width = 5120
     offset = rank * n                      # contiguous shard of the global index space
@@ -630,7 +640,9 @@ def run_fit(args, world, rank, local):
     rows_here = hi - lo
     n_total = float(st.counts.sum().item())
     return {"metric": "samples fitted/sec (sums, sums of squares, counts)", "unit": UNIT,
-            "workload": "cfg5: fit 1B samples x 128 features, 16 classes, 1 size group",
+            "workload": (f"cfg5: fit {total:,} samples x 128 features, 16 classes, 1 size group"
+                         if total == 1_000_000_000 else
+                         f"fit {total:,} samples x 128 features, 16 classes"),
             "value": round(total / ((ms + ar_ms) / 1e3), 1), "fit_kernel_ms": round(ms, 3),
             "allreduce_ms": round(ar_ms, 4), "n_gpus": world,
             "achieved_gbs_per_gpu": round(rows_here * bps / (ms / 1e3) / 1e9, 1),

@@ -28,5 +28,9 @@ def allreduce_stats(stats, group=None):
     if not dist.is_available() or not dist.is_initialized() or dist.get_world_size(group) == 1:
         return stats
     flat = stats.packed()
+    if dist.get_backend(group) == "gloo" and flat.is_cuda:   # gloo reduces host tensors
+        host = flat.cpu()
+        dist.all_reduce(host, op=dist.ReduceOp.SUM, group=group)
+        return stats.unpack_(host.to(flat.device))
     dist.all_reduce(flat, op=dist.ReduceOp.SUM, group=group)
     return stats.unpack_(flat)
