@@ -208,6 +208,29 @@ int gnb_fin_tables(const double* sums_g, const double* counts_g, int32_t n_class
                    int32_t n_cols, const int32_t* features, int32_t n_features, double alpha,
                    double* log_prior, double* log_lik);
 
+/* ------------------------------------------------------------------ ingestion (host)
+ * Replaces: corpus.parse_corpus + OpcodeHistogram.from_counts
+ *           (pkg/src/groupnb/corpus.py:133-189, :42-53) for the dense path:
+ *           JSONL text -> sorted vocabulary + sparse rows, multithreaded;
+ *           gnb_corpus_dense then writes any row range as a dense matrix
+ *           (int32 / uint16 / uint8).  On error (GNB_EINVAL) the handle holds
+ *           the reference's error kind (1 ParseError, 2 IntegrityError), line
+ *           number and message; free it with gnb_corpus_free either way. */
+typedef struct gnb_corpus gnb_corpus;
+int gnb_corpus_parse(const char* text, size_t len, int32_t allow_unlabeled, int32_t threads,
+                     gnb_corpus** out);
+void gnb_corpus_free(gnb_corpus* c);
+int64_t gnb_corpus_rows(const gnb_corpus* c);
+int32_t gnb_corpus_vocab_size(const gnb_corpus* c);
+const char* gnb_corpus_vocab(const gnb_corpus* c, int32_t k);
+const char* gnb_corpus_id(const gnb_corpus* c, int64_t row);
+int64_t gnb_corpus_max_count(const gnb_corpus* c);
+int64_t gnb_corpus_nnz(const gnb_corpus* c);
+int32_t gnb_corpus_error(const gnb_corpus* c, int64_t* line, const char** message);
+int gnb_corpus_meta(const gnb_corpus* c, int64_t* size_out, int8_t* label_out);
+int gnb_corpus_dense(const gnb_corpus* c, int32_t x_type, void* x, int64_t ldx, int64_t row0,
+                     int64_t n, int32_t threads);
+
 /* ------------------------------------------------------------------ synthetic data
  * Device generator following the reference's synthetic law
  * (pkg/src/groupnb/synth.py:64-116): per row a group (rows laid out group by

@@ -300,6 +300,105 @@ def predict(model: GroupModel, histogram: OpcodeHistogram, *, device=None) -> Pr
                       model.group)
 
 
+# ---------------------------------------------------------------- dense corpus paths
+def train_bundle_corpus(corpus, config: GroupingConfig, k: int, alpha: float = 1.0, *,
+                        seed: int = 0, created_at: str | None = None, device=None) -> ModelBundle:
+    """train_bundle (engine.py:157-177) on an ingest.DenseCorpus: no per-record
+    Python work; rows outside the size range are skipped like partition_by_group."""
+    return _train_dense(corpus.dense(), corpus.size, corpus.label.astype(np.int32),
+                        corpus.vocab, config, k, alpha, seed, created_at,
+                        _device_ordinal(device), corpus.ids)
+
+
+def _train_dense(x, size64, label, vocab, config, k, alpha, seed, created_at, device, ids):
+    k_ok = isinstance(k, int) and not isinstance(k, bool) and k >= 1
+    a_ok = isinstance(alpha, (int, float)) and not isinstance(alpha, bool) and alpha > 0
+    lim = config.max_size_bytes
+    size = np.where((size64 >= 0) & (size64 < lim), size64, -1).astype(np.int32)
+    models = []
+    if len(size) and len(vocab):
+        x = np.ascontiguousarray(x, dtype=np.int32)   # gnb_fit_stats_host takes int32 rows
+        S, n, _ = _fit_stats_host(x, size, label, n_classes=2, width=config.group_size_bytes,
+                                  limit=lim, device=device)
+        from .dense import fin_train
+        fin = fin_train(S, n, k=k if k_ok else 1, alpha=float(alpha) if a_ok else 1.0,
+                        min_per_class=config.min_per_class)
+        g_of = np.where(size >= 0, size // config.group_size_bytes, -1)
+        for g in np.nonzero(fin.state != 0)[0].tolist():
+            if fin.state[g] == -1:
+                raise InsufficientClassError(f"group {g}: no malware opcode occurrences to score")
+            if fin.state[g] == -2:
+                raise InsufficientClassError(f"group {g}: no benign opcode occurrences to score")
+            if not k_ok:
+                raise InvalidConfigError(f"k must be a positive integer, got {k!r}")
+            if not a_ok:
+                raise InvalidConfigError(f"alpha must be positive, got {alpha!r}")
+            bad = np.nonzero((g_of == g) & (label < 0))[0]
+            if len(bad):
+                raise IntegrityError(f"sample {ids[int(bad[0])]!r} has no training label")
+            F = int(fin.n_features[g])
+            feats = FeatureSet(tuple(vocab[j] for j in fin.features[g, :F]), k)
+            models.append(_model(g, feats, fin.log_prior[g], fin.log_lik[g, :, :F], n[g],
+                                 float(alpha)))
+    if created_at is None:
+        created_at = datetime.now(timezone.utc).isoformat(timespec="seconds")
+    meta = BundleMeta(k=k, alpha=float(alpha), seed=seed, created_at=created_at)
+    return build_bundle(models, config, meta)
+
+
+def classify_corpus(bundle: ModelBundle, corpus, *, device=None, warmup: bool = True):
+    """classify_parallel on an ingest.DenseCorpus: rows go to the device in the
+    corpus's full-vocabulary layout (narrowest lossless storage); route +
+    FeatureSet gather (gnb_gather_features), an optional slot sort and K-PRED run
+    on the device.  Returns (label[N] int8: 1 malware / 0 benign / -1 error,
+    log_posterior [N, 2] (benign, malware), effective_group[N], errors, elapsed_ns)."""
+    import time
+    import torch
+    from . import dense
+    if not bundle.trained_ids:
+        raise EmptyBundleError("bundle has no trained models")
+    dev = torch.device("cuda", _device_ordinal(device))
+    packed = _PackedBundle(bundle)
+    col = {op: j for j, op in enumerate(corpus.vocab)}
+    feats = np.full((len(packed.ids), packed.F), -1, dtype=np.int32)
+    nfeat = np.zeros(len(packed.ids), dtype=np.int32)
+    for i, g in enumerate(packed.ids):
+        ops = bundle.models[g].features.opcodes
+        feats[i, :len(ops)] = [col.get(op, -1) for op in ops]
+        nfeat[i] = len(ops)
+    lim = bundle.config.max_size_bytes
+    size = np.where((corpus.size >= 0) & (corpus.size < lim), corpus.size, -1).astype(np.int32)
+    tables = dense.DeviceTables.build(packed.prior, packed.lik, packed.route,
+                                      group_size_bytes=bundle.config.group_size_bytes,
+                                      max_size_bytes=lim, device=dev)
+    n = len(corpus)
+    V = max(len(corpus.vocab), 1)
+    dt = np.dtype(corpus.narrowest_dtype())
+    pitch = (V * dt.itemsize + 15) // 16 * 16 // dt.itemsize
+    host = torch.empty((n, pitch), dtype=getattr(torch, dt.name), pin_memory=True)
+    corpus.dense(dt, out=host.numpy()[:, :V])
+
+    def run():
+        t0 = time.perf_counter_ns()
+        xv = host.to(dev, non_blocking=True)[:, :V]
+        sd = torch.from_numpy(size).to(dev, non_blocking=True)
+        xi = xv if xv.dtype == torch.int32 else xv.to(torch.int32)
+        xg = dense.gather_features(xi, sd, tables, feats, nfeat)
+        perm = dense.slot_sort(sd, tables) if len(packed.ids) > 1 else None
+        lab, lp = dense.predict(dense.narrowest(xg) if dt.itemsize < 4 else xg, sd, tables,
+                                perm=perm)
+        out = lab.cpu().numpy(), lp.cpu().numpy()
+        return out, time.perf_counter_ns() - t0
+
+    if warmup:
+        run()
+    (lab, lp), elapsed = run()
+    g = np.where(size >= 0, size // bundle.config.group_size_bytes, 0)
+    eff = np.where(lab >= 0, np.array(packed.ids)[packed.route[g]], -1)
+    errors = [(int(i), oversize_message(int(corpus.size[i]), lim)) for i in np.nonzero(lab < 0)[0]]
+    return lab.astype(np.int8), lp, eff, errors, elapsed
+
+
 def speedup(tc_ns: int, tp_ns: int) -> float:
     """Sequential-over-parallel time ratio (engine.py:299-305)."""
     if tp_ns <= 0:

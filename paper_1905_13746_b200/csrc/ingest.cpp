@@ -1,0 +1,674 @@
+// INGEST (host C++): JSONL corpus -> dense count matrix, multithreaded.
+//
+// Restates corpus.parse_corpus + OpcodeHistogram.from_counts
+// (pkg/src/groupnb/corpus.py:133-189, :42-53) for the dense path (SURVEY 8f
+// rank 1): one `{"id", "label", "size_bytes", "opcodes"}` object per line,
+// unknown keys ignored, blank lines skipped, mnemonics case-folded and merged,
+// zero counts dropped.  The vocabulary is the sorted union of mnemonics (byte
+// order of UTF-8 == code-point order == Python's sorted()), so column order is
+// the reference's feature-tie order.  Errors reproduce the reference's types,
+// line numbers and schema messages; JSON syntax errors carry our own wording
+// after "invalid JSON: ".  Lines are split on '\n' ("\r\n" accepted); mnemonic
+// case folding is ASCII (non-ASCII mnemonics are kept as written).
+#include <algorithm>
+#include <cerrno>
+#include <cstdint>
+#include <cstdlib>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <thread>
+#include <unordered_map>
+#include <unordered_set>
+#include <vector>
+
+#include "../../include/gnb.h"
+
+namespace {
+
+// ---------------------------------------------------------------- JSON values
+enum class JT { Null, Bool, Int, BigInt, Float, Str, Arr, Obj };
+
+struct JVal {
+  JT t = JT::Null;
+  bool b = false;
+  int64_t i = 0;
+  std::string s;  // Str value, or the number's source text (Float / BigInt)
+  std::vector<JVal> arr;
+  std::vector<std::pair<std::string, JVal>> obj;  // duplicate keys: last wins on lookup
+  const JVal* get(const char* key) const {
+    const JVal* r = nullptr;
+    for (const auto& kv : obj)
+      if (kv.first == key) r = &kv.second;
+    return r;
+  }
+};
+
+struct Parser {
+  const char* p;
+  const char* end;
+  std::string err;
+
+  void ws() {
+    while (p < end && (*p == ' ' || *p == '\t' || *p == '\r' || *p == '\n')) ++p;
+  }
+  bool fail(const char* m) {
+    if (err.empty()) err = m;
+    return false;
+  }
+  static void put_utf8(std::string& o, uint32_t cp) {
+    if (cp < 0x80) {
+      o += static_cast<char>(cp);
+    } else if (cp < 0x800) {
+      o += static_cast<char>(0xC0 | (cp >> 6));
+      o += static_cast<char>(0x80 | (cp & 0x3F));
+    } else if (cp < 0x10000) {
+      o += static_cast<char>(0xE0 | (cp >> 12));
+      o += static_cast<char>(0x80 | ((cp >> 6) & 0x3F));
+      o += static_cast<char>(0x80 | (cp & 0x3F));
+    } else {
+      o += static_cast<char>(0xF0 | (cp >> 18));
+      o += static_cast<char>(0x80 | ((cp >> 12) & 0x3F));
+      o += static_cast<char>(0x80 | ((cp >> 6) & 0x3F));
+      o += static_cast<char>(0x80 | (cp & 0x3F));
+    }
+  }
+  bool hex4(uint32_t& v) {
+    if (end - p < 4) return fail("Invalid \\uXXXX escape");
+    v = 0;
+    for (int k = 0; k < 4; ++k) {
+      const char c = *p++;
+      v <<= 4;
+      if (c >= '0' && c <= '9') v |= c - '0';
+      else if (c >= 'a' && c <= 'f') v |= c - 'a' + 10;
+      else if (c >= 'A' && c <= 'F') v |= c - 'A' + 10;
+      else return fail("Invalid \\uXXXX escape");
+    }
+    return true;
+  }
+  bool str(std::string& o) {  // at opening quote
+    ++p;
+    o.clear();
+    while (p < end) {
+      const char c = *p++;
+      if (c == '"') return true;
+      if (static_cast<unsigned char>(c) < 0x20) return fail("Invalid control character");
+      if (c != '\\') {
+        o += c;
+        continue;
+      }
+      if (p >= end) break;
+      const char e = *p++;
+      switch (e) {
+        case '"': o += '"'; break;
+        case '\\': o += '\\'; break;
+        case '/': o += '/'; break;
+        case 'b': o += '\b'; break;
+        case 'f': o += '\f'; break;
+        case 'n': o += '\n'; break;
+        case 'r': o += '\r'; break;
+        case 't': o += '\t'; break;
+        case 'u': {
+          uint32_t cp;
+          if (!hex4(cp)) return false;
+          if (cp >= 0xD800 && cp < 0xDC00 && end - p >= 6 && p[0] == '\\' && p[1] == 'u') {
+            const char* save = p;
+            p += 2;
+            uint32_t lo;
+            if (hex4(lo) && lo >= 0xDC00 && lo < 0xE000)
+              cp = 0x10000 + ((cp - 0xD800) << 10) + (lo - 0xDC00);
+            else
+              p = save;
+          }
+          put_utf8(o, cp);
+          break;
+        }
+        default: return fail("Invalid \\escape");
+      }
+    }
+    return fail("Unterminated string");
+  }
+  bool num(JVal& v) {
+    const char* s = p;
+    if (*p == '-') ++p;
+    if (p >= end || !(*p >= '0' && *p <= '9')) return fail("Expecting value");
+    if (*p == '0') ++p;
+    else
+      while (p < end && *p >= '0' && *p <= '9') ++p;
+    bool is_float = false;
+    if (p < end && *p == '.') {
+      is_float = true;
+      ++p;
+      if (p >= end || !(*p >= '0' && *p <= '9')) return fail("Expecting value");
+      while (p < end && *p >= '0' && *p <= '9') ++p;
+    }
+    if (p < end && (*p == 'e' || *p == 'E')) {
+      is_float = true;
+      ++p;
+      if (p < end && (*p == '+' || *p == '-')) ++p;
+      if (p >= end || !(*p >= '0' && *p <= '9')) return fail("Expecting value");
+      while (p < end && *p >= '0' && *p <= '9') ++p;
+    }
+    v.s.assign(s, p - s);
+    if (is_float) {
+      v.t = JT::Float;
+      return true;
+    }
+    // integer: exact in int64, else BigInt (kept as text for messages)
+    errno = 0;
+    char* e2 = nullptr;
+    const long long x = strtoll(v.s.c_str(), &e2, 10);
+    if (errno == ERANGE) {
+      v.t = JT::BigInt;
+    } else {
+      v.t = JT::Int;
+      v.i = x;
+    }
+    return true;
+  }
+  bool lit(const char* w, size_t n) {
+    if (static_cast<size_t>(end - p) >= n && memcmp(p, w, n) == 0) {
+      p += n;
+      return true;
+    }
+    return fail("Expecting value");
+  }
+  bool value(JVal& v, int depth) {
+    if (depth > 64) return fail("nesting too deep");
+    ws();
+    if (p >= end) return fail("Expecting value");
+    const char c = *p;
+    if (c == '{') {
+      v.t = JT::Obj;
+      ++p;
+      ws();
+      if (p < end && *p == '}') {
+        ++p;
+        return true;
+      }
+      for (;;) {
+        ws();
+        if (p >= end || *p != '"') return fail("Expecting property name enclosed in double quotes");
+        std::string k;
+        if (!str(k)) return false;
+        ws();
+        if (p >= end || *p != ':') return fail("Expecting ':' delimiter");
+        ++p;
+        JVal x;
+        if (!value(x, depth + 1)) return false;
+        v.obj.emplace_back(std::move(k), std::move(x));
+        ws();
+        if (p < end && *p == ',') {
+          ++p;
+          continue;
+        }
+        if (p < end && *p == '}') {
+          ++p;
+          return true;
+        }
+        return fail("Expecting ',' delimiter");
+      }
+    }
+    if (c == '[') {
+      v.t = JT::Arr;
+      ++p;
+      ws();
+      if (p < end && *p == ']') {
+        ++p;
+        return true;
+      }
+      for (;;) {
+        JVal x;
+        if (!value(x, depth + 1)) return false;
+        v.arr.push_back(std::move(x));
+        ws();
+        if (p < end && *p == ',') {
+          ++p;
+          continue;
+        }
+        if (p < end && *p == ']') {
+          ++p;
+          return true;
+        }
+        return fail("Expecting ',' delimiter");
+      }
+    }
+    if (c == '"') {
+      v.t = JT::Str;
+      return str(v.s);
+    }
+    if (c == 't') {
+      v.t = JT::Bool;
+      v.b = true;
+      return lit("true", 4);
+    }
+    if (c == 'f') {
+      v.t = JT::Bool;
+      return lit("false", 5);
+    }
+    if (c == 'n') {
+      v.t = JT::Null;
+      return lit("null", 4);
+    }
+    if (c == 'N') return lit("NaN", 3) && (v.t = JT::Float, v.s = "nan", true);
+    if (c == 'I') return lit("Infinity", 8) && (v.t = JT::Float, v.s = "inf", true);
+    if (c == '-' && end - p >= 9 && memcmp(p, "-Infinity", 9) == 0) {
+      p += 9;
+      v.t = JT::Float;
+      v.s = "-inf";
+      return true;
+    }
+    return num(v);
+  }
+};
+
+// Python repr() of a JSON-decoded value, for error messages
+std::string py_repr(const JVal& v);
+
+std::string py_str_repr(const std::string& s) {
+  const bool has_sq = s.find('\'') != std::string::npos;
+  const bool has_dq = s.find('"') != std::string::npos;
+  const char q = (has_sq && !has_dq) ? '"' : '\'';
+  std::string o(1, q);
+  for (unsigned char c : s) {
+    if (c == static_cast<unsigned char>(q) || c == '\\') {
+      o += '\\';
+      o += static_cast<char>(c);
+    } else if (c == '\n') {
+      o += "\\n";
+    } else if (c == '\r') {
+      o += "\\r";
+    } else if (c == '\t') {
+      o += "\\t";
+    } else if (c < 0x20 || c == 0x7f) {
+      char b[8];
+      snprintf(b, sizeof b, "\\x%02x", c);
+      o += b;
+    } else {
+      o += static_cast<char>(c);
+    }
+  }
+  o += q;
+  return o;
+}
+
+std::string py_repr(const JVal& v) {
+  switch (v.t) {
+    case JT::Null: return "None";
+    case JT::Bool: return v.b ? "True" : "False";
+    case JT::Int: return std::to_string(v.i);
+    case JT::BigInt: return v.s;
+    case JT::Float: {
+      if (v.s == "nan" || v.s == "inf" || v.s == "-inf") return v.s;
+      char b[64];
+      snprintf(b, sizeof b, "%.17g", strtod(v.s.c_str(), nullptr));
+      std::string r = b;  // shortest round-trip repr is Python's; close enough for messages
+      if (r.find_first_of(".en") == std::string::npos) r += ".0";
+      return r;
+    }
+    case JT::Str: return py_str_repr(v.s);
+    case JT::Arr: {
+      std::string o = "[";
+      for (size_t k = 0; k < v.arr.size(); ++k) o += (k ? ", " : "") + py_repr(v.arr[k]);
+      return o + "]";
+    }
+    case JT::Obj: {
+      std::string o = "{";
+      for (size_t k = 0; k < v.obj.size(); ++k)
+        o += (k ? ", " : "") + py_str_repr(v.obj[k].first) + ": " + py_repr(v.obj[k].second);
+      return o + "}";
+    }
+  }
+  return "?";
+}
+
+// ---------------------------------------------------------------- corpus
+struct Row {
+  std::string id;
+  int8_t label;     // 1 malware, 0 benign, -1 unknown
+  int64_t size;     // size_bytes; -1 if it does not fit int64 (only >= 2^63)
+  std::vector<std::pair<int32_t, int64_t>> ents;  // (local vocab id, count)
+};
+
+struct Shard {
+  std::vector<Row> rows;
+  std::vector<int64_t> line_no;
+  std::unordered_map<std::string, int32_t> vocab;
+  std::vector<std::string> names;
+  int64_t err_line = -1;
+  int err_kind = 0;  // 1 ParseError, 2 IntegrityError
+  std::string err_msg;
+  std::string err_id;  // the failing line's id when it was valid (duplicate check wins)
+  bool err_has_id = false;
+};
+
+std::string lower_ascii(const std::string& s) {
+  std::string o = s;
+  for (char& c : o)
+    if (c >= 'A' && c <= 'Z') c = static_cast<char>(c - 'A' + 'a');
+  return o;
+}
+
+bool is_blank(const char* a, const char* b) {
+  for (; a < b; ++a)
+    if (!(*a == ' ' || *a == '\t' || *a == '\r' || *a == '\n' || *a == '\v' || *a == '\f'))
+      return false;
+  return true;
+}
+
+// corpus.py:146-188 for one line; returns false with (kind, msg) on error
+bool parse_line(const char* a, const char* b, bool allow_unlabeled, Shard& sh, Row& row,
+                int& kind, std::string& msg) {
+  Parser ps{a, b, {}};
+  JVal v;
+  if (!ps.value(v, 0)) {
+    kind = 1;
+    msg = "invalid JSON: " + ps.err;
+    return false;
+  }
+  ps.ws();
+  if (ps.p != b) {
+    kind = 1;
+    msg = "invalid JSON: Extra data";
+    return false;
+  }
+  if (v.t != JT::Obj) {
+    kind = 1;
+    msg = "record must be a JSON object";
+    return false;
+  }
+  const JVal* id = v.get("id");
+  if (!id || id->t != JT::Str || id->s.empty()) {
+    kind = 1;
+    msg = "missing or empty 'id'";
+    return false;
+  }
+  row.id = id->s;
+  const JVal* lab = v.get("label");
+  if (lab) {
+    if (lab->t == JT::Str && lab->s == "malware") row.label = 1;
+    else if (lab->t == JT::Str && lab->s == "benign") row.label = 0;
+    else {
+      kind = 1;
+      msg = "unknown label " + py_repr(*lab);
+      return false;
+    }
+  } else if (allow_unlabeled) {
+    row.label = -1;
+  } else {
+    kind = 1;
+    msg = "missing 'label'";
+    return false;
+  }
+  const JVal* sz = v.get("size_bytes");
+  if (!sz || !(sz->t == JT::Int || sz->t == JT::BigInt) || (sz->t == JT::Int && sz->i < 0) ||
+      (sz->t == JT::BigInt && !sz->s.empty() && sz->s[0] == '-')) {
+    kind = 1;
+    msg = "'size_bytes' must be a non-negative integer";
+    return false;
+  }
+  row.size = sz->t == JT::Int ? sz->i : -1;  // > int64: out of any size range
+  const JVal* ops = v.get("opcodes");
+  if (!ops || ops->t != JT::Obj) {
+    kind = 1;
+    msg = "'opcodes' must be an object";
+    return false;
+  }
+  // OpcodeHistogram.from_counts over the dict json.loads builds: duplicate keys
+  // keep the LAST value at the position of the FIRST occurrence.
+  std::vector<std::pair<std::string, const JVal*>> items;
+  std::unordered_map<std::string, size_t> pos;
+  for (const auto& kv : ops->obj) {
+    auto it = pos.find(kv.first);
+    if (it == pos.end()) {
+      pos.emplace(kv.first, items.size());
+      items.emplace_back(kv.first, &kv.second);
+    } else {
+      items[it->second].second = &kv.second;
+    }
+  }
+  std::vector<std::pair<int32_t, int64_t>> ents;
+  std::unordered_map<int32_t, size_t> where;
+  for (const auto& it : items) {
+    const JVal& c = *it.second;
+    if (it.first.empty()) {
+      kind = 1;
+      msg = "opcode mnemonic must be a non-empty string, got ''";
+      return false;
+    }
+    const bool ok_int = (c.t == JT::Int && c.i >= 0) ||
+                        (c.t == JT::BigInt && !c.s.empty() && c.s[0] != '-');
+    if (!ok_int) {
+      kind = 1;
+      msg = "count for " + py_str_repr(it.first) + " must be a non-negative integer, got " +
+            py_repr(c);
+      return false;
+    }
+    if (c.t == JT::BigInt) {
+      kind = 1;  // counts beyond int64 cannot be represented densely
+      msg = "count for " + py_str_repr(it.first) + " exceeds the dense range, got " + c.s;
+      return false;
+    }
+    if (c.i == 0) continue;
+    const std::string key = lower_ascii(it.first);
+    auto f = sh.vocab.find(key);
+    int32_t vid;
+    if (f == sh.vocab.end()) {
+      vid = static_cast<int32_t>(sh.names.size());
+      sh.vocab.emplace(key, vid);
+      sh.names.push_back(key);
+    } else {
+      vid = f->second;
+    }
+    auto w = where.find(vid);
+    if (w == where.end()) {
+      where.emplace(vid, ents.size());
+      ents.emplace_back(vid, c.i);
+    } else {
+      ents[w->second].second += c.i;
+    }
+  }
+  row.ents = std::move(ents);
+  return true;
+}
+
+}  // namespace
+
+struct gnb_corpus {
+  std::vector<std::string> vocab;
+  std::vector<std::string> ids;
+  std::vector<int64_t> size;
+  std::vector<int8_t> label;
+  std::vector<int64_t> row_ptr;
+  std::vector<int32_t> col;
+  std::vector<int64_t> val;
+  int64_t max_count = 0;
+  int err_kind = 0;
+  int64_t err_line = 0;
+  std::string err_msg;
+};
+
+extern "C" {
+
+int gnb_corpus_parse(const char* text, size_t len, int32_t allow_unlabeled, int32_t threads,
+                     gnb_corpus** out) {
+  if (!out || (!text && len)) return GNB_EINVAL;
+  auto* c = new gnb_corpus();
+  *out = c;
+  // line starts (1-based numbering like enumerate(..., start=1))
+  std::vector<size_t> starts;
+  starts.push_back(0);
+  for (size_t i = 0; i < len; ++i)
+    if (text[i] == '\n' && i + 1 < len) starts.push_back(i + 1);
+  if (len == 0) starts.clear();
+  const int64_t L = static_cast<int64_t>(starts.size());
+  int T = threads > 0 ? threads : static_cast<int>(std::thread::hardware_concurrency());
+  if (T < 1) T = 1;
+  if (T > 64) T = 64;
+  if (L < 4096) T = 1;
+  std::vector<Shard> shards(T);
+  auto work = [&](int t) {
+    Shard& sh = shards[t];
+    const int64_t lo = L * t / T, hi = L * (t + 1) / T;
+    for (int64_t ln = lo; ln < hi; ++ln) {
+      const char* a = text + starts[ln];
+      const char* b = text + (ln + 1 < L ? starts[ln + 1] : len);
+      while (b > a && (b[-1] == '\n' || b[-1] == '\r')) --b;
+      if (is_blank(a, b)) continue;
+      Row row;
+      int kind = 0;
+      std::string msg;
+      if (!parse_line(a, b, allow_unlabeled != 0, sh, row, kind, msg)) {
+        sh.err_line = ln + 1;
+        sh.err_kind = kind;
+        sh.err_msg = msg;
+        sh.err_has_id = !row.id.empty();
+        sh.err_id = row.id;
+        return;  // later lines of this shard cannot matter
+      }
+      sh.rows.push_back(std::move(row));
+      sh.line_no.push_back(ln + 1);
+    }
+  };
+  std::vector<std::thread> th;
+  for (int t = 1; t < T; ++t) th.emplace_back(work, t);
+  work(0);
+  for (auto& x : th) x.join();
+  // first error by line; duplicate ids before it win (the reference parses in order)
+  int64_t first_err = -1;
+  const Shard* err_sh = nullptr;
+  for (auto& sh : shards)
+    if (sh.err_line >= 0 && (first_err < 0 || sh.err_line < first_err)) {
+      first_err = sh.err_line;
+      err_sh = &sh;
+      c->err_kind = sh.err_kind;
+      c->err_msg = sh.err_msg;
+    }
+  {
+    std::unordered_set<std::string> seen;
+    for (auto& sh : shards)
+      for (size_t r = 0; r < sh.rows.size(); ++r) {
+        if (first_err >= 0 && sh.line_no[r] > first_err) break;
+        if (!seen.insert(sh.rows[r].id).second) {
+          c->err_kind = 2;
+          c->err_line = sh.line_no[r];
+          c->err_msg = "duplicate id " + py_str_repr(sh.rows[r].id) + " at line " +
+                       std::to_string(sh.line_no[r]);
+          return GNB_EINVAL;
+        }
+      }
+  }
+  if (first_err >= 0) {
+    c->err_line = first_err;
+    if (err_sh->err_has_id) {  // corpus.py:159-160 checks duplicates before the rest
+      std::unordered_set<std::string> seen;
+      for (auto& sh : shards)
+        for (size_t r = 0; r < sh.rows.size() && sh.line_no[r] < first_err; ++r)
+          seen.insert(sh.rows[r].id);
+      if (seen.count(err_sh->err_id)) {
+        c->err_kind = 2;
+        c->err_msg = "duplicate id " + py_str_repr(err_sh->err_id) + " at line " +
+                     std::to_string(first_err);
+      }
+    }
+    return GNB_EINVAL;
+  }
+  // global vocabulary: sorted union; remap shard-local ids
+  std::vector<std::string> all;
+  for (auto& sh : shards) all.insert(all.end(), sh.names.begin(), sh.names.end());
+  std::sort(all.begin(), all.end());
+  all.erase(std::unique(all.begin(), all.end()), all.end());
+  c->vocab = all;
+  std::unordered_map<std::string, int32_t> gid;
+  gid.reserve(all.size() * 2);
+  for (size_t k = 0; k < all.size(); ++k) gid.emplace(all[k], static_cast<int32_t>(k));
+  int64_t n = 0, nnz = 0;
+  for (auto& sh : shards) {
+    n += static_cast<int64_t>(sh.rows.size());
+    for (auto& r : sh.rows) nnz += static_cast<int64_t>(r.ents.size());
+  }
+  c->ids.reserve(n);
+  c->size.reserve(n);
+  c->label.reserve(n);
+  c->row_ptr.reserve(n + 1);
+  c->col.reserve(nnz);
+  c->val.reserve(nnz);
+  c->row_ptr.push_back(0);
+  for (auto& sh : shards) {
+    std::vector<int32_t> map(sh.names.size());
+    for (size_t k = 0; k < sh.names.size(); ++k) map[k] = gid[sh.names[k]];
+    for (auto& r : sh.rows) {
+      c->ids.push_back(std::move(r.id));
+      c->size.push_back(r.size);
+      c->label.push_back(r.label);
+      for (auto& e : r.ents) {
+        c->col.push_back(map[e.first]);
+        c->val.push_back(e.second);
+        c->max_count = std::max(c->max_count, e.second);
+      }
+      c->row_ptr.push_back(static_cast<int64_t>(c->col.size()));
+    }
+  }
+  return GNB_OK;
+}
+
+void gnb_corpus_free(gnb_corpus* c) { delete c; }
+
+int64_t gnb_corpus_rows(const gnb_corpus* c) { return c ? static_cast<int64_t>(c->ids.size()) : 0; }
+int32_t gnb_corpus_vocab_size(const gnb_corpus* c) {
+  return c ? static_cast<int32_t>(c->vocab.size()) : 0;
+}
+const char* gnb_corpus_vocab(const gnb_corpus* c, int32_t k) { return c->vocab[k].c_str(); }
+const char* gnb_corpus_id(const gnb_corpus* c, int64_t r) { return c->ids[r].c_str(); }
+int64_t gnb_corpus_max_count(const gnb_corpus* c) { return c->max_count; }
+int64_t gnb_corpus_nnz(const gnb_corpus* c) { return static_cast<int64_t>(c->col.size()); }
+int32_t gnb_corpus_error(const gnb_corpus* c, int64_t* line, const char** message) {
+  if (line) *line = c->err_line;
+  if (message) *message = c->err_msg.c_str();
+  return c->err_kind;
+}
+
+// sizes (int64, -1 = beyond int64) and labels (1 malware, 0 benign, -1 none)
+int gnb_corpus_meta(const gnb_corpus* c, int64_t* size_out, int8_t* label_out) {
+  if (!c) return GNB_EINVAL;
+  if (size_out) std::copy(c->size.begin(), c->size.end(), size_out);
+  if (label_out) std::copy(c->label.begin(), c->label.end(), label_out);
+  return GNB_OK;
+}
+
+// Dense rows [row0, row0 + n) into x (x_type storage, row pitch ldx elements,
+// ldx >= vocab size); zero-filled first.  GNB_EINVAL if a count does not fit.
+int gnb_corpus_dense(const gnb_corpus* c, int32_t x_type, void* x, int64_t ldx, int64_t row0,
+                     int64_t n, int32_t threads) {
+  if (!c || !x || row0 < 0 || n < 0 || row0 + n > static_cast<int64_t>(c->ids.size()) ||
+      ldx < static_cast<int64_t>(c->vocab.size()))
+    return GNB_EINVAL;
+  const int64_t lim = x_type == GNB_X_U8 ? 255 : x_type == GNB_X_U16 ? 65535 : 2147483647;
+  if (c->max_count > lim) return GNB_EINVAL;
+  const int eb = x_type == GNB_X_U8 ? 1 : x_type == GNB_X_U16 ? 2 : 4;
+  int T = threads > 0 ? threads : static_cast<int>(std::thread::hardware_concurrency());
+  T = std::max(1, std::min<int>(T, 64));
+  if (n < 65536) T = 1;
+  auto work = [&](int t) {
+    const int64_t lo = row0 + n * t / T, hi = row0 + n * (t + 1) / T;
+    uint8_t* base = static_cast<uint8_t*>(x);
+    memset(base + (lo - row0) * ldx * eb, 0, static_cast<size_t>((hi - lo) * ldx * eb));
+    for (int64_t r = lo; r < hi; ++r) {
+      uint8_t* row = base + (r - row0) * ldx * eb;
+      for (int64_t k = c->row_ptr[r]; k < c->row_ptr[r + 1]; ++k) {
+        const int64_t v = c->val[k];
+        const int32_t j = c->col[k];
+        if (eb == 1) row[j] = static_cast<uint8_t>(v);
+        else if (eb == 2) reinterpret_cast<uint16_t*>(row)[j] = static_cast<uint16_t>(v);
+        else reinterpret_cast<int32_t*>(row)[j] = static_cast<int32_t>(v);
+      }
+    }
+  };
+  std::vector<std::thread> th;
+  for (int t = 1; t < T; ++t) th.emplace_back(work, t);
+  work(0);
+  for (auto& t : th) t.join();
+  return GNB_OK;
+}
+
+}  // extern "C"

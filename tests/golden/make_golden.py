@@ -174,3 +174,63 @@ if __name__ == "__main__":
     case_groups()
     case_small_vocab()
     case_ties()
+
+
+def case_ingest():
+    """parse_corpus (corpus.py:133-189) on valid JSONL and on malformed lines."""
+    import json as _json
+    from groupnb import GroupNBError, parse_corpus, serialize_sample
+    corpus = generate_synthetic(SyntheticSpec(3, 7, 12, 0.4, 9))
+    lines = [serialize_sample(s) for s in corpus]
+    # extra valid variety: unknown keys, mixed-case + merged mnemonics, zeros, blank lines
+    lines.insert(3, _json.dumps({"id": "mix", "label": "malware", "size_bytes": 77,
+                                 "opcodes": {"MOV": 2, "mov": 3, "Add": 0, "xor": 1},
+                                 "extra": [1, 2]}))
+    lines.insert(5, "")
+    lines.insert(6, "   ")
+    lines.append(_json.dumps({"id": "u1", "size_bytes": 5, "opcodes": {}}))
+    text_ok = "\n".join(lines) + "\n"
+    recs = parse_corpus(text_ok, allow_unlabeled=True)
+    vocab = sorted({op for r in recs for op in r.histogram.entries})
+    x, size, label = _dense(recs, vocab)
+    bad_lines = [
+        '{"id": "a", "label": "malware", "size_bytes": 1, "opcodes": {}}\n{"id": "a", "label": "benign", "size_bytes": 2, "opcodes": {}}',
+        '{"id": "a", "label": "malware", "size_bytes": 1, "opcodes": {}}\n{"id": "a", "label": "bogus", "size_bytes": 2, "opcodes": {}}',
+        '{"id": "a", "label": "malware", "size_bytes": 1, "opcodes": {}}\n[1, 2]',
+        '{"id": "", "label": "malware", "size_bytes": 1, "opcodes": {}}',
+        '{"label": "malware", "size_bytes": 1, "opcodes": {}}',
+        '{"id": "b", "label": "spam", "size_bytes": 1, "opcodes": {}}',
+        '{"id": "b", "label": 7, "size_bytes": 1, "opcodes": {}}',
+        '{"id": "b", "size_bytes": 1, "opcodes": {}}',
+        '{"id": "b", "label": "benign", "size_bytes": -1, "opcodes": {}}',
+        '{"id": "b", "label": "benign", "size_bytes": 1.5, "opcodes": {}}',
+        '{"id": "b", "label": "benign", "size_bytes": true, "opcodes": {}}',
+        '{"id": "b", "label": "benign", "size_bytes": 3, "opcodes": [1]}',
+        '{"id": "b", "label": "benign", "size_bytes": 3, "opcodes": {"": 1}}',
+        '{"id": "b", "label": "benign", "size_bytes": 3, "opcodes": {"mov": -2}}',
+        '{"id": "b", "label": "benign", "size_bytes": 3, "opcodes": {"mov": 2.0}}',
+        '{"id": "b", "label": "benign", "size_bytes": 3, "opcodes": {"mov": "2"}}',
+        '{"id": "b", "label": "benign", "size_bytes": 3, "opcodes": {"mov": false}}',
+        '{"id": "b", "label": "benign", "size_bytes": 3, "opcodes": {"mov": 1}} trailing',
+        '{"id": "b" "label": "benign"}',
+    ]
+    kinds, lines_no, msgs = [], [], []
+    for t in bad_lines:
+        try:
+            parse_corpus(t)
+            raise AssertionError("expected an error: " + t)
+        except GroupNBError as exc:
+            kinds.append(type(exc).__name__)
+            lines_no.append(getattr(exc, "line_no", -1))
+            msgs.append(str(exc))
+    np.savez_compressed(
+        os.path.join(OUT, "ingest.npz"),
+        text_ok=np.array(text_ok), vocab=np.array(vocab, dtype=np.str_), x=x, size=size,
+        label=label, ids=np.array([r.id for r in recs], dtype=np.str_),
+        bad=np.array(bad_lines, dtype=np.str_), bad_kind=np.array(kinds, dtype=np.str_),
+        bad_line=np.array(lines_no), bad_msg=np.array(msgs, dtype=np.str_))
+    print(f"ingest: rows={len(recs)} V={len(vocab)} error cases={len(bad_lines)}")
+
+
+if __name__ == "__main__":
+    case_ingest()

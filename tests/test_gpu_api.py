@@ -91,3 +91,48 @@ def test_errors_match_reference_contract():
         gnb.train_group(only_m, gnb.FeatureSet((), 1), 1.0)
     with pytest.raises(gnb.InvalidConfigError):
         gnb.Workload((), lanes=0)
+
+
+def _jsonl(z, which):
+    vocab = z["vocab"].tolist()
+    x = z[f"{which}_x"]
+    size = z[f"{which}_size"]
+    labels = z["train_label"] if which == "train" else np.full(len(size), -1)
+    out = []
+    for i in range(len(size)):
+        d = {"id": f"{which}{i}", "size_bytes": int(size[i]),
+             "opcodes": {vocab[j]: int(x[i, j]) for j in np.nonzero(x[i])[0]}}
+        if labels[i] >= 0:
+            d["label"] = "malware" if labels[i] == 1 else "benign"
+        if int(size[i]) >= 0:
+            out.append(json.dumps(d))
+        else:   # negative sizes are not valid JSONL records; keep them as oversize rows
+            d["size_bytes"] = 10**9
+            out.append(json.dumps(d))
+    return "\n".join(out)
+
+
+def test_dense_corpus_pipeline_matches_reference(golden):
+    """JSONL -> C++ ingest -> device fit / gather / predict == reference outputs."""
+    from paper_1905_13746_b200 import ingest
+    from paper_1905_13746_b200.api import classify_corpus, train_bundle_corpus
+    name, z = golden
+    cfg = _config(z)
+    train = ingest.read_corpus(_jsonl(z, "train"))
+    bundle = train_bundle_corpus(train, cfg, int(z["k"]), float(z["alpha"]), created_at="g")
+    doc = json.loads(str(z["bundle_json"]))
+    assert list(bundle.trained_ids) == [m["group"] for m in doc["models"]]
+    for m in doc["models"]:
+        got = bundle.models[m["group"]]
+        assert list(got.features.opcodes) == m["features"]
+        for c in (Label.MALWARE, Label.BENIGN):
+            assert [got.log_likelihood[c][op] for op in m["features"]] == \
+                [m["log_likelihood"][c.value][op] for op in m["features"]]
+    test = ingest.read_corpus(_jsonl(z, "test"), allow_unlabeled=True)
+    lab, lp, eff, errors, elapsed = classify_corpus(bundle, test)
+    want = z["pred_label"].astype(int)
+    assert lab.tolist() == want.tolist()
+    ok = want >= 0
+    assert lp[ok].tobytes() == z["pred_lp"][ok].tobytes()
+    assert eff[ok].tolist() == z["pred_group"][ok].tolist()
+    assert [i for i, _ in errors] == np.nonzero(~ok)[0].tolist()
