@@ -231,6 +231,15 @@ int gnb_corpus_meta(const gnb_corpus* c, int64_t* size_out, int8_t* label_out);
 int gnb_corpus_dense(const gnb_corpus* c, int32_t x_type, void* x, int64_t ldx, int64_t row0,
                      int64_t n, int32_t threads);
 
+/* engine.write_predictions (pkg/src/groupnb/engine.py:466-481) for a parsed
+ * corpus: byte-identical JSONL (17 significant digits).  label: 1 malware,
+ * 0 benign, < 0 size error; logpost[n][2] = (benign, malware).  The text is
+ * malloc'ed; release it with gnb_free_text. */
+int gnb_corpus_write_predictions(const gnb_corpus* c, const int8_t* label, const double* logpost,
+                                 const int32_t* effective_group, int64_t max_size_bytes,
+                                 int32_t threads, char** out_text, size_t* out_len);
+void gnb_free_text(char* p);
+
 /* ------------------------------------------------------------------ synthetic data
  * Device generator following the reference's synthetic law
  * (pkg/src/groupnb/synth.py:64-116): per row a group (rows laid out group by

@@ -672,3 +672,123 @@ int gnb_corpus_dense(const gnb_corpus* c, int32_t x_type, void* x, int64_t ldx, 
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------- prediction writer
+namespace {
+
+// json.dumps(str) with the default ensure_ascii=True
+void json_str(std::string& o, const std::string& s) {
+  o += '"';
+  size_t i = 0;
+  while (i < s.size()) {
+    const unsigned char c = static_cast<unsigned char>(s[i]);
+    if (c < 0x80) {
+      ++i;
+      switch (c) {
+        case '"': o += "\\\""; break;
+        case '\\': o += "\\\\"; break;
+        case '\n': o += "\\n"; break;
+        case '\r': o += "\\r"; break;
+        case '\t': o += "\\t"; break;
+        case '\b': o += "\\b"; break;
+        case '\f': o += "\\f"; break;
+        default:
+          if (c < 0x20) {
+            char b[8];
+            snprintf(b, sizeof b, "\\u%04x", c);
+            o += b;
+          } else {
+            o += static_cast<char>(c);
+          }
+      }
+      continue;
+    }
+    // UTF-8 -> code point -> \uXXXX (surrogate pairs above U+FFFF)
+    uint32_t cp = 0;
+    int extra = c >= 0xF0 ? 3 : c >= 0xE0 ? 2 : 1;
+    cp = c & (0x3F >> extra);
+    ++i;
+    for (int k = 0; k < extra && i < s.size(); ++k, ++i)
+      cp = (cp << 6) | (static_cast<unsigned char>(s[i]) & 0x3F);
+    char b[16];
+    if (cp >= 0x10000) {
+      cp -= 0x10000;
+      snprintf(b, sizeof b, "\\u%04x\\u%04x", 0xD800 + (cp >> 10), 0xDC00 + (cp & 0x3FF));
+    } else {
+      snprintf(b, sizeof b, "\\u%04x", cp);
+    }
+    o += b;
+  }
+  o += '"';
+}
+
+void fmt17(std::string& o, double v) {  // format(v, ".17g")
+  char b[40];
+  snprintf(b, sizeof b, "%.17g", v);
+  o += b;
+}
+
+}  // namespace
+
+extern "C" {
+
+// engine.write_predictions (pkg/src/groupnb/engine.py:466-481) for a parsed
+// corpus: one JSONL object per row, 17-significant-digit floats, byte-identical
+// to the reference's output.  label: 1 malware, 0 benign, < 0 size error;
+// logpost [n][2] = (benign, malware).  *out_text is malloc'ed: gnb_free_text.
+int gnb_corpus_write_predictions(const gnb_corpus* c, const int8_t* label, const double* logpost,
+                                 const int32_t* effective_group, int64_t max_size_bytes,
+                                 int32_t threads, char** out_text, size_t* out_len) {
+  if (!c || !label || !logpost || !effective_group || !out_text || !out_len) return GNB_EINVAL;
+  const int64_t n = static_cast<int64_t>(c->ids.size());
+  int T = threads > 0 ? threads : static_cast<int>(std::thread::hardware_concurrency());
+  T = std::max(1, std::min<int>(T, 64));
+  if (n < 16384) T = 1;
+  std::vector<std::string> part(T);
+  auto work = [&](int t) {
+    std::string& o = part[t];
+    const int64_t lo = n * t / T, hi = n * (t + 1) / T;
+    o.reserve(static_cast<size_t>(hi - lo) * 120);
+    for (int64_t r = lo; r < hi; ++r) {
+      o += "{\"id\": ";
+      json_str(o, c->ids[r]);
+      if (label[r] < 0) {
+        o += ", \"error\": ";
+        json_str(o, "size_bytes " + (c->size[r] >= 0 ? std::to_string(c->size[r])
+                                                      : std::string("(huge)")) +
+                        " outside [0, " + std::to_string(max_size_bytes) + ")");
+        o += "}\n";
+        continue;
+      }
+      o += label[r] == 1 ? ", \"label\": \"malware\"" : ", \"label\": \"benign\"";
+      o += ", \"log_posterior\": {\"malware\": ";
+      fmt17(o, logpost[2 * r + 1]);
+      o += ", \"benign\": ";
+      fmt17(o, logpost[2 * r]);
+      o += "}, \"effective_group\": ";
+      o += std::to_string(effective_group[r]);
+      o += "}\n";
+    }
+  };
+  std::vector<std::thread> th;
+  for (int t = 1; t < T; ++t) th.emplace_back(work, t);
+  work(0);
+  for (auto& x : th) x.join();
+  size_t total = 0;
+  for (auto& p : part) total += p.size();
+  char* buf = static_cast<char*>(malloc(total + 1));
+  if (!buf) return GNB_ENOMEM;
+  size_t off = 0;
+  for (auto& p : part) {
+    memcpy(buf + off, p.data(), p.size());
+    off += p.size();
+  }
+  buf[total] = '\0';
+  *out_text = buf;
+  *out_len = total;
+  return GNB_OK;
+}
+
+void gnb_free_text(char* p) { free(p); }
+
+}  // extern "C"

@@ -40,6 +40,12 @@ _L.gnb_corpus_meta.restype = C.c_int
 _L.gnb_corpus_dense.argtypes = [_p, _i32, _p, _i64, _i64, _i64, _i32]
 _L.gnb_corpus_dense.restype = C.c_int
 
+_L.gnb_corpus_write_predictions.argtypes = [_p, _p, _p, _p, _i64, _i32,
+                                            C.POINTER(C.c_void_p), C.POINTER(_sz)]
+_L.gnb_corpus_write_predictions.restype = C.c_int
+_L.gnb_free_text.argtypes = [_p]
+_L.gnb_free_text.restype = None
+
 _DTYPES = {np.dtype(np.int32): N.X_I32, np.dtype(np.uint16): N.X_U16, np.dtype(np.uint8): N.X_U8}
 
 
@@ -92,6 +98,26 @@ class DenseCorpus:
                                threads) != N.GNB_OK:
             raise InvalidConfigError(f"counts up to {self.max_count} do not fit {dtype}")
         return out
+
+    def predictions_jsonl(self, label, logpost, effective_group, max_size_bytes: int,
+                          threads: int = 0) -> str:
+        """engine.write_predictions (engine.py:466-481) text for this corpus:
+        label 1/0/<0 (error), logpost [N, 2] (benign, malware)."""
+        lab = np.ascontiguousarray(label, dtype=np.int8)
+        lp = np.ascontiguousarray(logpost, dtype=np.float64)
+        eff = np.ascontiguousarray(effective_group, dtype=np.int32)
+        if lab.shape != (len(self),) or lp.shape != (len(self), 2) or eff.shape != lab.shape:
+            raise InvalidConfigError("need label [N], logpost [N, 2], effective_group [N]")
+        buf, n = C.c_void_p(), _sz()
+        rc = _L.gnb_corpus_write_predictions(self._h, lab.ctypes.data, lp.ctypes.data,
+                                             eff.ctypes.data, max_size_bytes, threads,
+                                             C.byref(buf), C.byref(n))
+        if rc != N.GNB_OK:
+            raise InvalidConfigError("gnb_corpus_write_predictions failed")
+        try:
+            return C.string_at(buf.value, n.value).decode()
+        finally:
+            _L.gnb_free_text(buf)
 
     def records(self) -> list[SampleRecord]:
         """The reference's object model (slow path, for object-API callers)."""

@@ -232,5 +232,42 @@ def case_ingest():
     print(f"ingest: rows={len(recs)} V={len(vocab)} error cases={len(bad_lines)}")
 
 
+def case_writer():
+    """write_predictions (engine.py:466-481) text, incl. error rows and non-ASCII ids."""
+    import io
+    from groupnb import parse_corpus, serialize_sample, write_predictions
+    config = GroupingConfig()
+    corpus = generate_synthetic(SyntheticSpec(3, 8, 16, 0.3, 21))
+    train, _ = partition_by_group(corpus, config)
+    bundle = train_bundle(train, k=10, alpha=1.0, created_at="golden")
+    rng = np.random.default_rng(5)
+    test = [corpus[i] for i in rng.permutation(len(corpus))[:30]]
+    odd = ["caf\u00e9-\u00fc", 'q"uote\\back', "tab\tnl", "emoji-\U0001F600"]
+    for j, sid in enumerate(odd):
+        s = test[j]
+        test[j] = SampleRecord(sid, Label.UNKNOWN, s.size_bytes, s.histogram)
+    test.insert(7, _sample("big", Label.UNKNOWN, 600000, {"op01": 1}))
+    text_in = "\n".join(serialize_sample(s) for s in test) + "\n"
+    samples = parse_corpus(text_in, allow_unlabeled=True)
+    run = classify_sequential(bundle, Workload(tuple(samples), lanes=1), warmup=False)
+    sink = io.StringIO()
+    write_predictions(run, samples, sink)
+    m = len(samples)
+    lab = np.full(m, -1, np.int8)
+    lp = np.full((m, 2), np.nan)
+    eff = np.full(m, -1, np.int32)
+    for i, p in enumerate(run.predictions):
+        if p is not None:
+            lab[i] = _LABEL_CODE[p.label]
+            lp[i] = [p.log_posterior[Label.BENIGN], p.log_posterior[Label.MALWARE]]
+            eff[i] = p.effective_group
+    train_text = "\n".join(serialize_sample(s) for s in train.all_samples()) + "\n"
+    np.savez_compressed(os.path.join(OUT, "writer.npz"), text_in=np.array(text_in),
+                        train_text=np.array(train_text), label=lab, lp=lp, eff=eff,
+                        out=np.array(sink.getvalue()), k=10)
+    print(f"writer: rows={m} bytes={len(sink.getvalue())}")
+
+
 if __name__ == "__main__":
     case_ingest()
+    case_writer()

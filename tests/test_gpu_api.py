@@ -136,3 +136,18 @@ def test_dense_corpus_pipeline_matches_reference(golden):
     assert lp[ok].tobytes() == z["pred_lp"][ok].tobytes()
     assert eff[ok].tolist() == z["pred_group"][ok].tolist()
     assert [i for i, _ in errors] == np.nonzero(~ok)[0].tolist()
+
+
+def test_jsonl_to_jsonl_matches_reference_bytes():
+    """JSONL in -> device fit + classify -> JSONL out, byte-identical to the reference's
+    train_bundle / classify_sequential / write_predictions (tests/golden/writer.npz)."""
+    from conftest import load_golden
+    from paper_1905_13746_b200 import ingest
+    from paper_1905_13746_b200.api import classify_corpus, train_bundle_corpus
+    w = load_golden("writer")
+    cfg = gnb.GroupingConfig()
+    bundle = train_bundle_corpus(ingest.read_corpus(str(w["train_text"])), cfg, int(w["k"]),
+                                 1.0, created_at="golden")
+    test = ingest.read_corpus(str(w["text_in"]), allow_unlabeled=True)
+    lab, lp, eff, errors, _ = classify_corpus(bundle, test)
+    assert test.predictions_jsonl(lab, lp, eff, cfg.max_size_bytes) == str(w["out"])

@@ -69,3 +69,11 @@ def test_large_parallel_parse_matches_single_thread():
     with pytest.raises(IntegrityError) as ei:
         ingest.read_corpus("\n".join(lines), threads=8)
     assert "at line 12346" in str(ei.value)
+
+
+def test_prediction_writer_byte_identical():
+    """gnb_corpus_write_predictions == the reference's write_predictions text."""
+    w = load_golden("writer")
+    c = ingest.read_corpus(str(w["text_in"]), allow_unlabeled=True)
+    text = c.predictions_jsonl(w["label"], np.nan_to_num(w["lp"]), w["eff"], 512000)
+    assert text == str(w["out"])
