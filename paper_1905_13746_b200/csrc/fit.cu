@@ -462,6 +462,14 @@ template <typename T>
 static cudaError_t launch_fit_typed(const CUtensorMap& map, const FitParams& p,
                                    cudaStream_t stream) {
   // keys are dealt to warps round-robin: no more warps than keys
+  static int nw8 = -1;  // GNB_FIT_NW8=0 disables the 8-consumer-warp CTA (profiling)
+  if (nw8 < 0) {
+    const char* e = getenv("GNB_FIT_NW8");
+    nw8 = e ? atoi(e) : 1;
+  }
+  // 8 consumer warps pay off for int32 rows (32-KB stages, consumer-bound); for
+  // uint8/uint16 tiles the producer's sort is the limit (profiles/r01_tuning.md)
+  if (sizeof(T) == 4 && p.n_keys >= 8 && nw8) return launch_fit_nw<T, 8>(map, p, stream);
   if (p.n_keys >= 4) return launch_fit_nw<T, 4>(map, p, stream);
   if (p.n_keys >= 2) return launch_fit_nw<T, 2>(map, p, stream);
   return launch_fit_nw<T, 1>(map, p, stream);
