@@ -316,7 +316,7 @@ static int fit_stats_device(const void* x, int x_type, int64_t n_rows, int32_t n
     const int64_t n = std::min(kMaxRowsPerLaunch, n_rows - r0);
     CUtensorMap map;
     const void* xr = static_cast<const uint8_t*>(x) + r0 * ldx * eb;
-    if (!encode_map(&map, xr, n, n_cols, ldx, fit_box_rows(), false, x_type))
+    if (!encode_map(&map, xr, n, n_cols, ldx, fit_box_rows(x_type), false, x_type))
       return fail(GNB_ECUDA, "fit_stats: cuTensorMapEncodeTiled failed");
     FitParams p{};
     p.x_type = x_type;

@@ -35,8 +35,6 @@
 
 namespace gnb {
 
-constexpr int kFitRows = 128;        // rows per tile (u8 permutation, 4 keys per lane)
-constexpr int kKeysPerLane = kFitRows / 32;
 constexpr int kMaxHistKeys = 4096;   // keys sorted by the shared-memory histogram
 
 // Stage geometry per X storage: a lane owns CPL consecutive columns.
@@ -45,6 +43,9 @@ constexpr int kMaxHistKeys = 4096;   // keys sorted by the shared-memory histogr
 //   uint8 : 1 box  x 128 columns = 128 columns, CPL 4 (LDS.32)
 template <typename T>
 struct FitGeom {
+  // rows per tile (u8 permutation).  256-row tiles for narrow rows were
+  // measured slower (fewer CTAs per SM), profiles/r01_tuning.md.
+  static constexpr int kRows = 128;
   static constexpr int kBoxCols = kChunkBytesPerRow / static_cast<int>(sizeof(T));
   static constexpr int kBoxes = sizeof(T) == 4 ? 2 : 1;
   static constexpr int kGroupCols = kBoxCols * kBoxes;
@@ -52,21 +53,23 @@ struct FitGeom {
   static constexpr int kLaneBytes = kCPL * static_cast<int>(sizeof(T));
 };
 
+template <int ROWS>
 struct FitHdr {
   int n_runs;
   int pad[3];
-  uint8_t perm[kFitRows];
-  int2 runs[kFitRows];  // {key, start | len << 16}
+  uint8_t perm[ROWS];
+  int2 runs[ROWS];  // {key, start | len << 16}
 };
 
 template <typename T, int NW, int STAGES>
 struct FitSmem {
-  static constexpr int kBox = kFitRows * kChunkBytesPerRow;  // 16 KB
+  using Hdr = FitHdr<FitGeom<T>::kRows>;
+  static constexpr int kBox = FitGeom<T>::kRows * kChunkBytesPerRow;  // 16 / 32 KB
   static constexpr int kStage = FitGeom<T>::kBoxes * kBox;    // 32 / 16 KB
   static constexpr int kX = 0;
   static constexpr int kHdr = kX + STAGES * kStage;
-  static constexpr int kScratch = kHdr + STAGES * static_cast<int>(sizeof(FitHdr));
-  static constexpr int kBar = kScratch + static_cast<int>(sizeof(FitHdr));
+  static constexpr int kScratch = kHdr + STAGES * static_cast<int>(sizeof(Hdr));
+  static constexpr int kBar = kScratch + static_cast<int>(sizeof(Hdr));
   static constexpr int kPart = (kBar + 2 * STAGES * 8 + 15) / 16 * 16;
   static constexpr int kFixed = kPart + 1024;  // + alignment slack
 };
@@ -104,8 +107,11 @@ __global__ void __launch_bounds__((NW + 1) * 32)
     fit_tma_kernel(const __grid_constant__ CUtensorMap xmap, const FitParams p) {
   using L = FitSmem<T, NW, STAGES>;
   using Geo = FitGeom<T>;
+  using FitHdrT = typename L::Hdr;
   constexpr int kGroupCols = Geo::kGroupCols;
   constexpr int CPL = Geo::kCPL;
+  constexpr int kFitRows = Geo::kRows;
+  constexpr int kKeysPerLane = kFitRows / 32;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::kBar);
@@ -138,7 +144,7 @@ __global__ void __launch_bounds__((NW + 1) * 32)
   if (warp == NW) {
     // ------------------------------------------------------------ producer
     const uint64_t pol_x = policy_evict_normal();
-    FitHdr* scratch = reinterpret_cast<FitHdr*>(smem + L::kScratch);
+    FitHdrT* scratch = reinterpret_cast<FitHdrT*>(smem + L::kScratch);
     int stage = 0;
     uint32_t phase = 0;
     unsigned long long bad_label = 0, out_of_range = 0;
@@ -270,7 +276,7 @@ __global__ void __launch_bounds__((NW + 1) * 32)
       const int hdr_words = (16 + kFitRows + n_runs * 8 + 15) / 16;  // 16-B units
       for (int cg = 0; cg < NG; ++cg) {
         mbar_wait(&empty[stage], phase ^ 1);
-        FitHdr* hdr = reinterpret_cast<FitHdr*>(smem + L::kHdr + stage * sizeof(FitHdr));
+        FitHdrT* hdr = reinterpret_cast<FitHdrT*>(smem + L::kHdr + stage * sizeof(FitHdrT));
         const int4* src4 = reinterpret_cast<const int4*>(scratch);
         int4* dst4 = reinterpret_cast<int4*>(hdr);
         for (int i = lane; i < hdr_words; i += 32) dst4[i] = src4[i];
@@ -313,8 +319,8 @@ __global__ void __launch_bounds__((NW + 1) * 32)
     for (int64_t tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
       for (int cg = 0; cg < NG; ++cg) {
         mbar_wait(&full[stage], phase);
-        const FitHdr* hdr =
-            reinterpret_cast<const FitHdr*>(smem + L::kHdr + stage * sizeof(FitHdr));
+        const FitHdrT* hdr =
+            reinterpret_cast<const FitHdrT*>(smem + L::kHdr + stage * sizeof(FitHdrT));
         const uint8_t* xs = smem + L::kX + stage * L::kStage + lane_off;
         const int col0 = cg * kGroupCols + CPL * lane;
         const int n_runs = hdr->n_runs;
@@ -433,7 +439,9 @@ static cudaError_t launch_fit(const CUtensorMap& map, FitParams p, cudaStream_t 
   return cudaGetLastError();
 }
 
-int fit_box_rows() { return kFitRows; }
+int fit_box_rows(int x_type) {
+  return x_type == GNB_X_I32 ? FitGeom<int32_t>::kRows : FitGeom<uint8_t>::kRows;
+}
 
 // GNB_FIT_VARIANT (profiling only): 0 = 2 stages x 2 CTAs/SM (default; measured
 // best on B200, profiles/r01_tuning.md), 1 = 4 stages x 1 CTA/SM,
@@ -448,13 +456,24 @@ static int fit_variant() {
   return v;
 }
 
+// CTAs per SM the partial-sum budget is sized for, narrow rows (GNB_FIT_CTAS).
+static int narrow_ctas() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("GNB_FIT_CTAS");
+    v = e ? atoi(e) : 2;
+    if (v < 1 || v > 8) v = 2;
+  }
+  return v;
+}
+
 template <typename T, int NW>
 static cudaError_t launch_fit_nw(const CUtensorMap& map, const FitParams& p, cudaStream_t stream) {
   switch (fit_variant()) {
     case 1: return launch_fit<T, NW, 4>(map, p, stream, 1);
     case 2: return launch_fit<T, NW, 5>(map, p, stream, 1);
     case 3: return launch_fit<T, NW, 3>(map, p, stream, 1);
-    default: return launch_fit<T, NW, 2>(map, p, stream, 2);
+    default: return launch_fit<T, NW, 2>(map, p, stream, sizeof(T) == 4 ? 2 : narrow_ctas());
   }
 }
 
@@ -476,7 +495,7 @@ static cudaError_t launch_fit_typed(const CUtensorMap& map, const FitParams& p,
 }
 
 cudaError_t fit_launch(const CUtensorMap& map, FitParams p, cudaStream_t stream) {
-  p.n_tiles = (p.n_rows + kFitRows - 1) / kFitRows;
+  p.n_tiles = (p.n_rows + fit_box_rows(p.x_type) - 1) / fit_box_rows(p.x_type);
   switch (p.x_type) {
     case GNB_X_U16: return launch_fit_typed<uint16_t>(map, p, stream);
     case GNB_X_U8: return launch_fit_typed<uint8_t>(map, p, stream);

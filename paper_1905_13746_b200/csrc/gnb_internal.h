@@ -60,7 +60,7 @@ cudaError_t pack_tables(const double* log_prior, const double* log_lik, int S, i
 int predict_box_rows(int n_classes);  // TMA box height of the K-PRED variant
 cudaError_t predict_launch(const CUtensorMap* map, PredictParams p, cudaStream_t stream,
                            int force_generic);
-int fit_box_rows();  // TMA box height of K-FIT tiles
+int fit_box_rows(int x_type);  // TMA box height of K-FIT tiles
 cudaError_t fit_launch(const CUtensorMap& map, FitParams p, cudaStream_t stream);
 
 struct GenParams {
