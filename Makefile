@@ -6,7 +6,14 @@ PKG := paper_1905_13746_b200
 SRC := $(PKG)/csrc/predict.cu $(PKG)/csrc/fit.cu $(PKG)/csrc/gen.cu $(PKG)/csrc/gather.cu $(PKG)/csrc/sort.cu $(PKG)/csrc/api.cu $(PKG)/csrc/fin.cpp $(PKG)/csrc/ingest.cpp
 HDR := $(wildcard $(PKG)/csrc/*.h $(PKG)/csrc/*.cuh) include/gnb.h
 
-all: $(PKG)/libgnb.so oracle
+PYINC := $(shell python3 -c "import sysconfig; print(sysconfig.get_paths()['include'])")
+PYEXT := $(shell python3 -c "import sysconfig; print(sysconfig.get_config_var('EXT_SUFFIX'))")
+ADAPT := $(PKG)/_adapt$(PYEXT)
+
+all: $(PKG)/libgnb.so $(ADAPT) oracle
+
+$(ADAPT): $(PKG)/csrc/adapt.cpp
+	g++ -O3 -std=c++17 -fPIC -shared -I$(PYINC) -o $@ $<
 
 $(PKG)/libgnb.so: $(SRC) $(HDR)
 	$(NVCC) $(NVFLAGS) -shared -o $@ $(SRC)
@@ -15,7 +22,7 @@ oracle:
 	$(MAKE) -C oracle
 
 clean:
-	rm -f $(PKG)/libgnb.so
+	rm -f $(PKG)/libgnb.so $(ADAPT)
 	$(MAKE) -C oracle clean
 
 .PHONY: all oracle clean

@@ -24,6 +24,7 @@ from typing import Sequence
 
 import numpy as np
 
+from . import _adapt
 from . import _native as N
 from .errors import (EmptyBundleError, InsufficientClassError, IntegrityError,
                      InvalidConfigError, MeasurementError)
@@ -47,34 +48,20 @@ def _device_ordinal(device) -> int:
     return 0 if idx is None else int(idx)
 
 
-def _label_codes(samples: Sequence[SampleRecord]) -> np.ndarray:
-    return np.fromiter((CLASS_INDEX.get(s.label, -1) for s in samples), dtype=np.int32,
-                       count=len(samples))
+def _meta(samples: Sequence[SampleRecord], limit: int):
+    """int32 sizes (outside [0, limit) -> -1, still an error row) and class codes
+    (benign 0, malware 1, unlabeled -1), via the C-API packer."""
+    size = np.empty(len(samples), dtype=np.int32)
+    label = np.empty(len(samples), dtype=np.int32)
+    _adapt.meta_into(samples, limit, Label.MALWARE, Label.BENIGN, size, label)
+    return size, label
 
 
 def _densify(samples: Sequence[SampleRecord], columns: dict[str, int], width: int) -> np.ndarray:
     """[N, width] int32 counts of the opcodes in `columns` (others ignored)."""
     x = np.zeros((len(samples), width), dtype=np.int32)
-    rows, cols, vals = [], [], []
-    for i, s in enumerate(samples):
-        for op, n in s.histogram.entries.items():
-            j = columns.get(op)
-            if j is not None:
-                rows.append(i)
-                cols.append(j)
-                vals.append(n)
-    if vals:
-        v = np.asarray(vals, dtype=np.int64)
-        if int(v.max()) > _I32_MAX:
-            raise InvalidConfigError("opcode counts must be < 2^31 for the GPU path")
-        x[np.asarray(rows), np.asarray(cols)] = v
+    _adapt.densify_into(samples, columns, x, width)
     return x
-
-
-def _sizes(samples: Sequence[SampleRecord], limit: int) -> np.ndarray:
-    """int32 sizes; anything outside [0, limit) becomes -1 (still an error row)."""
-    return np.fromiter((s.size_bytes if 0 <= s.size_bytes < limit else -1 for s in samples),
-                       dtype=np.int32, count=len(samples))
 
 
 def _fit_stats_host(x: np.ndarray, size: np.ndarray, label: np.ndarray, *, n_classes: int,
@@ -105,7 +92,8 @@ def train_group(samples: Sequence[SampleRecord], features: FeatureSet, alpha: fl
     cols = {op: j for j, op in enumerate(dict.fromkeys(ops))}
     x = _densify(samples, cols, max(len(cols), 1))
     zeros = np.zeros(len(samples), dtype=np.int32)
-    S, n, _ = _fit_stats_host(x, zeros, _label_codes(samples), n_classes=2, width=1, limit=1,
+    _, labels = _meta(samples, 1)
+    S, n, _ = _fit_stats_host(x, zeros, labels, n_classes=2, width=1, limit=1,
                               device=_device_ordinal(device))
     for c in CLASSES:
         if n[0, CLASS_INDEX[c]] == 0:
@@ -136,38 +124,12 @@ def train_bundle(train: GroupedCorpus, k: int, alpha: float = 1.0, *, seed: int 
     config = train.config
     samples = train.all_samples()
     vocab = sorted({op for s in samples for op in s.histogram.entries})
-    k_ok = isinstance(k, int) and not isinstance(k, bool) and k >= 1
-    a_ok = isinstance(alpha, (int, float)) and not isinstance(alpha, bool) and alpha > 0
-    models = []
-    if samples and vocab:
-        x = _densify(samples, {op: j for j, op in enumerate(vocab)}, len(vocab))
-        S, n, _ = _fit_stats_host(x, _sizes(samples, config.max_size_bytes),
-                                  _label_codes(samples), n_classes=2,
-                                  width=config.group_size_bytes, limit=config.max_size_bytes,
-                                  device=_device_ordinal(device))
-        from .dense import fin_train
-        fin = fin_train(S, n, k=k if k_ok else 1, alpha=float(alpha) if a_ok else 1.0,
-                        min_per_class=config.min_per_class)
-        for g in np.nonzero(fin.state != 0)[0].tolist():
-            if fin.state[g] == -1:
-                raise InsufficientClassError(f"group {g}: no malware opcode occurrences to score")
-            if fin.state[g] == -2:
-                raise InsufficientClassError(f"group {g}: no benign opcode occurrences to score")
-            if not k_ok:
-                raise InvalidConfigError(f"k must be a positive integer, got {k!r}")
-            if not a_ok:
-                raise InvalidConfigError(f"alpha must be positive, got {alpha!r}")
-            for s in train.groups.get(g, ()):
-                if s.label not in CLASS_INDEX:
-                    raise IntegrityError(f"sample {s.id!r} has no training label")
-            F = int(fin.n_features[g])
-            feats = FeatureSet(tuple(vocab[j] for j in fin.features[g, :F]), k)
-            models.append(_model(g, feats, fin.log_prior[g], fin.log_lik[g, :, :F],
-                                 n[g], float(alpha)))
-    if created_at is None:
-        created_at = datetime.now(timezone.utc).isoformat(timespec="seconds")
-    meta = BundleMeta(k=k, alpha=float(alpha), seed=seed, created_at=created_at)
-    return build_bundle(models, config, meta)
+    x = _densify(samples, {op: j for j, op in enumerate(vocab)}, max(len(vocab), 1))
+    size = np.array([s.size_bytes for s in samples], dtype=object)
+    size64 = np.array([v if -2**63 <= v < 2**63 else -1 for v in size], dtype=np.int64)
+    _, label = _meta(samples, config.max_size_bytes)
+    return _train_dense(x[:, :len(vocab)], size64, label, vocab, config, k, alpha, seed,
+                        created_at, _device_ordinal(device), [s.id for s in samples])
 
 
 # ---------------------------------------------------------------- predict
@@ -194,27 +156,14 @@ class _PackedBundle:
             self.columns.append({op: j for j, op in enumerate(m.features.opcodes)})
 
 
-def _gather(samples, packed: _PackedBundle, config: GroupingConfig) -> np.ndarray:
-    """Row i = counts of its routed model's features, FeatureSet order (engine.py:198-202)."""
+def _gather(samples, packed: _PackedBundle, config: GroupingConfig):
+    """Row i = counts of its routed model's features, FeatureSet order
+    (engine.py:198-202), plus int32 sizes (-1 outside [0, limit))."""
     x = np.zeros((len(samples), packed.F), dtype=np.int32)
-    w, lim = config.group_size_bytes, config.max_size_bytes
-    rows, cols, vals = [], [], []
-    for i, s in enumerate(samples):
-        if not 0 <= s.size_bytes < lim:
-            continue
-        colmap = packed.columns[packed.route[s.size_bytes // w]]
-        for op, n in s.histogram.entries.items():
-            j = colmap.get(op)
-            if j is not None:
-                rows.append(i)
-                cols.append(j)
-                vals.append(n)
-    if vals:
-        v = np.asarray(vals, dtype=np.int64)
-        if int(v.max()) > _I32_MAX:
-            raise InvalidConfigError("opcode counts must be < 2^31 for the GPU path")
-        x[np.asarray(rows), np.asarray(cols)] = v
-    return x
+    size = np.empty(len(samples), dtype=np.int32)
+    _adapt.gather_into(samples, packed.route, packed.columns, packed.F,
+                       config.group_size_bytes, config.max_size_bytes, x, size)
+    return x, size
 
 
 def _predict_host(x, size, packed: _PackedBundle, config: GroupingConfig, device: int):
@@ -244,8 +193,7 @@ def classify_gpu(bundle: ModelBundle, workload: Workload, *, warmup: bool = True
     if not samples:
         return TimedRun((), (), 0)
     packed = _PackedBundle(bundle)
-    x = _gather(samples, packed, config)
-    size = _sizes(samples, config.max_size_bytes)
+    x, size = _gather(samples, packed, config)
     dev = _device_ordinal(device)
     if warmup:
         _predict_host(x, size, packed, config, dev)
@@ -293,8 +241,8 @@ def predict(model: GroupModel, histogram: OpcodeHistogram, *, device=None) -> Pr
     bundle = ModelBundle(cfg, {0: model}, (0,), BundleMeta(len(model.features.opcodes), 1.0, 0, ""))
     packed = _PackedBundle(bundle)
     sample = SampleRecord("_", Label.UNKNOWN, 0, histogram)
-    x = _gather([sample], packed, cfg)
-    label, lp, _ = _predict_host(x, np.zeros(1, np.int32), packed, cfg, _device_ordinal(device))
+    x, size = _gather([sample], packed, cfg)
+    label, lp, _ = _predict_host(x, size, packed, cfg, _device_ordinal(device))
     return Prediction(INDEX_CLASS[int(label[0])],
                       {Label.MALWARE: float(lp[0, 1]), Label.BENIGN: float(lp[0, 0])},
                       model.group)

@@ -1,0 +1,64 @@
+"""ADAPT C-API packer (SampleRecord -> dense) against a plain Python restatement (CPU)."""
+
+import numpy as np
+import pytest
+
+from paper_1905_13746_b200 import _adapt
+from paper_1905_13746_b200.model import Label, OpcodeHistogram, SampleRecord
+
+
+def _samples(rng, n):
+    ops = [f"op{i}" for i in range(30)]
+    out = []
+    for i in range(n):
+        h = {ops[j]: int(rng.integers(1, 1000)) for j in rng.choice(30, int(rng.integers(0, 12)),
+                                                                     replace=False)}
+        lab = (Label.MALWARE, Label.BENIGN, Label.UNKNOWN)[i % 3]
+        out.append(SampleRecord(f"s{i}", lab, int(rng.integers(-10, 60000)),
+                                OpcodeHistogram.from_counts(h)))
+    return out
+
+
+def test_densify_and_meta():
+    rng = np.random.default_rng(0)
+    s = _samples(rng, 500)
+    cols = {f"op{i}": i // 2 for i in range(0, 30, 2)}   # every other opcode, packed
+    x = np.zeros((500, 15), np.int32)
+    _adapt.densify_into(s, cols, x, 15)
+    want = np.zeros_like(x)
+    for i, r in enumerate(s):
+        for op, n in r.histogram.entries.items():
+            if op in cols:
+                want[i, cols[op]] = n
+    assert np.array_equal(x, want)
+    size = np.empty(500, np.int32)
+    lab = np.empty(500, np.int32)
+    _adapt.meta_into(s, 50000, Label.MALWARE, Label.BENIGN, size, lab)
+    assert size.tolist() == [r.size_bytes if 0 <= r.size_bytes < 50000 else -1 for r in s]
+    assert lab.tolist() == [{Label.MALWARE: 1, Label.BENIGN: 0}.get(r.label, -1) for r in s]
+
+
+def test_gather_routes_per_sample():
+    rng = np.random.default_rng(1)
+    s = _samples(rng, 300)
+    route = np.array([0, 1, 1, 0, 1, 0], np.int32)          # 6 groups of 10000 bytes
+    colmaps = [{"op1": 0, "op2": 1, "op3": 2}, {"op29": 0, "op1": 2}]
+    x = np.zeros((300, 3), np.int32)
+    size = np.empty(300, np.int32)
+    _adapt.gather_into(s, route, colmaps, 3, 10000, 60000, x, size)
+    for i, r in enumerate(s):
+        if not 0 <= r.size_bytes < 60000:
+            assert size[i] == -1 and not x[i].any()
+            continue
+        cm = colmaps[route[r.size_bytes // 10000]]
+        want = np.zeros(3, np.int32)
+        for op, n in r.histogram.entries.items():
+            if op in cm:
+                want[cm[op]] = n
+        assert np.array_equal(x[i], want)
+
+
+def test_counts_beyond_int32_rejected():
+    s = [SampleRecord("a", Label.MALWARE, 1, OpcodeHistogram({"op": 2**31}))]
+    with pytest.raises(OverflowError):
+        _adapt.densify_into(s, {"op": 0}, np.zeros((1, 1), np.int32), 1)
