@@ -16,7 +16,9 @@
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
+#include <functional>
 #include <string>
+#include <string_view>
 #include <thread>
 #include <unordered_map>
 #include <unordered_set>
@@ -327,11 +329,14 @@ struct Row {
   std::string id;
   int8_t label;     // 1 malware, 0 benign, -1 unknown
   int64_t size;     // size_bytes; -1 if it does not fit int64 (only >= 2^63)
-  std::vector<std::pair<int32_t, int64_t>> ents;  // (local vocab id, count)
+  int64_t e0 = 0, e1 = 0;  // entries [e0, e1) in the shard's col/val arrays
 };
 
 struct Shard {
   std::vector<Row> rows;
+  std::vector<int32_t> col;  // shard-local vocab id per entry
+  std::vector<int64_t> val;
+  std::vector<int64_t> mark, pos;  // per local vocab id: last row touching it, entry index
   std::vector<int64_t> line_no;
   std::unordered_map<std::string, int32_t> vocab;
   std::vector<std::string> names;
@@ -353,6 +358,181 @@ bool is_blank(const char* a, const char* b) {
   for (; a < b; ++a)
     if (!(*a == ' ' || *a == '\t' || *a == '\r' || *a == '\n' || *a == '\v' || *a == '\f'))
       return false;
+  return true;
+}
+
+
+// Fast path for clean records: one pass, no DOM, no per-value allocation.
+// Returns false on anything unusual (escapes, duplicate keys, non-integer or
+// negative numbers, unknown labels, syntax errors...); the caller then runs
+// parse_line, which implements every rule and error message.
+struct FastScratch {
+  std::string key;
+};
+
+inline void skip_ws(const char*& p, const char* e) {
+  while (p < e && (*p == ' ' || *p == '\t' || *p == '\r' || *p == '\n')) ++p;
+}
+
+// "...": plain string without escapes; [s, s+n) excludes the quotes
+inline bool plain_str(const char*& p, const char* e, const char*& s, size_t& n) {
+  if (p >= e || *p != '"') return false;
+  s = ++p;
+  while (p < e && *p != '"') {
+    if (*p == '\\' || static_cast<unsigned char>(*p) < 0x20) return false;
+    ++p;
+  }
+  if (p >= e) return false;
+  n = static_cast<size_t>(p - s);
+  ++p;
+  return true;
+}
+
+inline bool plain_uint(const char*& p, const char* e, int64_t& v) {
+  const char* s = p;
+  v = 0;
+  while (p < e && *p >= '0' && *p <= '9') {
+    if (p - s >= 18) return false;  // leave big numbers to the full parser
+    v = v * 10 + (*p - '0');
+    ++p;
+  }
+  if (p == s || (p - s > 1 && *s == '0')) return false;
+  return !(p < e && (*p == '.' || *p == 'e' || *p == 'E'));
+}
+
+bool skip_value(const char*& p, const char* e, int depth) {  // syntax-checked skip
+  Parser ps{p, e, {}};
+  JVal v;
+  if (!ps.value(v, depth)) return false;
+  p = ps.p;
+  return true;
+}
+
+bool fast_line(const char* a, const char* b, bool allow_unlabeled, Shard& sh, Row& row,
+               FastScratch& fs) {
+  const char* p = a;
+  skip_ws(p, b);
+  if (p >= b || *p != '{') return false;
+  ++p;
+  unsigned seen = 0;  // id 1, label 2, size 4, opcodes 8
+  row.label = -1;
+  const int64_t row_tag = static_cast<int64_t>(sh.rows.size()) + 1;
+  const size_t col0 = sh.col.size();
+  row.e0 = static_cast<int64_t>(col0);
+  // on any bail-out the entries appended so far are dropped by the caller
+  skip_ws(p, b);
+  if (p < b && *p == '}') return false;
+  for (;;) {
+    skip_ws(p, b);
+    const char* ks;
+    size_t kn;
+    if (!plain_str(p, b, ks, kn)) return false;
+    skip_ws(p, b);
+    if (p >= b || *p != ':') return false;
+    ++p;
+    skip_ws(p, b);
+    unsigned bit = 0;
+    if (kn == 2 && memcmp(ks, "id", 2) == 0) bit = 1;
+    else if (kn == 5 && memcmp(ks, "label", 5) == 0) bit = 2;
+    else if (kn == 10 && memcmp(ks, "size_bytes", 10) == 0) bit = 4;
+    else if (kn == 7 && memcmp(ks, "opcodes", 7) == 0) bit = 8;
+    if (bit & seen) return false;  // duplicate key: json.loads keeps the last one
+    seen |= bit;
+    if (bit == 1) {
+      const char* s;
+      size_t n;
+      if (!plain_str(p, b, s, n) || n == 0) return false;
+      row.id.assign(s, n);
+    } else if (bit == 2) {
+      const char* s;
+      size_t n;
+      if (!plain_str(p, b, s, n)) return false;
+      if (n == 7 && memcmp(s, "malware", 7) == 0) row.label = 1;
+      else if (n == 6 && memcmp(s, "benign", 6) == 0) row.label = 0;
+      else return false;
+    } else if (bit == 4) {
+      int64_t v;
+      if (!plain_uint(p, b, v)) return false;
+      row.size = v;
+    } else if (bit == 8) {
+      if (p >= b || *p != '{') return false;
+      ++p;
+      skip_ws(p, b);
+      if (p < b && *p == '}') {
+        ++p;
+      } else {
+        for (;;) {
+          skip_ws(p, b);
+          const char* s;
+          size_t n;
+          if (!plain_str(p, b, s, n) || n == 0) return false;
+          skip_ws(p, b);
+          if (p >= b || *p != ':') return false;
+          ++p;
+          skip_ws(p, b);
+          int64_t v;
+          if (!plain_uint(p, b, v)) return false;
+          // a zero count may shadow an earlier duplicate key (JSON last-wins):
+          // rare, so the full parser takes it
+          if (v == 0) return false;
+          {
+            fs.key.assign(s, n);
+            for (char& c : fs.key)
+              if (c >= 'A' && c <= 'Z') c = static_cast<char>(c - 'A' + 'a');
+            auto f = sh.vocab.find(fs.key);
+            int32_t vid;
+            if (f == sh.vocab.end()) {
+              vid = static_cast<int32_t>(sh.names.size());
+              sh.vocab.emplace(fs.key, vid);
+              sh.names.push_back(fs.key);
+              sh.mark.push_back(0);
+              sh.pos.push_back(0);
+            } else {
+              vid = f->second;
+            }
+            if (sh.mark[vid] == row_tag) {
+              // repeated key (exact duplicate: JSON last-wins) or case variant
+              // (merged): both rare, both left to the full parser
+              return false;
+            } else {
+              sh.mark[vid] = row_tag;
+              sh.pos[vid] = static_cast<int64_t>(sh.col.size());
+              sh.col.push_back(vid);
+              sh.val.push_back(v);
+            }
+          }
+          skip_ws(p, b);
+          if (p < b && *p == ',') {
+            ++p;
+            continue;
+          }
+          if (p < b && *p == '}') {
+            ++p;
+            break;
+          }
+          return false;
+        }
+      }
+    } else {
+      if (!skip_value(p, b, 1)) return false;
+    }
+    skip_ws(p, b);
+    if (p < b && *p == ',') {
+      ++p;
+      continue;
+    }
+    if (p < b && *p == '}') {
+      ++p;
+      break;
+    }
+    return false;
+  }
+  skip_ws(p, b);
+  if (p != b) return false;
+  if (!(seen & 1) || !(seen & 4) || !(seen & 8)) return false;
+  if (!(seen & 2) && !allow_unlabeled) return false;
+  row.e1 = static_cast<int64_t>(sh.col.size());
+  (void)col0;
   return true;
 }
 
@@ -457,6 +637,8 @@ bool parse_line(const char* a, const char* b, bool allow_unlabeled, Shard& sh, R
       vid = static_cast<int32_t>(sh.names.size());
       sh.vocab.emplace(key, vid);
       sh.names.push_back(key);
+      sh.mark.push_back(0);
+      sh.pos.push_back(0);
     } else {
       vid = f->second;
     }
@@ -468,7 +650,12 @@ bool parse_line(const char* a, const char* b, bool allow_unlabeled, Shard& sh, R
       ents[w->second].second += c.i;
     }
   }
-  row.ents = std::move(ents);
+  row.e0 = static_cast<int64_t>(sh.col.size());
+  for (const auto& e : ents) {
+    sh.col.push_back(e.first);
+    sh.val.push_back(e.second);
+  }
+  row.e1 = static_cast<int64_t>(sh.col.size());
   return true;
 }
 
@@ -495,31 +682,62 @@ int gnb_corpus_parse(const char* text, size_t len, int32_t allow_unlabeled, int3
   if (!out || (!text && len)) return GNB_EINVAL;
   auto* c = new gnb_corpus();
   *out = c;
-  // line starts (1-based numbering like enumerate(..., start=1))
-  std::vector<size_t> starts;
-  starts.push_back(0);
-  for (size_t i = 0; i < len; ++i)
-    if (text[i] == '\n' && i + 1 < len) starts.push_back(i + 1);
-  if (len == 0) starts.clear();
-  const int64_t L = static_cast<int64_t>(starts.size());
   int T = threads > 0 ? threads : static_cast<int>(std::thread::hardware_concurrency());
-  if (T < 1) T = 1;
-  if (T > 64) T = 64;
-  if (L < 4096) T = 1;
+  T = std::max(1, std::min(T, 64));
+  if (len < (size_t(1) << 20)) T = 1;
+  auto run = [T](const std::function<void(int)>& f) {
+    std::vector<std::thread> th;
+    for (int t = 1; t < T; ++t) th.emplace_back(f, t);
+    f(0);
+    for (auto& x : th) x.join();
+  };
+  // byte ranges cut at line starts; per-range line counts give 1-based line
+  // numbers (enumerate(..., start=1)) without a serial scan
+  std::vector<size_t> cut(T + 1, len);
+  cut[0] = 0;
+  for (int t = 1; t < T; ++t) {
+    size_t q = len * static_cast<size_t>(t) / T;
+    while (q < len && text[q - 1] != '\n') ++q;
+    cut[t] = std::max(q, cut[t - 1]);
+  }
+  std::vector<int64_t> nlines(T, 0), first_line(T, 1);
+  run([&](int t) {
+    int64_t k = 0;
+    for (size_t i = cut[t]; i < cut[t + 1]; ++i) k += text[i] == '\n';
+    if (cut[t + 1] > cut[t] && text[cut[t + 1] - 1] != '\n') ++k;  // unterminated last line
+    nlines[t] = k;
+  });
+  for (int t = 1; t < T; ++t) first_line[t] = first_line[t - 1] + nlines[t - 1];
   std::vector<Shard> shards(T);
-  auto work = [&](int t) {
+  run([&](int t) {
     Shard& sh = shards[t];
-    const int64_t lo = L * t / T, hi = L * (t + 1) / T;
-    for (int64_t ln = lo; ln < hi; ++ln) {
-      const char* a = text + starts[ln];
-      const char* b = text + (ln + 1 < L ? starts[ln + 1] : len);
-      while (b > a && (b[-1] == '\n' || b[-1] == '\r')) --b;
+    FastScratch fs;
+    sh.rows.reserve(static_cast<size_t>(nlines[t]));
+    sh.line_no.reserve(static_cast<size_t>(nlines[t]));
+    const char* p = text + cut[t];
+    const char* end = text + cut[t + 1];
+    int64_t ln = first_line[t];
+    for (; p < end; ++ln) {
+      const char* a = p;
+      const char* nl = static_cast<const char*>(memchr(a, '\n', static_cast<size_t>(end - a)));
+      const char* b = nl ? nl : end;
+      p = nl ? nl + 1 : end;
+      while (b > a && b[-1] == '\r') --b;
       if (is_blank(a, b)) continue;
       Row row;
       int kind = 0;
       std::string msg;
+      const size_t mark = sh.col.size();
+      if (fast_line(a, b, allow_unlabeled != 0, sh, row, fs)) {
+        sh.rows.push_back(std::move(row));
+        sh.line_no.push_back(ln);
+        continue;
+      }
+      sh.col.resize(mark);  // discard the fast path's partial entries
+      sh.val.resize(mark);
+      row = Row();
       if (!parse_line(a, b, allow_unlabeled != 0, sh, row, kind, msg)) {
-        sh.err_line = ln + 1;
+        sh.err_line = ln;
         sh.err_kind = kind;
         sh.err_msg = msg;
         sh.err_has_id = !row.id.empty();
@@ -527,13 +745,9 @@ int gnb_corpus_parse(const char* text, size_t len, int32_t allow_unlabeled, int3
         return;  // later lines of this shard cannot matter
       }
       sh.rows.push_back(std::move(row));
-      sh.line_no.push_back(ln + 1);
+      sh.line_no.push_back(ln);
     }
-  };
-  std::vector<std::thread> th;
-  for (int t = 1; t < T; ++t) th.emplace_back(work, t);
-  work(0);
-  for (auto& x : th) x.join();
+  });
   // first error by line; duplicate ids before it win (the reference parses in order)
   int64_t first_err = -1;
   const Shard* err_sh = nullptr;
@@ -545,7 +759,10 @@ int gnb_corpus_parse(const char* text, size_t len, int32_t allow_unlabeled, int3
       c->err_msg = sh.err_msg;
     }
   {
-    std::unordered_set<std::string> seen;
+    size_t total = 0;
+    for (auto& sh : shards) total += sh.rows.size();
+    std::unordered_set<std::string_view> seen;
+    seen.reserve(total * 2);
     for (auto& sh : shards)
       for (size_t r = 0; r < sh.rows.size(); ++r) {
         if (first_err >= 0 && sh.line_no[r] > first_err) break;
@@ -557,21 +774,16 @@ int gnb_corpus_parse(const char* text, size_t len, int32_t allow_unlabeled, int3
           return GNB_EINVAL;
         }
       }
-  }
-  if (first_err >= 0) {
-    c->err_line = first_err;
-    if (err_sh->err_has_id) {  // corpus.py:159-160 checks duplicates before the rest
-      std::unordered_set<std::string> seen;
-      for (auto& sh : shards)
-        for (size_t r = 0; r < sh.rows.size() && sh.line_no[r] < first_err; ++r)
-          seen.insert(sh.rows[r].id);
-      if (seen.count(err_sh->err_id)) {
+    if (first_err >= 0) {
+      c->err_line = first_err;
+      // corpus.py:159-160 checks duplicates before the rest of the record
+      if (err_sh->err_has_id && seen.count(err_sh->err_id)) {
         c->err_kind = 2;
         c->err_msg = "duplicate id " + py_str_repr(err_sh->err_id) + " at line " +
                      std::to_string(first_err);
       }
+      return GNB_EINVAL;
     }
-    return GNB_EINVAL;
   }
   // global vocabulary: sorted union; remap shard-local ids
   std::vector<std::string> all;
@@ -582,33 +794,38 @@ int gnb_corpus_parse(const char* text, size_t len, int32_t allow_unlabeled, int3
   std::unordered_map<std::string, int32_t> gid;
   gid.reserve(all.size() * 2);
   for (size_t k = 0; k < all.size(); ++k) gid.emplace(all[k], static_cast<int32_t>(k));
-  int64_t n = 0, nnz = 0;
-  for (auto& sh : shards) {
-    n += static_cast<int64_t>(sh.rows.size());
-    for (auto& r : sh.rows) nnz += static_cast<int64_t>(r.ents.size());
+  std::vector<int64_t> row_off(T + 1, 0), ent_off(T + 1, 0);
+  for (int t = 0; t < T; ++t) {
+    row_off[t + 1] = row_off[t] + static_cast<int64_t>(shards[t].rows.size());
+    ent_off[t + 1] = ent_off[t] + static_cast<int64_t>(shards[t].col.size());
   }
-  c->ids.reserve(n);
-  c->size.reserve(n);
-  c->label.reserve(n);
-  c->row_ptr.reserve(n + 1);
-  c->col.reserve(nnz);
-  c->val.reserve(nnz);
-  c->row_ptr.push_back(0);
-  for (auto& sh : shards) {
+  const int64_t n = row_off[T], nnz = ent_off[T];
+  c->ids.resize(n);
+  c->size.resize(n);
+  c->label.resize(n);
+  c->row_ptr.resize(n + 1);
+  c->col.resize(nnz);
+  c->val.resize(nnz);
+  c->row_ptr[0] = 0;
+  std::vector<int64_t> maxc(T, 0);
+  run([&](int t) {  // scatter each shard into its slice of the global arrays
+    Shard& sh = shards[t];
     std::vector<int32_t> map(sh.names.size());
-    for (size_t k = 0; k < sh.names.size(); ++k) map[k] = gid[sh.names[k]];
-    for (auto& r : sh.rows) {
-      c->ids.push_back(std::move(r.id));
-      c->size.push_back(r.size);
-      c->label.push_back(r.label);
-      for (auto& e : r.ents) {
-        c->col.push_back(map[e.first]);
-        c->val.push_back(e.second);
-        c->max_count = std::max(c->max_count, e.second);
+    for (size_t k = 0; k < sh.names.size(); ++k) map[k] = gid.at(sh.names[k]);
+    int64_t r = row_off[t], e = ent_off[t];
+    for (auto& row : sh.rows) {
+      c->ids[r] = std::move(row.id);
+      c->size[r] = row.size;
+      c->label[r] = row.label;
+      for (int64_t k = row.e0; k < row.e1; ++k, ++e) {
+        c->col[e] = map[sh.col[k]];
+        c->val[e] = sh.val[k];
+        maxc[t] = std::max(maxc[t], sh.val[k]);
       }
-      c->row_ptr.push_back(static_cast<int64_t>(c->col.size()));
+      c->row_ptr[++r] = e;
     }
-  }
+  });
+  for (int64_t m : maxc) c->max_count = std::max(c->max_count, m);
   return GNB_OK;
 }
 

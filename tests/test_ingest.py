@@ -77,3 +77,15 @@ def test_prediction_writer_byte_identical():
     c = ingest.read_corpus(str(w["text_in"]), allow_unlabeled=True)
     text = c.predictions_jsonl(w["label"], np.nan_to_num(w["lp"]), w["eff"], 512000)
     assert text == str(w["out"])
+
+
+@pytest.mark.parametrize("ops,want", [
+    ('{"mov": 5, "mov": 0}', {}), ('{"mov": 0, "mov": 5}', {"mov": 5}),
+    ('{"MOV": 2, "mov": 3}', {"mov": 5}), ('{"a": 1, "b": 2, "a": 7}', {"a": 7, "b": 2}),
+    ('{"x\\u0041": 1}', {"xa": 1}), ('{"add": 0}', {})])
+def test_duplicate_and_case_keys_like_json_loads(ops, want):
+    """Edge rules the fast path defers to the full parser: JSON last-wins duplicates,
+    case-fold merging, zero counts, escaped keys (json.loads + from_counts semantics)."""
+    text = '{"id": "a", "label": "benign", "size_bytes": 1, "opcodes": %s}' % ops
+    rec = ingest.parse_corpus(text)[0]
+    assert rec.histogram.entries == want
