@@ -3,7 +3,7 @@ NVCC ?= nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -O3
 PKG := paper_1905_13746_b200
-SRC := $(PKG)/csrc/predict.cu $(PKG)/csrc/fit.cu $(PKG)/csrc/gen.cu $(PKG)/csrc/gather.cu $(PKG)/csrc/sort.cu $(PKG)/csrc/api.cu $(PKG)/csrc/fin.cpp $(PKG)/csrc/ingest.cpp
+SRC := $(PKG)/csrc/predict.cu $(PKG)/csrc/fit.cu $(PKG)/csrc/gen.cu $(PKG)/csrc/gather.cu $(PKG)/csrc/sort.cu $(PKG)/csrc/fin_select.cu $(PKG)/csrc/api.cu $(PKG)/csrc/fin.cpp $(PKG)/csrc/ingest.cpp
 HDR := $(wildcard $(PKG)/csrc/*.h $(PKG)/csrc/*.cuh) include/gnb.h
 
 PYINC := $(shell python3 -c "import sysconfig; print(sysconfig.get_paths()['include'])")

@@ -201,6 +201,16 @@ int gnb_fin_train(const double* sums, const double* counts, int32_t n_groups, in
                   int32_t* n_features, int32_t* features, double* log_prior,
                   double* log_lik);
 
+/* gnb_fin_train with the scoring + top-k on the DEVICE (one CTA per group,
+ * shared-memory bitonic sort of (-score, column)); sums/counts are DEVICE
+ * pointers (gnb_fit_stats outputs), results land in HOST arrays as for
+ * gnb_fin_train and are identical to it (libm logs on the host).  Vocabularies
+ * up to 16384 columns; synchronises `stream`. */
+int gnb_fin_train_device(const double* sums, const double* counts, int32_t n_groups,
+                         int32_t n_cols, int32_t k, double alpha, int32_t min_per_class,
+                         int32_t* group_state, int32_t* n_features, int32_t* features,
+                         double* log_prior, double* log_lik, uintptr_t stream);
+
 /* train_group for ONE group with a given feature list and C classes
  * (classifier.py:103-120 with a class axis; C = 2 reproduces the reference):
  * sums_g[C][V], counts_g[C] -> log_prior[C], log_lik[C][F].  Host, libm log. */

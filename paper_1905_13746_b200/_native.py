@@ -71,6 +71,8 @@ _SIGS = {
     "gnb_fit_stats_host": ([_p, _i64, _i32, _i64, _p, _p, _i32, _i32, _i32, _p, _p, _p, _p, _i32],
                            C.c_int),
     "gnb_fin_train": ([_p, _p, _i32, _i32, _i32, _f64, _i32, _p, _p, _p, _p, _p], C.c_int),
+    "gnb_fin_train_device": ([_p, _p, _i32, _i32, _i32, _f64, _i32, _p, _p, _p, _p, _p, _up],
+                             C.c_int),
     "gnb_fin_tables": ([_p, _p, _i32, _i32, _p, _i32, _f64, _p, _p], C.c_int),
     "gnb_generate": ([_p, _i64, _i32, _i64, _p, _p, _i64, _p, _i32, _i32, _i32, _f64, _u64, _p,
                       _i32, _up],

@@ -233,6 +233,68 @@ int gnb_predict_typed(const void* x, int32_t x_type, int64_t n_rows, int32_t n_f
                         logpost_out, reinterpret_cast<cudaStream_t>(stream));
 }
 
+int gnb_fin_train_device(const double* sums, const double* counts, int32_t n_groups,
+                         int32_t n_cols, int32_t k, double alpha, int32_t min_per_class,
+                         int32_t* group_state, int32_t* n_features, int32_t* features,
+                         double* log_prior, double* log_lik, uintptr_t stream_) {
+  if (!sums || !counts || !group_state || !n_features || !features || !log_prior || !log_lik)
+    return fail(GNB_EINVAL, "fin_train_device: null pointer");
+  if (n_groups < 1 || n_cols < 1 || k < 1 || !(alpha > 0.0) || min_per_class < 1)
+    return fail(GNB_EINVAL, "fin_train_device: bad arguments");
+  if (n_cols > fin_select_max_vocab())
+    return fail(GNB_EUNSUPPORTED, "fin_train_device: vocabulary above %d columns",
+                fin_select_max_vocab());
+  cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
+  const size_t G = static_cast<size_t>(n_groups);
+  int32_t* d_i32 = nullptr;
+  double* d_sel = nullptr;
+  GNB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_i32), (2 + size_t(k)) * G * 4, stream),
+           "malloc");
+  GNB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_sel), 2 * size_t(k) * G * 8, stream),
+           "malloc");
+  int32_t* d_state = d_i32;
+  int32_t* d_nf = d_i32 + G;
+  int32_t* d_feat = d_i32 + 2 * G;
+  cudaError_t e = fin_select_launch(sums, counts, n_groups, n_cols, k, min_per_class, d_state,
+                                    d_nf, d_feat, d_sel, stream);
+  std::vector<double> sel(2 * size_t(k) * G), cnt(2 * G);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(group_state, d_state, G * 4, cudaMemcpyDeviceToHost, stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(n_features, d_nf, G * 4, cudaMemcpyDeviceToHost, stream);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(features, d_feat, G * size_t(k) * 4, cudaMemcpyDeviceToHost, stream);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(sel.data(), d_sel, sel.size() * 8, cudaMemcpyDeviceToHost, stream);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(cnt.data(), counts, cnt.size() * 8, cudaMemcpyDeviceToHost, stream);
+  cudaFreeAsync(d_i32, stream);
+  cudaFreeAsync(d_sel, stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+  if (e != cudaSuccess) return cuda_fail(e, "fin_train_device");
+  // libm logarithms on the host (bit-identical to CPython's math.log)
+  std::vector<int32_t> iota(static_cast<size_t>(k));
+  for (int j = 0; j < k; ++j) iota[j] = j;
+  std::vector<double> lik(2 * size_t(k));
+  for (size_t g = 0; g < G; ++g) {
+    std::fill(log_prior + 2 * g, log_prior + 2 * g + 2, 0.0);
+    std::fill(log_lik + 2 * g * k, log_lik + 2 * (g + 1) * k, 0.0);
+    if (group_state[g] != 1) {
+      std::fill(features + g * k, features + (g + 1) * k, 0);
+      continue;
+    }
+    const int F = n_features[g];
+    const double* sg = sel.data() + 2 * g * k;  // [2][k]
+    std::vector<double> s2(2 * size_t(F));
+    for (int c = 0; c < 2; ++c)
+      for (int j = 0; j < F; ++j) s2[c * F + j] = sg[c * k + j];
+    gnb_fin_tables(s2.data(), cnt.data() + 2 * g, 2, F, iota.data(), F, alpha, log_prior + 2 * g,
+                   lik.data());
+    for (int c = 0; c < 2; ++c)
+      for (int j = 0; j < F; ++j) log_lik[(2 * g + c) * k + j] = lik[c * size_t(F) + j];
+  }
+  return GNB_OK;
+}
+
 size_t gnb_slot_sort_workspace_bytes(int64_t n_rows, int32_t n_slots) {
   if (n_rows < 0 || n_slots < 1) return 0;
   return slot_sort_workspace(n_rows, n_slots);

@@ -92,6 +92,11 @@ size_t slot_sort_workspace(int64_t n, int S);
 cudaError_t slot_sort(const int32_t* size, int64_t n, int width, int limit, const int32_t* route,
                       int S, int32_t* perm, void* workspace, cudaStream_t stream);
 
+int fin_select_max_vocab();
+cudaError_t fin_select_launch(const double* sums, const double* counts, int G, int V, int k,
+                              int min_per_class, int32_t* state, int32_t* n_features,
+                              int32_t* features, double* selected, cudaStream_t stream);
+
 // Host helpers (api.cu)
 bool encode_rows_map(CUtensorMap* map, const void* base, int64_t n_rows, int32_t n_cols,
                      int64_t ldx, int box_rows);

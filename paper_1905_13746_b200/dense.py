@@ -266,6 +266,23 @@ def fin_train(sums, counts, *, k: int, alpha: float, min_per_class: int) -> FinR
     return res
 
 
+def fin_train_device(stats: FitStats, *, k: int, alpha: float, min_per_class: int,
+                     stream=None) -> FinResult:
+    """fin_train with scoring + top-k on the device (C = 2, V <= 16384)."""
+    S, n = stats.sums, stats.counts
+    if S.dim() != 3 or S.shape[1] != 2:
+        raise InvalidConfigError("fin_train_device needs 2-class statistics")
+    G, _, V = S.shape
+    res = FinResult(np.zeros(G, np.int32), np.zeros(G, np.int32), np.zeros((G, k), np.int32),
+                    np.zeros((G, 2)), np.zeros((G, 2, k)))
+    ptr = lambda a: a.ctypes.data  # noqa: E731
+    N.check(N.lib.gnb_fin_train_device(
+        S.contiguous().data_ptr(), n.contiguous().data_ptr(), G, V, k, float(alpha),
+        min_per_class, ptr(res.state), ptr(res.n_features), ptr(res.features),
+        ptr(res.log_prior), ptr(res.log_lik), _stream(stream)), "gnb_fin_train_device")
+    return res
+
+
 def fin_tables(sums_g, counts_g, features, alpha: float):
     """train_group for one group with a given feature list; any class count."""
     S = np.ascontiguousarray(np.asarray(sums_g, dtype=np.float64))

@@ -120,3 +120,29 @@ def test_narrow_storage_fit(dtype, hi, V, C):
     assert np.array_equal(st.sumsq.cpu().numpy(), Q.astype(np.float64))
     assert np.array_equal(st.counts.cpu().numpy(), n.astype(np.float64))
     assert st.status.cpu().tolist() == [bad, oor]
+
+
+@pytest.mark.parametrize("V,G,k", [(1, 1, 1), (40, 3, 15), (256, 1, 100), (1000, 32, 200),
+                                   (5000, 4, 300), (16384, 2, 64)])
+def test_device_fin_matches_host_fin(V, G, k):
+    """Device scoring + top-k (bitonic sort) == host FIN (itself pinned to the reference)."""
+    rng = np.random.default_rng(V + G)
+    S = rng.integers(0, 50, size=(G, 2, V)) * (rng.random((G, 2, V)) < 0.7)
+    half = V // 2
+    S[:, :, 1:2 * half:2] = S[:, :, 0:2 * half:2]                 # plenty of score ties
+    n = rng.integers(0, 12, size=(G, 2))
+    if G > 2:
+        S[1, 1] = 0                                                # insufficient malware
+    st = dense.FitStats(torch.from_numpy(S.astype(np.float64)).cuda(), None,
+                        torch.from_numpy(n.astype(np.float64)).cuda(),
+                        torch.zeros(2, dtype=torch.int64, device="cuda"))
+    dev = dense.fin_train_device(st, k=k, alpha=1.0, min_per_class=3)
+    host = dense.fin_train(S.astype(np.float64), n.astype(np.float64), k=k, alpha=1.0,
+                           min_per_class=3)
+    assert dev.state.tolist() == host.state.tolist()
+    assert dev.n_features.tolist() == host.n_features.tolist()
+    for g in range(G):
+        F = int(host.n_features[g])
+        assert dev.features[g, :F].tolist() == host.features[g, :F].tolist()
+    assert dev.log_prior.tobytes() == host.log_prior.tobytes()
+    assert dev.log_lik.tobytes() == host.log_lik.tobytes()
