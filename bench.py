@@ -54,6 +54,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-logpost", action="store_true")
     ap.add_argument("--fit-rows", type=int, default=1_000_000_000)
+    ap.add_argument("--ref-rows", type=int, default=2_000_000,
+                    help="CPU reference arm: rows scored per step (bounded sample)")
     ap.add_argument("--dist-backend", choices=("nccl", "gloo"), default="nccl",
                     help="gloo: exercise the multi-rank path with ranks sharing one GPU "
                          "(host-side collectives only; testing, not a bench number)")
@@ -422,7 +424,7 @@ def run_reference(args, world, rank):
     if rank != 0:
         return None
     V = args.features
-    sample = 2_000_000
+    sample = args.ref_rows
     x, size, label = O.synth_dense(sample, V, seed=0, divergence=0.8)
     S, _, n, _, _ = O.fit_stats(x, size, label, 2, 5120, 5120)
     feats, _ = O.select_features(S[0], V, 0)
