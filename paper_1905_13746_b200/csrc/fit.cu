@@ -41,13 +41,13 @@ constexpr int kMaxHistKeys = 4096;   // keys sorted by the shared-memory histogr
 //   int32 : 2 boxes x 32 columns = 64 columns, CPL 2 (LDS.64)
 //   uint16: 1 box  x 64 columns  = 64 columns, CPL 2 (LDS.32)
 //   uint8 : 1 box  x 128 columns = 128 columns, CPL 4 (LDS.32)
-template <typename T>
+template <typename T, int BX = (sizeof(T) == 4 ? 2 : 1)>
 struct FitGeom {
   // rows per tile (u8 permutation).  256-row tiles for narrow rows were
   // measured slower (fewer CTAs per SM), profiles/r01_tuning.md.
   static constexpr int kRows = 128;
   static constexpr int kBoxCols = kChunkBytesPerRow / static_cast<int>(sizeof(T));
-  static constexpr int kBoxes = sizeof(T) == 4 ? 2 : 1;
+  static constexpr int kBoxes = BX;
   static constexpr int kGroupCols = kBoxCols * kBoxes;
   static constexpr int kCPL = kGroupCols / 32;
   static constexpr int kLaneBytes = kCPL * static_cast<int>(sizeof(T));
@@ -61,11 +61,12 @@ struct FitHdr {
   int2 runs[ROWS];  // {key, start | len << 16}
 };
 
-template <typename T, int NW, int STAGES>
+template <typename T, int NW, int STAGES, int BX>
 struct FitSmem {
-  using Hdr = FitHdr<FitGeom<T>::kRows>;
-  static constexpr int kBox = FitGeom<T>::kRows * kChunkBytesPerRow;  // 16 / 32 KB
-  static constexpr int kStage = FitGeom<T>::kBoxes * kBox;    // 32 / 16 KB
+  using Geo = FitGeom<T, BX>;
+  using Hdr = FitHdr<Geo::kRows>;
+  static constexpr int kBox = Geo::kRows * kChunkBytesPerRow;  // 16 KB
+  static constexpr int kStage = Geo::kBoxes * kBox;             // 16 / 32 KB
   static constexpr int kX = 0;
   static constexpr int kHdr = kX + STAGES * kStage;
   static constexpr int kScratch = kHdr + STAGES * static_cast<int>(sizeof(Hdr));
@@ -82,31 +83,41 @@ __device__ __forceinline__ void add_u64x2(unsigned long long* p, unsigned long l
   *reinterpret_cast<ulonglong2*>(p) = v;
 }
 
-// column e (< CPL) of a lane's slice of one box row
-template <typename T>
-__device__ __forceinline__ void load_lane(const uint8_t* at, uint32_t (&x)[FitGeom<T>::kCPL]) {
-  if constexpr (sizeof(T) == 4) {
+// the CPL columns of a lane's slice of one box row
+template <typename T, int CPL>
+__device__ __forceinline__ void load_lane(const uint8_t* at, uint32_t (&x)[CPL]) {
+  constexpr int bytes = CPL * static_cast<int>(sizeof(T));
+  uint32_t w[bytes / 4];
+  if constexpr (bytes == 4) {
+    w[0] = *reinterpret_cast<const uint32_t*>(at);
+  } else if constexpr (bytes == 8) {
     const uint2 v = *reinterpret_cast<const uint2*>(at);
-    x[0] = v.x;
-    x[1] = v.y;
-  } else if constexpr (sizeof(T) == 2) {
-    const uint32_t w = *reinterpret_cast<const uint32_t*>(at);
-    x[0] = w & 0xffffu;
-    x[1] = w >> 16;
+    w[0] = v.x;
+    w[1] = v.y;
   } else {
-    const uint32_t w = *reinterpret_cast<const uint32_t*>(at);
-    x[0] = w & 0xffu;
-    x[1] = (w >> 8) & 0xffu;
-    x[2] = (w >> 16) & 0xffu;
-    x[3] = w >> 24;
+    const uint4 v = *reinterpret_cast<const uint4*>(at);
+    w[0] = v.x;
+    w[1] = v.y;
+    w[2] = v.z;
+    w[3] = v.w;
+  }
+#pragma unroll
+  for (int e = 0; e < CPL; ++e) {
+    if constexpr (sizeof(T) == 4) {
+      x[e] = w[e];
+    } else {
+      constexpr int per = 4 / static_cast<int>(sizeof(T));
+      constexpr uint32_t mask = sizeof(T) == 2 ? 0xffffu : 0xffu;
+      x[e] = (w[e / per] >> (8 * sizeof(T) * (e % per))) & mask;
+    }
   }
 }
 
-template <typename T, int NW, int STAGES>
+template <typename T, int NW, int STAGES, int BX>
 __global__ void __launch_bounds__((NW + 1) * 32)
     fit_tma_kernel(const __grid_constant__ CUtensorMap xmap, const FitParams p) {
-  using L = FitSmem<T, NW, STAGES>;
-  using Geo = FitGeom<T>;
+  using L = FitSmem<T, NW, STAGES, BX>;
+  using Geo = typename L::Geo;
   using FitHdrT = typename L::Hdr;
   constexpr int kGroupCols = Geo::kGroupCols;
   constexpr int CPL = Geo::kCPL;
@@ -344,7 +355,7 @@ __global__ void __launch_bounds__((NW + 1) * 32)
 #pragma unroll
               for (int u = 0; u < 4; ++u) {
                 const uint32_t r = hdr->perm[start + i + u];
-                load_lane<T>(xs + (r << 7), v[u]);
+                load_lane<T, CPL>(xs + (r << 7), v[u]);
               }
 #pragma unroll
               for (int u = 0; u < 4; ++u)
@@ -356,7 +367,7 @@ __global__ void __launch_bounds__((NW + 1) * 32)
             }
             for (; i < len; ++i) {
               uint32_t v[CPL];
-              load_lane<T>(xs + (static_cast<uint32_t>(hdr->perm[start + i]) << 7), v);
+              load_lane<T, CPL>(xs + (static_cast<uint32_t>(hdr->perm[start + i]) << 7), v);
 #pragma unroll
               for (int e = 0; e < CPL; ++e) {
                 sa[e] += v[e];
@@ -364,11 +375,16 @@ __global__ void __launch_bounds__((NW + 1) * 32)
               }
             }
             if (k < KS) {
+              if constexpr (CPL == 1) {
+                part_s[static_cast<int64_t>(k) * Vp + col0] += sa[0];
+                if (p.sumsq) part_q[static_cast<int64_t>(k) * Vp + col0] += qa[0];
+              } else {
 #pragma unroll
-              for (int e = 0; e < CPL; e += 2) {
-                add_u64x2(part_s + static_cast<int64_t>(k) * Vp + col0 + e, sa[e], sa[e + 1]);
-                if (p.sumsq)
-                  add_u64x2(part_q + static_cast<int64_t>(k) * Vp + col0 + e, qa[e], qa[e + 1]);
+                for (int e = 0; e < CPL; e += 2) {
+                  add_u64x2(part_s + static_cast<int64_t>(k) * Vp + col0 + e, sa[e], sa[e + 1]);
+                  if (p.sumsq)
+                    add_u64x2(part_q + static_cast<int64_t>(k) * Vp + col0 + e, qa[e], qa[e + 1]);
+                }
               }
             } else {
 #pragma unroll
@@ -403,12 +419,12 @@ __global__ void __launch_bounds__((NW + 1) * 32)
     if (part_n[k]) atomicAdd(p.counts + k, static_cast<double>(part_n[k]));
 }
 
-template <typename T, int NW, int STAGES>
+template <typename T, int NW, int STAGES, int BX = (sizeof(T) == 4 ? 2 : 1)>
 static cudaError_t launch_fit(const CUtensorMap& map, FitParams p, cudaStream_t stream,
                               int ctas_per_sm) {
-  using L = FitSmem<T, NW, STAGES>;
-  auto kern = fit_tma_kernel<T, NW, STAGES>;
-  constexpr int kGroupCols = FitGeom<T>::kGroupCols;
+  using L = FitSmem<T, NW, STAGES, BX>;
+  auto kern = fit_tma_kernel<T, NW, STAGES, BX>;
+  constexpr int kGroupCols = L::Geo::kGroupCols;
   p.n_chunks = (p.n_cols + kGroupCols - 1) / kGroupCols;
   int dev = 0, sms = 0, max_smem = 0;
   cudaGetDevice(&dev);
@@ -445,7 +461,7 @@ int fit_box_rows(int x_type) {
 
 // GNB_FIT_VARIANT (profiling only): 0 = 2 stages x 2 CTAs/SM (default; measured
 // best on B200, profiles/r01_tuning.md), 1 = 4 stages x 1 CTA/SM,
-// 2 = 5 stages x 1 CTA/SM, 3 = 3 stages x 1 CTA/SM.
+// 2 = one-box (16 KB) stages x 4 x 2 CTAs/SM, 3 = one-box stages x 3 x 2 CTAs/SM.
 static int fit_variant() {
   static int v = -1;
   if (v < 0) {
@@ -471,8 +487,8 @@ template <typename T, int NW>
 static cudaError_t launch_fit_nw(const CUtensorMap& map, const FitParams& p, cudaStream_t stream) {
   switch (fit_variant()) {
     case 1: return launch_fit<T, NW, 4>(map, p, stream, 1);
-    case 2: return launch_fit<T, NW, 5>(map, p, stream, 1);
-    case 3: return launch_fit<T, NW, 3>(map, p, stream, 1);
+    case 2: return launch_fit<T, NW, 4, 1>(map, p, stream, 2);  // 16-KB stages, 4 deep
+    case 3: return launch_fit<T, NW, 3, 1>(map, p, stream, 2);
     default: return launch_fit<T, NW, 2>(map, p, stream, sizeof(T) == 4 ? 2 : narrow_ctas());
   }
 }
