@@ -64,6 +64,14 @@ def parse():
     ap.add_argument("--workload", choices=("predict", "sweep", "ragged", "fit"), default="predict",
                     help="predict = cfg4 (driver default); sweep = cfg2 F sweep at 1M rows; "
                          "ragged = cfg3 32 size groups in one launch; fit = cfg5 1B x 128, C=16")
+    ap.add_argument("--flush", choices=("clean", "write"), default="clean",
+                    help="secondary workloads' L2 flush before each launch: write = 512 MB "
+                         "write only (leaves ~126 MB of dirty lines that the timed kernel "
+                         "then writes back); clean = the write followed by a 256 MB read "
+                         "of another buffer, so L2 holds only clean lines")
+    ap.add_argument("--pitch", choices=("packed", "line"), default="packed",
+                    help="sweep/ragged int32 row pitch: packed = 16-B multiple, line = "
+                         "128-B multiple (pad columns are never read)")
     return ap.parse_args()
 
 
@@ -465,17 +473,31 @@ def run_reference(args, world, rank):
 
 
 # ---------------------------------------------------------------- secondary workloads
+FLUSH_MODE = "clean"
+
+
+def _pitch(args, F):
+    """int32 row pitch (elements): 16-B multiple ("packed") or 128-B line ("line")."""
+    return (F + 31) // 32 * 32 if args.pitch == "line" else (F + 3) // 4 * 4
+
+
 def _timed_launches(fn, steps, warmup, flush_bytes=512 << 20):
     """Mean device time (ms) of fn() over `steps` launches, L2 flushed before each
-    (a 512 MB write, > 126 MB L2), CUDA events on the launching stream."""
+    (a 512 MB write, > 126 MB L2; in "clean" mode followed by a 256 MB read of a
+    second buffer so the flush's dirty lines are written back before the timed
+    region, not inside it), CUDA events on the launching stream."""
     import torch
     flush = torch.empty(flush_bytes // 4, dtype=torch.int32, device="cuda")
+    clean = torch.ones(flush_bytes // 8, dtype=torch.int32, device="cuda")
+    sink = torch.empty((), dtype=torch.int64, device="cuda")
     for _ in range(warmup):
         fn()
     times = []
     s = torch.cuda.current_stream()
     for _ in range(steps):
         flush.zero_()
+        if FLUSH_MODE == "clean":
+            torch.sum(clean, 0, out=sink)
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(s)
         fn()
@@ -496,7 +518,8 @@ def run_sweep(args, world, rank, local):
     peak, kind = peaks()
     rows = []
     for F in (50, 100, 200, 500, 1000):
-        x, size, lab = dense.generate(n, F, divergence=0.8, seed=0, device=dev)
+        x, size, lab = dense.generate(n, F, divergence=0.8, seed=0, device=dev,
+                                      ldx=_pitch(args, F))
         st = dense.fit_stats(x, size, lab, n_classes=2, group_size_bytes=5120,
                              max_size_bytes=5120)
         fin = dense.fin_train(st.sums.cpu().numpy(), st.counts.cpu().numpy(), k=F, alpha=1.0,
@@ -520,7 +543,7 @@ def run_sweep(args, world, rank, local):
                      "frac": round(n * bps / (mean_ms / 1e3) / 1e9 / peak, 4)})
         del x, size, lab, label, lp
     return {"metric": METRIC, "workload": "cfg2: F sweep at 1M samples, 2 classes, L2 flushed "
-            "before every launch", "unit": UNIT, "peak_gbs": peak, "peak_source": kind,
+            "before every launch", "flush": FLUSH_MODE, "pitch": args.pitch, "unit": UNIT, "peak_gbs": peak, "peak_source": kind,
             "bytes_per_sample": "4F+24", "rows": rows, "steps": args.steps}
 
 
@@ -538,7 +561,8 @@ def run_ragged(args, world, rank, local):
     counts = np.floor(N * w / w.sum()).astype(np.int64)
     counts[0] += N - counts.sum()
     width, limit = 5120, G * 5120
-    x, size, lab = dense.generate(N, V, group_rows=counts, divergence=0.8, seed=0, device=dev)
+    x, size, lab = dense.generate(N, V, group_rows=counts, divergence=0.8, seed=0, device=dev,
+                                  ldx=_pitch(args, V))
     st = dense.fit_stats(x, size, lab, n_classes=2, group_size_bytes=width, max_size_bytes=limit)
     fin = dense.fin_train(st.sums.cpu().numpy(), st.counts.cpu().numpy(), k=V, alpha=1.0,
                           min_per_class=6)
@@ -579,7 +603,7 @@ def run_ragged(args, world, rank, local):
     srt_ok = bool(torch.equal(lab_srt, label))
     return {"metric": METRIC, "workload": "cfg3: 4,194,304 samples, 32 ragged size groups "
             "(0.9^g), F=200, groups 5/8/17 untrained -> routed, single launch",
-            "unit": UNIT, "value": round(N / (mean_ms / 1e3), 1), "ms": round(mean_ms, 4),
+            "flush": FLUSH_MODE, "pitch": args.pitch, "unit": UNIT, "value": round(N / (mean_ms / 1e3), 1), "ms": round(mean_ms, 4),
             "achieved_gbs": round(N * bps / (mean_ms / 1e3) / 1e9, 1),
             "frac": round(N * bps / (mean_ms / 1e3) / 1e9 / peak, 4), "peak_gbs": peak,
             "trained_groups": len(trained), "bit_exact_subsample_vs_oracle": ok,
@@ -657,7 +681,9 @@ def run_fit(args, world, rank, local):
 
 
 def main():
+    global FLUSH_MODE
     args = parse()
+    FLUSH_MODE = args.flush
     world, rank, local = dist_init(args)
     if args.impl == "reference":
         out = run_reference(args, world, rank)

@@ -82,7 +82,8 @@ namespace gnb {
 // boxes of 32 columns x box_rows rows.  swizzle128: SWIZZLE_128B (predict)
 // or none (fit).
 static bool encode_map(CUtensorMap* map, const void* base, int64_t n_rows, int32_t n_cols,
-                       int64_t ldx, int box_rows, bool swizzle128, int x_type = GNB_X_I32) {
+                       int64_t ldx, int box_rows, bool swizzle128, int x_type = GNB_X_I32,
+                       int box_cols = 0) {
   auto fn = encode_fn();
   if (fn == nullptr) return false;
   const int eb = elem_bytes(x_type);
@@ -91,7 +92,7 @@ static bool encode_map(CUtensorMap* map, const void* base, int64_t n_rows, int32
                                                        : CU_TENSOR_MAP_DATA_TYPE_INT32;
   cuuint64_t dims[2] = {static_cast<cuuint64_t>(n_cols), static_cast<cuuint64_t>(n_rows)};
   cuuint64_t strides[1] = {static_cast<cuuint64_t>(ldx) * eb};
-  cuuint32_t box[2] = {static_cast<cuuint32_t>(kChunkBytesPerRow / eb),
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(box_cols > 0 ? box_cols : kChunkBytesPerRow / eb),
                        static_cast<cuuint32_t>(box_rows)};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = fn(map, dt, 2, const_cast<void*>(base), dims, strides,
@@ -195,9 +196,15 @@ static int predict_device(const void* x, int x_type, int64_t n_rows, int32_t F, 
     CUtensorMap map;
     const CUtensorMap* mp = nullptr;
     if (use_tma) {
-      // gather mode: box height 1 (tile::gather4 loads 4 rows per instruction)
-      if (!encode_map(&map, p.x, n, F, ldx, perm ? 1 : predict_box_rows(C), true, x_type))
-        return fail(GNB_ECUDA, "predict: cuTensorMapEncodeTiled failed");
+      // row-box mode (short rows): whole rows per box, unswizzled; gather mode:
+      // box height 1 (tile::gather4 loads 4 rows per instruction)
+      const int wq = perm ? 0 : predict_rowbox_quads(F, x_type, C);
+      const bool ok = wq > 0 ? encode_map(&map, p.x, n, F, ldx, kRowBoxRows, false, x_type,
+                                          wq * 16 / eb)
+                             : encode_map(&map, p.x, n, F, ldx, perm ? 1 : predict_box_rows(C),
+                                          true, x_type);
+      if (!ok) return fail(GNB_ECUDA, "predict: cuTensorMapEncodeTiled failed");
+      p.rowbox_quads = wq;
       mp = &map;
     }
     GNB_CUDA(predict_launch(mp, p, stream, force_generic), "predict launch");

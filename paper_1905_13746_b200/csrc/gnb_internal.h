@@ -31,6 +31,8 @@ struct PredictParams {
   int64_t n_tiles;  // set by predict_launch
   int32_t x_policy; // 0 evict_normal (default), 1 evict_first
   const int32_t* perm;  // nullable: rows in routed-slot order (gather mode)
+  int32_t rowbox_quads;  // > 0: row-box mode, smem row = this many 16-B quads (odd)
+  int32_t rowbox_stages; // row-box ring depth, set by predict_launch
 };
 
 struct FitParams {
@@ -58,6 +60,10 @@ cudaError_t pack_tables(const double* log_prior, const double* log_lik, int S, i
                         void* packed, cudaStream_t stream);
 // map == nullptr (or force_generic) selects the L1 path that accepts any ldx.
 int predict_box_rows(int n_classes);  // TMA box height of the K-PRED variant
+// Row-box mode (short rows): quads per box row, 0 when the shape does not use it.
+// The box is then {quads * 16 / elem_bytes columns, kRowBoxRows rows}, no swizzle.
+int predict_rowbox_quads(int n_features, int x_type, int n_classes);
+constexpr int kRowBoxRows = 128;
 cudaError_t predict_launch(const CUtensorMap* map, PredictParams p, cudaStream_t stream,
                            int force_generic);
 int fit_box_rows(int x_type);  // TMA box height of K-FIT tiles

@@ -420,6 +420,183 @@ __global__ void __launch_bounds__((NW + 1) * 32)
   }
 }
 
+// ------------------------------------------------------------------ row-box kernel
+// Short rows (F <= ~100 int32 features): one TMA box holds kRowBoxRows whole
+// rows, unswizzled, WQ 16-B quads per smem row with WQ odd so the 8 lanes of an
+// LDS.128 phase (consecutive rows, stride WQ*16 B) hit 8 distinct bank groups.
+// One stage per tile, no partial 128-B chunks: the 128-B-box kernel above
+// spends a whole 16-KB stage on e.g. the 18 trailing features of F=50, so short
+// rows kept too few bytes in flight per SM.  Ring depth and CTAs per SM follow
+// the box size (predict_launch).  Same arithmetic and order as every path.
+struct RowBoxSmem {
+  uint32_t x_bytes, tab_bytes, hdr_bytes, x, tab, hdr, sizes, bar, total;
+  // ahead: tiles whose row sizes are in flight ahead of routing
+  __host__ __device__ RowBoxSmem(int wq, int tab_feats, int cp, int stages, int ahead) {
+    x_bytes = static_cast<uint32_t>(kRowBoxRows) * wq * 16;
+    tab_bytes = static_cast<uint32_t>(tab_feats) * cp * 8;
+    hdr_bytes = (4 + kRowBoxRows * 4 + 15) / 16 * 16;
+    x = 0;
+    tab = x + stages * x_bytes;
+    hdr = tab + stages * tab_bytes;
+    sizes = hdr + stages * hdr_bytes;  // [ahead][kRowBoxRows] prefetched sizes
+    bar = sizes + ahead * kRowBoxRows * 4;
+    total = bar + 2 * stages * 8;
+  }
+};
+
+__host__ __device__ inline int rowbox_tab_feats(int F, int EQ, int n_tab_blocks) {
+  const int nq = (F + EQ - 1) / EQ;
+  const int want = nq * EQ, have = n_tab_blocks * kTabBlockFeatures;
+  return want < have ? want : have;
+}
+
+template <int CP, typename T, int kRowBoxAhead>
+__global__ void __launch_bounds__(5 * 32)
+    predict_rowbox_kernel(const __grid_constant__ CUtensorMap xmap, const PredictParams p) {
+  constexpr int NW = 4, ROWS = kRowBoxRows, EQ = Elem<T>::kPerQuad;
+  static_assert(ROWS == NW * 32, "one row per consumer thread");
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
+  const int ST = p.rowbox_stages, WQ = p.rowbox_quads;
+  const int tab_feats = rowbox_tab_feats(p.n_features, EQ, p.n_tab_blocks);
+  const RowBoxSmem L(WQ, tab_feats, CP, ST, kRowBoxAhead);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.bar);
+  uint64_t* empty = full + ST;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < ST; ++s) {
+      mbar_init(&full[s], 32);
+      mbar_init(&empty[s], NW);
+    }
+    mbar_fence_init();
+  }
+  if (warp == NW && lane == 0) prefetch_tensormap(&xmap);
+  __syncthreads();
+  const int64_t n_tiles = p.n_tiles;
+  const int64_t slot_tab = static_cast<int64_t>(p.n_tab_blocks) * kTabBlockFeatures * CP;
+
+  if (warp == NW) {
+    // ---------------------------------------------------------- producer
+    const uint64_t pol_x = p.x_policy == 1 ? policy_evict_first() : policy_evict_normal();
+    const uint64_t pol_t = policy_evict_last();
+    int stage = 0;
+    uint32_t phase = 0;
+    // Row sizes travel kRowBoxAhead tiles ahead of routing (LDGSTS into a
+    // smem ring, each lane reading back only its own entries): with one stage
+    // per tile, a size load per tile on the critical path capped the rate at
+    // one tile per loaded-HBM round trip.
+    int* szr = reinterpret_cast<int*>(smem + L.sizes);
+    auto fetch_sizes = [&](int64_t tile, int k) {
+      if (tile < n_tiles) {
+#pragma unroll
+        for (int i = 0; i < ROWS / 32; ++i) {
+          const int64_t r = tile * ROWS + lane + 32 * i;
+          cp_async4(szr + k * ROWS + lane + 32 * i, p.size + (r < p.n_rows ? r : p.n_rows - 1));
+        }
+      }
+      cp_async_commit();
+    };
+#pragma unroll
+    for (int k = 0; k < kRowBoxAhead; ++k) fetch_sizes(blockIdx.x + int64_t(k) * gridDim.x, k);
+    int k_cur = 0;
+    for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+      const int64_t r0 = tile * ROWS;
+      int slots[ROWS / 32];
+      int lo = INT_MAX, hi = INT_MIN;
+      cp_async_wait<kRowBoxAhead - 1>();
+#pragma unroll
+      for (int i = 0; i < ROWS / 32; ++i) {
+        const int64_t r = r0 + lane + 32 * i;
+        const int sz = szr[k_cur * ROWS + lane + 32 * i];
+        int s = -1;
+        if (r < p.n_rows && sz >= 0 && sz < p.limit) {
+          s = __ldg(p.route + sz / p.width);
+          lo = min(lo, s);
+          hi = max(hi, s);
+        }
+        slots[i] = s;
+      }
+      fetch_sizes(tile + int64_t(kRowBoxAhead) * gridDim.x, k_cur);
+      if (++k_cur == kRowBoxAhead) k_cur = 0;
+      lo = __reduce_min_sync(0xffffffffu, lo);
+      hi = __reduce_max_sync(0xffffffffu, hi);
+      const int tile_slot = (lo == INT_MAX) ? 0 : (lo == hi ? lo : -1);
+      mbar_wait(&empty[stage], phase ^ 1);
+      int* hdr = reinterpret_cast<int*>(smem + L.hdr + stage * L.hdr_bytes);
+#pragma unroll
+      for (int i = 0; i < ROWS / 32; ++i) hdr[1 + lane + 32 * i] = slots[i];
+      if (lane == 0) hdr[0] = tile_slot;
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive_expect_tx(&full[stage], L.x_bytes + (tile_slot >= 0 ? L.tab_bytes : 0));
+        tma_load_2d(smem + L.x + stage * L.x_bytes, &xmap, 0, static_cast<int32_t>(r0),
+                    &full[stage], pol_x);
+        if (tile_slot >= 0)
+          bulk_load(smem + L.tab + stage * L.tab_bytes, p.tab + tile_slot * slot_tab,
+                    L.tab_bytes, &full[stage], pol_t);
+      } else {
+        mbar_arrive(&full[stage]);
+      }
+      if (++stage == ST) {
+        stage = 0;
+        phase ^= 1;
+      }
+    }
+  } else {
+    // ---------------------------------------------------------- consumers
+    const int row = lane + 32 * warp;
+    const int nq = (p.n_features + EQ - 1) / EQ;
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+      mbar_wait(&full[stage], phase);
+      const int* hdr = reinterpret_cast<const int*>(smem + L.hdr + stage * L.hdr_bytes);
+      const int ts = hdr[0];
+      const int slot = hdr[1 + row];
+      const int s = ts >= 0 ? ts : max(slot, 0);
+      double acc[CP];
+#pragma unroll
+      for (int c = 0; c < CP; ++c) acc[c] = __ldg(p.prior + s * CP + c);
+      uint32_t neg = 0;
+      const uint8_t* xrow = smem + L.x + stage * L.x_bytes + row * (WQ * 16);
+      if (ts >= 0) {
+        const double* tab = reinterpret_cast<const double*>(smem + L.tab + stage * L.tab_bytes);
+#pragma unroll 2
+        for (int q = 0; q < nq; ++q) {
+          const uint4 v = *reinterpret_cast<const uint4*>(xrow + 16 * q);
+          if (Elem<T>::kSigned) neg |= v.x | v.y | v.z | v.w;
+#pragma unroll
+          for (int e = 0; e < EQ; ++e) {
+            const double xd = converted<T>(v, e);
+#pragma unroll
+            for (int c = 0; c < CP; c += 2) {  // broadcast LDS.128 per 2 classes
+              const double2 t2 = *reinterpret_cast<const double2*>(tab + (EQ * q + e) * CP + c);
+              acc[c] = __dadd_rn(acc[c], __dmul_rn(xd, t2.x));
+              acc[c + 1] = __dadd_rn(acc[c + 1], __dmul_rn(xd, t2.y));
+            }
+          }
+        }
+      } else {
+        const GlobalTab tab{p.tab + s * slot_tab};
+#pragma unroll 1
+        for (int q = 0; q < nq; ++q) {
+          const uint4 v = *reinterpret_cast<const uint4*>(xrow + 16 * q);
+          if (Elem<T>::kSigned) neg |= v.x | v.y | v.z | v.w;
+          score_quad<CP, T>(acc, v, tab, EQ * q);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[stage]);
+      if (++stage == ST) {
+        stage = 0;
+        phase ^= 1;
+      }
+      const int64_t r = tile * ROWS + row;
+      if (r < p.n_rows) write_row<CP>(p, r, slot, neg, acc);
+    }
+  }
+}
+
 // ------------------------------------------------------------------ generic kernel
 // Any layout (unaligned X, row pitch not a multiple of 16 B): one thread per
 // row, loads through L1.  Same arithmetic, same results; slower.
@@ -483,6 +660,77 @@ static cudaError_t launch_tma(const CUtensorMap& map, const PredictParams& p,
                            : launch_tma_mode<CP, T, R, NW, STAGES, false>(map, p, stream);
 }
 
+// Row-box eligibility: whole rows of <= kRowBoxMaxQuads 16-B quads (odd-padded)
+// and at most 256 box columns (TMA limit).  GNB_PRED_ROWBOX=0 disables (A/B).
+constexpr int kRowBoxMaxQuads = 26;       // 128 rows x 26 x 16 B = 52 KB per stage
+constexpr uint32_t kRowBoxRingBytes = 53248;  // ring depth: stages x box ~ 52 KB
+
+int predict_rowbox_quads(int n_features, int x_type, int n_classes) {
+  static int enabled = -1;
+  if (enabled < 0) {
+    const char* e = getenv("GNB_PRED_ROWBOX");
+    enabled = e ? atoi(e) != 0 : 1;
+  }
+  (void)n_classes;
+  if (!enabled || n_features < 1) return 0;
+  const int eb = x_type == GNB_X_U8 ? 1 : x_type == GNB_X_U16 ? 2 : 4;
+  const int nq = (n_features * eb + 15) / 16;
+  const int wq = nq | 1;
+  if (wq > kRowBoxMaxQuads || wq * 16 / eb > 256) return 0;
+  return wq;
+}
+
+template <int CP, typename T, int AHEAD>
+static cudaError_t launch_rowbox_a(const CUtensorMap& map, PredictParams p, cudaStream_t stream) {
+  auto kern = predict_rowbox_kernel<CP, T, AHEAD>;
+  static int sms = 0;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         227 * 1024);
+    if (e != cudaSuccess) return e;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    attr = true;
+  }
+  p.n_tiles = (p.n_rows + kRowBoxRows - 1) / kRowBoxRows;
+  const uint32_t box = static_cast<uint32_t>(kRowBoxRows) * p.rowbox_quads * 16;
+  int st = static_cast<int>(kRowBoxRingBytes / box);
+  static int st_env = -1;
+  if (st_env < 0) {
+    const char* e = getenv("GNB_ROWBOX_STAGES");
+    st_env = e ? atoi(e) : 0;
+  }
+  if (st_env > 0) st = st_env;
+  p.rowbox_stages = st < 2 ? 2 : st > 8 ? 8 : st;
+  const RowBoxSmem L(p.rowbox_quads,
+                     rowbox_tab_feats(p.n_features, Elem<T>::kPerQuad, p.n_tab_blocks), CP,
+                     p.rowbox_stages, AHEAD);
+  const size_t smem = L.total + 128;
+  int per_sm = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 5 * 32, smem);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) return cudaErrorInvalidConfiguration;
+  const int64_t want = static_cast<int64_t>(sms) * per_sm;
+  const int grid = static_cast<int>(p.n_tiles < want ? p.n_tiles : want);
+  if (grid == 0) return cudaSuccess;
+  kern<<<grid, 5 * 32, smem, stream>>>(map, p);
+  return cudaGetLastError();
+}
+
+template <int CP, typename T>
+static cudaError_t launch_rowbox(const CUtensorMap& map, const PredictParams& p,
+                                 cudaStream_t stream) {
+  static int ahead = -1;  // GNB_ROWBOX_AHEAD=4: deeper size prefetch (A/B)
+  if (ahead < 0) {
+    const char* e = getenv("GNB_ROWBOX_AHEAD");
+    ahead = e ? atoi(e) : 2;
+  }
+  return ahead == 4 ? launch_rowbox_a<CP, T, 4>(map, p, stream)
+                    : launch_rowbox_a<CP, T, 2>(map, p, stream);
+}
+
 template <int CP, typename T>
 static cudaError_t launch_generic(const PredictParams& p, cudaStream_t stream) {
   const int64_t blocks64 = (p.n_rows + 255) / 256;
@@ -544,6 +792,14 @@ int predict_box_rows(int n_classes) {
 template <typename T>
 static cudaError_t launch_typed(const CUtensorMap* map, const PredictParams& p, int CP,
                                 cudaStream_t stream) {
+  if (map != nullptr && p.rowbox_quads > 0 && p.perm == nullptr) {
+    switch (CP) {
+      case 2: return launch_rowbox<2, T>(*map, p, stream);
+      case 4: return launch_rowbox<4, T>(*map, p, stream);
+      case 8: return launch_rowbox<8, T>(*map, p, stream);
+      default: return launch_rowbox<16, T>(*map, p, stream);
+    }
+  }
   if (map != nullptr) {
     switch (CP) {
       case 2:
