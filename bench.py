@@ -315,12 +315,19 @@ def run_ours(args, world, rank, local):
     achieved = n * bytes_per_sample / (mean_launch_ms / 1e3) / 1e9
     peak, peak_kind = peaks()
     tps, ncu = ncu_traffic()
+    # the committed capture is of cfg4 (int32, F=256, C=2): per-sample traffic
+    # carries over to any row count of that shape, not to other shapes
+    if not (F == 256 and eb == 4):
+        tps, ncu = None, None
+    wq = ((F * eb + 15) // 16) | 1
+    kernel = ("gnb::predict_rowbox_kernel<2,T,2>" if wq <= 26 and wq * 16 // eb <= 256
+              else "gnb::predict_tma_kernel<2,T,1,4,2>")
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "peak_source": peak_kind,
                 "traffic": round(tps * n) if tps else None,
                 "algorithmic_bytes_per_launch": n * bytes_per_sample,
                 "bytes_per_sample": f"{eb}F+4+{out_bytes} = {bytes_per_sample}",
-                "kernel": "gnb::predict_tma_kernel<2,1,4,2>"}
+                "kernel": kernel}
     if ncu:
         roofline["traffic_source"] = ncu.get("source")
 
