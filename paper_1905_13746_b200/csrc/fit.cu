@@ -61,7 +61,7 @@ struct FitHdr {
   int2 runs[ROWS];  // {key, start | len << 16}
 };
 
-template <typename T, int NW, int STAGES, int BX>
+template <typename T, int NW, int STAGES, int BX, int NP = 1>
 struct FitSmem {
   using Geo = FitGeom<T, BX>;
   using Hdr = FitHdr<Geo::kRows>;
@@ -70,7 +70,7 @@ struct FitSmem {
   static constexpr int kX = 0;
   static constexpr int kHdr = kX + STAGES * kStage;
   static constexpr int kScratch = kHdr + STAGES * static_cast<int>(sizeof(Hdr));
-  static constexpr int kBar = kScratch + static_cast<int>(sizeof(Hdr));
+  static constexpr int kBar = kScratch + NP * static_cast<int>(sizeof(Hdr));
   static constexpr int kPart = (kBar + 2 * STAGES * 8 + 15) / 16 * 16;
   static constexpr int kFixed = kPart + 1024;  // + alignment slack
 };
@@ -113,10 +113,20 @@ __device__ __forceinline__ void load_lane(const uint8_t* at, uint32_t (&x)[CPL])
   }
 }
 
-template <typename T, int NW, int STAGES, int BX>
-__global__ void __launch_bounds__((NW + 1) * 32)
+// NP producer warps (1 or 2) sort alternate tiles; their latency-bound sorts
+// overlap, and a pair of named barriers keeps the stage issue in tile order
+// (mbarrier parity waits must never run two phases ahead).
+__device__ __forceinline__ void named_sync(int id) {
+  asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory");
+}
+__device__ __forceinline__ void named_arrive(int id) {
+  asm volatile("bar.arrive %0, 64;" ::"r"(id) : "memory");
+}
+
+template <typename T, int NW, int STAGES, int BX, int NP>
+__global__ void __launch_bounds__((NW + NP) * 32, 2)
     fit_tma_kernel(const __grid_constant__ CUtensorMap xmap, const FitParams p) {
-  using L = FitSmem<T, NW, STAGES, BX>;
+  using L = FitSmem<T, NW, STAGES, BX, NP>;
   using Geo = typename L::Geo;
   using FitHdrT = typename L::Hdr;
   constexpr int kGroupCols = Geo::kGroupCols;
@@ -138,11 +148,13 @@ __global__ void __launch_bounds__((NW + 1) * 32)
   const int nthreads = blockDim.x;
   const int64_t part_words = static_cast<int64_t>(KS) * Vp * (p.sumsq ? 2 : 1) + KS;
   for (int64_t i = threadIdx.x; i < part_words; i += nthreads) part_s[i] = 0ull;
-  // histogram sort scratch after the partials: hist[HK], kstart[HK]
+  // histogram sort scratch after the partials: per producer hist[HK], kstart[HK]
   const int HK = p.n_keys <= kMaxHistKeys ? p.n_keys : 0;
-  int* hist = reinterpret_cast<int*>(part_n + KS);
+  const int pid = warp >= NW ? warp - NW : 0;
+  int* hist = reinterpret_cast<int*>(part_n + KS) + pid * 2 * HK;
   int* kstart = hist + HK;
-  for (int i = threadIdx.x; i < HK; i += nthreads) hist[i] = 0;
+  for (int i = threadIdx.x; i < NP * 2 * HK; i += nthreads)
+    reinterpret_cast<int*>(part_n + KS)[i] = 0;
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 32);
@@ -152,12 +164,12 @@ __global__ void __launch_bounds__((NW + 1) * 32)
   }
   __syncthreads();
 
-  if (warp == NW) {
-    // ------------------------------------------------------------ producer
+  if (warp >= NW) {
+    // ------------------------------------------------------------ producer(s)
     const uint64_t pol_x = policy_evict_normal();
-    FitHdrT* scratch = reinterpret_cast<FitHdrT*>(smem + L::kScratch);
-    int stage = 0;
-    uint32_t phase = 0;
+    FitHdrT* scratch = reinterpret_cast<FitHdrT*>(smem + L::kScratch + pid * sizeof(FitHdrT));
+    const int64_t my_iters =
+        blockIdx.x < p.n_tiles ? (p.n_tiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
     unsigned long long bad_label = 0, out_of_range = 0;
     const uint32_t lt = (1u << lane) - 1u;
     const bool hist_sort = HK > 0;
@@ -174,8 +186,9 @@ __global__ void __launch_bounds__((NW + 1) * 32)
       }
     };
     int nsz[kKeysPerLane], nlab[kKeysPerLane];
-    load_raw(blockIdx.x, nsz, nlab);
-    for (int64_t tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
+    load_raw(blockIdx.x + int64_t(pid) * gridDim.x, nsz, nlab);
+    for (int64_t it = pid; it < my_iters; it += NP) {
+      const int64_t tile = blockIdx.x + it * gridDim.x;
       const int64_t r0 = tile * kFitRows;
       int key[kKeysPerLane];
 #pragma unroll
@@ -192,7 +205,7 @@ __global__ void __launch_bounds__((NW + 1) * 32)
           ++out_of_range;
         }
       }
-      load_raw(tile + gridDim.x, nsz, nlab);  // prefetch
+      load_raw(tile + int64_t(NP) * gridDim.x, nsz, nlab);  // prefetch
       int n_runs = 0;
       if (hist_sort) {
         // counting sort through a shared histogram: per key slot, lanes with
@@ -244,8 +257,12 @@ __global__ void __launch_bounds__((NW + 1) * 32)
 #pragma unroll
         for (int i = 0; i < kKeysPerLane; ++i) {
           if (kk[i] >= 0) {
-            if (kk[i] < KS) part_n[kk[i]] += static_cast<unsigned long long>(cnt[i]);
-            else atomicAdd(p.counts + kk[i], static_cast<double>(cnt[i]));
+            if (kk[i] < KS) {
+              if (NP == 1) part_n[kk[i]] += static_cast<unsigned long long>(cnt[i]);
+              else atomicAdd(part_n + kk[i], static_cast<unsigned long long>(cnt[i]));
+            } else {
+              atomicAdd(p.counts + kk[i], static_cast<double>(cnt[i]));
+            }
             hist[kk[i]] = 0;
           }
         }
@@ -276,8 +293,12 @@ __global__ void __launch_bounds__((NW + 1) * 32)
           }
           if (lane == 0) {
             scratch->runs[n_runs] = make_int2(k, pos | (len << 16));
-            if (k < KS) part_n[k] += static_cast<unsigned long long>(len);
-            else atomicAdd(p.counts + k, static_cast<double>(len));
+            if (k < KS) {
+              if (NP == 1) part_n[k] += static_cast<unsigned long long>(len);
+              else atomicAdd(part_n + k, static_cast<unsigned long long>(len));
+            } else {
+              atomicAdd(p.counts + k, static_cast<double>(len));
+            }
           }
           pos += len;
           ++n_runs;
@@ -285,7 +306,11 @@ __global__ void __launch_bounds__((NW + 1) * 32)
       }
       __syncwarp();
       const int hdr_words = (16 + kFitRows + n_runs * 8 + 15) / 16;  // 16-B units
-      for (int cg = 0; cg < NG; ++cg) {
+      if (NP > 1 && it > 0) named_sync(1 + ((it - 1) & 1));  // tile it-1 issued
+      int64_t g = it * NG;  // global stage sequence number of this tile's first chunk
+      for (int cg = 0; cg < NG; ++cg, ++g) {
+        const int stage = static_cast<int>(g % STAGES);
+        const uint32_t phase = static_cast<uint32_t>(g / STAGES) & 1u;
         mbar_wait(&empty[stage], phase ^ 1);
         FitHdrT* hdr = reinterpret_cast<FitHdrT*>(smem + L::kHdr + stage * sizeof(FitHdrT));
         const int4* src4 = reinterpret_cast<const int4*>(scratch);
@@ -304,12 +329,9 @@ __global__ void __launch_bounds__((NW + 1) * 32)
         } else {
           mbar_arrive(&full[stage]);
         }
-        if (++stage == STAGES) {
-          stage = 0;
-          phase ^= 1;
-        }
       }
       __syncwarp();
+      if (NP > 1 && it + 1 < my_iters) named_arrive(1 + (it & 1));
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -419,11 +441,11 @@ __global__ void __launch_bounds__((NW + 1) * 32)
     if (part_n[k]) atomicAdd(p.counts + k, static_cast<double>(part_n[k]));
 }
 
-template <typename T, int NW, int STAGES, int BX = (sizeof(T) == 4 ? 2 : 1)>
-static cudaError_t launch_fit(const CUtensorMap& map, FitParams p, cudaStream_t stream,
-                              int ctas_per_sm) {
-  using L = FitSmem<T, NW, STAGES, BX>;
-  auto kern = fit_tma_kernel<T, NW, STAGES, BX>;
+template <typename T, int NW, int STAGES, int BX, int NP>
+static cudaError_t launch_fit_np(const CUtensorMap& map, FitParams p, cudaStream_t stream,
+                                 int ctas_per_sm) {
+  using L = FitSmem<T, NW, STAGES, BX, NP>;
+  auto kern = fit_tma_kernel<T, NW, STAGES, BX, NP>;
   constexpr int kGroupCols = L::Geo::kGroupCols;
   p.n_chunks = (p.n_cols + kGroupCols - 1) / kGroupCols;
   int dev = 0, sms = 0, max_smem = 0;
@@ -432,7 +454,7 @@ static cudaError_t launch_fit(const CUtensorMap& map, FitParams p, cudaStream_t 
   cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   const int Vp = p.n_chunks * kGroupCols;
   const int per_key = Vp * 8 * (p.sumsq ? 2 : 1) + 8;
-  const int hist_bytes = p.n_keys <= kMaxHistKeys ? 8 * p.n_keys : 0;
+  const int hist_bytes = p.n_keys <= kMaxHistKeys ? 8 * NP * p.n_keys : 0;
   // Partials sized so `ctas_per_sm` CTAs share an SM; keys beyond the cap
   // (large group counts) accumulate per run in global memory.
   const int budget = (max_smem + 1024) / ctas_per_sm - 1024 - L::kFixed - hist_bytes;
@@ -445,14 +467,36 @@ static cudaError_t launch_fit(const CUtensorMap& map, FitParams p, cudaStream_t 
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   int per_sm = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, (NW + 1) * 32, smem);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, (NW + NP) * 32, smem);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) per_sm = 1;
   const int64_t want = static_cast<int64_t>(sms) * per_sm;
   const int grid = static_cast<int>(p.n_tiles < want ? p.n_tiles : want);
   if (grid == 0) return cudaSuccess;
-  kern<<<grid, (NW + 1) * 32, smem, stream>>>(map, p);
+  kern<<<grid, (NW + NP) * 32, smem, stream>>>(map, p);
   return cudaGetLastError();
+}
+
+// Producer warps per CTA: 2 unless GNB_FIT_NP=1 (A/B).  One producer warp's
+// sort is a latency-bound dependent chain (~7k cycles per 128-row tile under
+// load) that capped K-FIT at ~85 % of HBM with int32 rows (profiles/).
+static int fit_producers() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("GNB_FIT_NP");
+    v = e ? atoi(e) : 2;
+    if (v != 1) v = 2;
+  }
+  return v;
+}
+
+template <typename T, int NW, int STAGES, int BX = (sizeof(T) == 4 ? 2 : 1)>
+static cudaError_t launch_fit(const CUtensorMap& map, const FitParams& p, cudaStream_t stream,
+                              int ctas_per_sm) {
+  // large key spaces keep one producer (per-producer histograms double)
+  if (fit_producers() == 2 && p.n_keys <= 1024)
+    return launch_fit_np<T, NW, STAGES, BX, 2>(map, p, stream, ctas_per_sm);
+  return launch_fit_np<T, NW, STAGES, BX, 1>(map, p, stream, ctas_per_sm);
 }
 
 int fit_box_rows(int x_type) {
