@@ -548,7 +548,8 @@ static cudaError_t launch_fit_typed(const CUtensorMap& map, const FitParams& p,
   }
   // 8 consumer warps pay off for int32 rows (32-KB stages, consumer-bound); for
   // uint8/uint16 tiles the producer's sort is the limit (profiles/r01_tuning.md)
-  if (sizeof(T) == 4 && p.n_keys >= 8 && nw8) return launch_fit_nw<T, 8>(map, p, stream);
+  if ((sizeof(T) == 4 || nw8 == 2) && p.n_keys >= 8 && nw8)  // 2: any storage (A/B)
+    return launch_fit_nw<T, 8>(map, p, stream);
   if (p.n_keys >= 4) return launch_fit_nw<T, 4>(map, p, stream);
   if (p.n_keys >= 2) return launch_fit_nw<T, 2>(map, p, stream);
   return launch_fit_nw<T, 1>(map, p, stream);
