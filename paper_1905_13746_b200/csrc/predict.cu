@@ -174,11 +174,14 @@ __device__ __forceinline__ void write_row(const PredictParams& p, int64_t r, int
 // ------------------------------------------------------------------ TMA kernel
 // A consumer thread owns R rows of the tile (rows lane + 32*(w + NW*i)), so one
 // broadcast table read feeds R*CP independent accumulator chains.
-template <int CP, typename T, int R, int NW, int STAGES, bool GATHER = false>
+// A stage holds B consecutive 128-B column chunks of the tile (B boxes).
+template <int CP, typename T, int R, int NW, int STAGES, bool GATHER = false, int B = 1>
 struct PredictSmem {
   static constexpr int kRows = NW * 32 * R;                          // rows per tile (<= 256)
-  static constexpr int kXBytes = kRows * kChunkBytesPerRow;            // one box
-  static constexpr int kTabBytes = Elem<T>::kPerRow * CP * 8;          // one table slice
+  static constexpr int kBox = kRows * kChunkBytesPerRow;               // one box
+  static constexpr int kXBytes = B * kBox;                             // one stage
+  static constexpr int kTabChunk = Elem<T>::kPerRow * CP * 8;          // one chunk's table
+  static constexpr int kTabBytes = B * kTabChunk;                      // one stage's tables
   // tile_slot + row_slot[kRows] (+ row_id[kRows] in gather mode)
   static constexpr int kHdrBytes = ((4 + kRows * 4 * (GATHER ? 2 : 1)) + 15) / 16 * 16;
   static constexpr int kX = 0;
@@ -264,10 +267,11 @@ __device__ __forceinline__ void score_chunk_mixed(const PredictParams& p, double
 // slot_sort), loaded with TMA tile::gather4 (4 arbitrary rows per
 // instruction, one instruction per producer lane) into the same swizzled box
 // layout; outputs go back to the original row index.
-template <int CP, typename T, int R, int NW, int STAGES, bool GATHER>
+template <int CP, typename T, int R, int NW, int STAGES, bool GATHER, int B = 1>
 __global__ void __launch_bounds__((NW + 1) * 32)
     predict_tma_kernel(const __grid_constant__ CUtensorMap xmap, const PredictParams p) {
-  using L = PredictSmem<CP, T, R, NW, STAGES, GATHER>;
+  static_assert(!GATHER || B == 1, "gather mode stages one box");
+  using L = PredictSmem<CP, T, R, NW, STAGES, GATHER, B>;
   constexpr int ROWS = L::kRows;
   constexpr int CF = Elem<T>::kPerRow;
   constexpr int EQ = Elem<T>::kPerQuad;
@@ -289,6 +293,7 @@ __global__ void __launch_bounds__((NW + 1) * 32)
   __syncthreads();
 
   const int NCH = p.n_chunks;
+  const int NSC = (NCH + B - 1) / B;  // stages per tile
   const int64_t n_tiles = p.n_tiles;
 
   if (warp == NW) {
@@ -320,7 +325,9 @@ __global__ void __launch_bounds__((NW + 1) * 32)
       lo = __reduce_min_sync(0xffffffffu, lo);
       hi = __reduce_max_sync(0xffffffffu, hi);
       const int tile_slot = (lo == INT_MAX) ? 0 : (lo == hi ? lo : -1);
-      for (int ch = 0; ch < NCH; ++ch) {
+      for (int sc = 0; sc < NSC; ++sc) {
+        const int ch = sc * B;
+        const int nb = min(B, NCH - ch);
         mbar_wait(&empty[stage], phase ^ 1);
         StageHdr* hdr = reinterpret_cast<StageHdr*>(smem + L::kHdr + stage * L::kHdrBytes);
         if (ch == 0) {
@@ -334,13 +341,15 @@ __global__ void __launch_bounds__((NW + 1) * 32)
         __syncwarp();
         uint8_t* box = smem + L::kX + stage * L::kXBytes;
         if (lane == 0) {
-          const uint32_t bytes = L::kXBytes + (tile_slot >= 0 ? L::kTabBytes : 0);
+          const uint32_t bytes = nb * (L::kBox + (tile_slot >= 0 ? L::kTabChunk : 0));
           mbar_arrive_expect_tx(&full[stage], bytes);
           if (!GATHER)
-            tma_load_2d(box, &xmap, ch * CF, static_cast<int32_t>(r0), &full[stage], pol_x);
+            for (int b = 0; b < nb; ++b)
+              tma_load_2d(box + b * L::kBox, &xmap, (ch + b) * CF, static_cast<int32_t>(r0),
+                          &full[stage], pol_x);
           if (tile_slot >= 0)
             bulk_load(smem + L::kTab + stage * L::kTabBytes, chunk_table<CP, T>(p, tile_slot, ch),
-                      L::kTabBytes, &full[stage], pol_t);
+                      nb * L::kTabChunk, &full[stage], pol_t);
         }
         if (GATHER) {
           __syncwarp();  // expect_tx precedes every completion
@@ -375,12 +384,12 @@ __global__ void __launch_bounds__((NW + 1) * 32)
       uint32_t neg[R];
 #pragma unroll
       for (int i = 0; i < R; ++i) neg[i] = 0;
-      for (int ch = 0; ch < NCH; ++ch) {
+      for (int sc = 0; sc < NSC; ++sc) {
         mbar_wait(&full[stage], phase);
         const StageHdr* hdr =
             reinterpret_cast<const StageHdr*>(smem + L::kHdr + stage * L::kHdrBytes);
         const int ts = hdr->tile_slot;
-        if (ch == 0) {
+        if (sc == 0) {
 #pragma unroll
           for (int i = 0; i < R; ++i) {
             slot[i] = hdr->row_slot[rows[i]];
@@ -390,15 +399,22 @@ __global__ void __launch_bounds__((NW + 1) * 32)
             for (int c = 0; c < CP; ++c) acc[i][c] = __ldg(p.prior + s * CP + c);
           }
         }
-        const int nf = min(CF, p.n_features - ch * CF);
-        const int nq = (nf + EQ - 1) / EQ;
-        const uint8_t* box = smem + L::kX + stage * L::kXBytes;
-        if (ts >= 0) {
-          score_chunk_uniform<CP, T, R>(
-              acc, box, rows, reinterpret_cast<const double*>(smem + L::kTab + stage * L::kTabBytes),
-              nq, neg);
-        } else {
-          score_chunk_mixed<CP, T, R>(p, acc, box, rows, slot, ch, nq, neg);
+#pragma unroll
+        for (int b = 0; b < B; ++b) {
+          const int ch = sc * B + b;
+          if (B > 1 && ch >= NCH) break;
+          const int nf = min(CF, p.n_features - ch * CF);
+          const int nq = (nf + EQ - 1) / EQ;
+          const uint8_t* box = smem + L::kX + stage * L::kXBytes + b * L::kBox;
+          if (ts >= 0) {
+            score_chunk_uniform<CP, T, R>(
+                acc, box, rows,
+                reinterpret_cast<const double*>(smem + L::kTab + stage * L::kTabBytes +
+                                                b * L::kTabChunk),
+                nq, neg);
+          } else {
+            score_chunk_mixed<CP, T, R>(p, acc, box, rows, slot, ch, nq, neg);
+          }
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[stage]);
@@ -627,10 +643,10 @@ __global__ void __launch_bounds__(256) predict_generic_kernel(const PredictParam
 }
 
 // ------------------------------------------------------------------ launchers
-template <int CP, typename T, int R, int NW, int STAGES, bool GATHER>
+template <int CP, typename T, int R, int NW, int STAGES, bool GATHER, int B = 1>
 static cudaError_t launch_tma_mode(const CUtensorMap& map, PredictParams p, cudaStream_t stream) {
-  using L = PredictSmem<CP, T, R, NW, STAGES, GATHER>;
-  auto kern = predict_tma_kernel<CP, T, R, NW, STAGES, GATHER>;
+  using L = PredictSmem<CP, T, R, NW, STAGES, GATHER, B>;
+  auto kern = predict_tma_kernel<CP, T, R, NW, STAGES, GATHER, B>;
   p.n_tiles = (p.n_rows + L::kRows - 1) / L::kRows;
   p.n_chunks = (p.n_features + Elem<T>::kPerRow - 1) / Elem<T>::kPerRow;
   static int per_sm = 0;  // resident CTAs per SM for this instantiation
@@ -653,11 +669,11 @@ static cudaError_t launch_tma_mode(const CUtensorMap& map, PredictParams p, cuda
   return cudaGetLastError();
 }
 
-template <int CP, typename T, int R, int NW, int STAGES>
+template <int CP, typename T, int R, int NW, int STAGES, int B = 1>
 static cudaError_t launch_tma(const CUtensorMap& map, const PredictParams& p,
                               cudaStream_t stream) {
   return p.perm != nullptr ? launch_tma_mode<CP, T, R, NW, STAGES, true>(map, p, stream)
-                           : launch_tma_mode<CP, T, R, NW, STAGES, false>(map, p, stream);
+                           : launch_tma_mode<CP, T, R, NW, STAGES, false, B>(map, p, stream);
 }
 
 // Row-box eligibility: whole rows of <= kRowBoxMaxQuads 16-B quads (odd-padded)
@@ -768,7 +784,8 @@ cudaError_t pack_tables(const double* log_prior, const double* log_lik, int S, i
 struct PredVariant {
   int R, NW, STAGES;
 };
-static const PredVariant kCp2Variants[] = {{1, 4, 2}, {1, 4, 3}, {2, 2, 2}, {2, 4, 2}};
+static const PredVariant kCp2Variants[] = {{1, 4, 2}, {1, 4, 3}, {2, 2, 2}, {2, 4, 2},
+                                           {1, 4, 2}, {1, 4, 3}, {1, 4, 2}};  // 4-6: B=2,2,4
 
 static int cp2_variant() {
   static int v = -1;
@@ -807,7 +824,17 @@ static cudaError_t launch_typed(const CUtensorMap* map, const PredictParams& p, 
           case 1: return launch_tma<2, T, 1, 4, 3>(*map, p, stream);
           case 2: return launch_tma<2, T, 2, 2, 2>(*map, p, stream);
           case 3: return launch_tma<2, T, 2, 4, 2>(*map, p, stream);
-          default: return launch_tma<2, T, 1, 4, 2>(*map, p, stream);
+          case 4: return launch_tma<2, T, 1, 4, 2, 2>(*map, p, stream);
+          case 5: return launch_tma<2, T, 1, 4, 3, 2>(*map, p, stream);
+          case 6: return launch_tma<2, T, 1, 4, 2, 4>(*map, p, stream);
+          default: {
+            // long rows (>= 12 chunks, e.g. int32 F >= 353): 2 chunks per stage
+            // (3 CTAs/SM), F=500/1000 0.85/0.90 -> 0.91/0.96 of HBM; shorter
+            // rows keep 1-chunk stages (F=200: 0.89 vs 0.77), r01_tuning.md
+            const int nch = (p.n_features + Elem<T>::kPerRow - 1) / Elem<T>::kPerRow;
+            if (nch >= 12) return launch_tma<2, T, 1, 4, 2, 2>(*map, p, stream);
+            return launch_tma<2, T, 1, 4, 2>(*map, p, stream);
+          }
         }
       case 4: return launch_tma<4, T, 2, 4, 3>(*map, p, stream);
       case 8: return launch_tma<8, T, 1, 4, 4>(*map, p, stream);
