@@ -68,6 +68,18 @@ CUtensorMapL2promotion l2_promotion() {
   return static_cast<CUtensorMapL2promotion>(v);
 }
 
+// L2 promotion of the last chunk of gathered rows (GNB_GATHER_TAIL: -1 = same
+// map as the other chunks, else a CUtensorMapL2promotion value; default 0).
+int gather_tail_promo() {
+  static int v = -2;
+  if (v == -2) {
+    const char* e = getenv("GNB_GATHER_TAIL");
+    v = e ? atoi(e) : 0;
+    if (v < -1 || v > 3) v = 0;
+  }
+  return v;
+}
+
 int elem_bytes(int x_type) { return x_type == GNB_X_U8 ? 1 : x_type == GNB_X_U16 ? 2 : 4; }
 
 bool tma_ok(const void* base, int64_t ldx, int x_type = GNB_X_I32) {
@@ -83,7 +95,7 @@ namespace gnb {
 // or none (fit).
 static bool encode_map(CUtensorMap* map, const void* base, int64_t n_rows, int32_t n_cols,
                        int64_t ldx, int box_rows, bool swizzle128, int x_type = GNB_X_I32,
-                       int box_cols = 0) {
+                       int box_cols = 0, int promo = -1) {
   auto fn = encode_fn();
   if (fn == nullptr) return false;
   const int eb = elem_bytes(x_type);
@@ -98,7 +110,8 @@ static bool encode_map(CUtensorMap* map, const void* base, int64_t n_rows, int32
   CUresult r = fn(map, dt, 2, const_cast<void*>(base), dims, strides,
                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                   swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
-                  l2_promotion(), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                  promo >= 0 ? static_cast<CUtensorMapL2promotion>(promo) : l2_promotion(),
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
 
@@ -193,16 +206,19 @@ static int predict_device(const void* x, int x_type, int64_t n_rows, int32_t F, 
     p.label = label + r0;
     p.logpost = logpost ? logpost + r0 * C : nullptr;
     p.perm = use_tma ? perm : nullptr;  // the L1 kernel walks rows in order
-    CUtensorMap map;
-    const CUtensorMap* mp = nullptr;
+    PredictMaps map;
+    const PredictMaps* mp = nullptr;
     if (use_tma) {
       // row-box mode (short rows): whole rows per box, unswizzled; gather mode:
       // box height 1 (tile::gather4 loads 4 rows per instruction)
       const int wq = perm ? 0 : predict_rowbox_quads(F, x_type, C);
-      const bool ok = wq > 0 ? encode_map(&map, p.x, n, F, ldx, kRowBoxRows, false, x_type,
-                                          wq * 16 / eb)
-                             : encode_map(&map, p.x, n, F, ldx, perm ? 1 : predict_box_rows(C),
-                                          true, x_type);
+      bool ok = wq > 0 ? encode_map(&map.main, p.x, n, F, ldx, kRowBoxRows, false, x_type,
+                                    wq * 16 / eb)
+                       : encode_map(&map.main, p.x, n, F, ldx, perm ? 1 : predict_box_rows(C),
+                                    true, x_type);
+      map.tail = map.main;
+      if (ok && perm && gather_tail_promo() >= 0)
+        ok = encode_map(&map.tail, p.x, n, F, ldx, 1, true, x_type, 0, gather_tail_promo());
       if (!ok) return fail(GNB_ECUDA, "predict: cuTensorMapEncodeTiled failed");
       p.rowbox_quads = wq;
       mp = &map;

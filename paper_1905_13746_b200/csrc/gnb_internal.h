@@ -64,7 +64,14 @@ int predict_box_rows(int n_classes);  // TMA box height of the K-PRED variant
 // The box is then {quads * 16 / elem_bytes columns, kRowBoxRows rows}, no swizzle.
 int predict_rowbox_quads(int n_features, int x_type, int n_classes);
 constexpr int kRowBoxRows = 128;
-cudaError_t predict_launch(const CUtensorMap* map, PredictParams p, cudaStream_t stream,
+// K-PRED tensor maps: `main` for every chunk; `tail` for the last chunk of a
+// row in gather mode (encoded without L2 promotion, so a random row's last
+// partial chunk does not drag a 256-B block of its neighbour out of HBM).
+struct PredictMaps {
+  CUtensorMap main;
+  CUtensorMap tail;
+};
+cudaError_t predict_launch(const PredictMaps* maps, PredictParams p, cudaStream_t stream,
                            int force_generic);
 int fit_box_rows(int x_type);  // TMA box height of K-FIT tiles
 cudaError_t fit_launch(const CUtensorMap& map, FitParams p, cudaStream_t stream);

@@ -269,8 +269,8 @@ __device__ __forceinline__ void score_chunk_mixed(const PredictParams& p, double
 // layout; outputs go back to the original row index.
 template <int CP, typename T, int R, int NW, int STAGES, bool GATHER, int B = 1>
 __global__ void __launch_bounds__((NW + 1) * 32)
-    predict_tma_kernel(const __grid_constant__ CUtensorMap xmap, const PredictParams p) {
-  static_assert(!GATHER || B == 1, "gather mode stages one box");
+    predict_tma_kernel(const __grid_constant__ PredictMaps maps, const PredictParams p) {
+  const CUtensorMap& xmap = maps.main;
   using L = PredictSmem<CP, T, R, NW, STAGES, GATHER, B>;
   constexpr int ROWS = L::kRows;
   constexpr int CF = Elem<T>::kPerRow;
@@ -289,7 +289,10 @@ __global__ void __launch_bounds__((NW + 1) * 32)
     }
     mbar_fence_init();
   }
-  if (warp == NW && lane == 0) prefetch_tensormap(&xmap);
+  if (warp == NW && lane == 0) {
+    prefetch_tensormap(&xmap);
+    if (GATHER) prefetch_tensormap(&maps.tail);
+  }
   __syncthreads();
 
   const int NCH = p.n_chunks;
@@ -361,7 +364,10 @@ __global__ void __launch_bounds__((NW + 1) * 32)
               const int64_t pos = r0 + 4 * g + k;
               rr[k] = __ldg(p.perm + (pos < p.n_rows ? pos : p.n_rows - 1));
             }
-            tma_gather4(box + 4 * g * kChunkBytesPerRow, &xmap, ch * CF, rr, &full[stage]);
+            for (int b = 0; b < nb; ++b)
+              tma_gather4(box + b * L::kBox + 4 * g * kChunkBytesPerRow,
+                          ch + b == NCH - 1 ? &maps.tail : &xmap, (ch + b) * CF, rr,
+                          &full[stage]);
           }
         }
         if (lane != 0) mbar_arrive(&full[stage]);
@@ -468,7 +474,8 @@ __host__ __device__ inline int rowbox_tab_feats(int F, int EQ, int n_tab_blocks)
 
 template <int CP, typename T, int kRowBoxAhead>
 __global__ void __launch_bounds__(5 * 32)
-    predict_rowbox_kernel(const __grid_constant__ CUtensorMap xmap, const PredictParams p) {
+    predict_rowbox_kernel(const __grid_constant__ PredictMaps maps, const PredictParams p) {
+  const CUtensorMap& xmap = maps.main;
   constexpr int NW = 4, ROWS = kRowBoxRows, EQ = Elem<T>::kPerQuad;
   static_assert(ROWS == NW * 32, "one row per consumer thread");
   extern __shared__ uint8_t smem_raw[];
@@ -644,7 +651,7 @@ __global__ void __launch_bounds__(256) predict_generic_kernel(const PredictParam
 
 // ------------------------------------------------------------------ launchers
 template <int CP, typename T, int R, int NW, int STAGES, bool GATHER, int B = 1>
-static cudaError_t launch_tma_mode(const CUtensorMap& map, PredictParams p, cudaStream_t stream) {
+static cudaError_t launch_tma_mode(const PredictMaps& map, PredictParams p, cudaStream_t stream) {
   using L = PredictSmem<CP, T, R, NW, STAGES, GATHER, B>;
   auto kern = predict_tma_kernel<CP, T, R, NW, STAGES, GATHER, B>;
   p.n_tiles = (p.n_rows + L::kRows - 1) / L::kRows;
@@ -669,11 +676,23 @@ static cudaError_t launch_tma_mode(const CUtensorMap& map, PredictParams p, cuda
   return cudaGetLastError();
 }
 
+// Gather mode: GNB_GATHER_B=2 stages two chunks of each gathered row (A/B).
+static int gather_boxes() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("GNB_GATHER_B");
+    v = e ? atoi(e) : 1;
+  }
+  return v;
+}
+
 template <int CP, typename T, int R, int NW, int STAGES, int B = 1>
-static cudaError_t launch_tma(const CUtensorMap& map, const PredictParams& p,
+static cudaError_t launch_tma(const PredictMaps& map, const PredictParams& p,
                               cudaStream_t stream) {
-  return p.perm != nullptr ? launch_tma_mode<CP, T, R, NW, STAGES, true>(map, p, stream)
-                           : launch_tma_mode<CP, T, R, NW, STAGES, false, B>(map, p, stream);
+  if (p.perm != nullptr)
+    return gather_boxes() == 2 ? launch_tma_mode<CP, T, R, NW, STAGES, true, 2>(map, p, stream)
+                               : launch_tma_mode<CP, T, R, NW, STAGES, true, 1>(map, p, stream);
+  return launch_tma_mode<CP, T, R, NW, STAGES, false, B>(map, p, stream);
 }
 
 // Row-box eligibility: whole rows of <= kRowBoxMaxQuads 16-B quads (odd-padded)
@@ -697,7 +716,7 @@ int predict_rowbox_quads(int n_features, int x_type, int n_classes) {
 }
 
 template <int CP, typename T, int AHEAD>
-static cudaError_t launch_rowbox_a(const CUtensorMap& map, PredictParams p, cudaStream_t stream) {
+static cudaError_t launch_rowbox_a(const PredictMaps& map, PredictParams p, cudaStream_t stream) {
   auto kern = predict_rowbox_kernel<CP, T, AHEAD>;
   static int sms = 0;
   static bool attr = false;
@@ -736,7 +755,7 @@ static cudaError_t launch_rowbox_a(const CUtensorMap& map, PredictParams p, cuda
 }
 
 template <int CP, typename T>
-static cudaError_t launch_rowbox(const CUtensorMap& map, const PredictParams& p,
+static cudaError_t launch_rowbox(const PredictMaps& map, const PredictParams& p,
                                  cudaStream_t stream) {
   static int ahead = -1;  // GNB_ROWBOX_AHEAD=4: deeper size prefetch (A/B)
   if (ahead < 0) {
@@ -807,7 +826,7 @@ int predict_box_rows(int n_classes) {
 }
 
 template <typename T>
-static cudaError_t launch_typed(const CUtensorMap* map, const PredictParams& p, int CP,
+static cudaError_t launch_typed(const PredictMaps* map, const PredictParams& p, int CP,
                                 cudaStream_t stream) {
   if (map != nullptr && p.rowbox_quads > 0 && p.perm == nullptr) {
     switch (CP) {
@@ -849,7 +868,7 @@ static cudaError_t launch_typed(const CUtensorMap* map, const PredictParams& p, 
   }
 }
 
-cudaError_t predict_launch(const CUtensorMap* map, PredictParams p, cudaStream_t stream,
+cudaError_t predict_launch(const PredictMaps* map, PredictParams p, cudaStream_t stream,
                            int force_generic) {
   const int CP = class_pad(p.n_classes);
   static int x_policy = -1;  // GNB_X_POLICY=1: X loads evict_first (profiling; default normal)
