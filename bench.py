@@ -56,6 +56,9 @@ def parse():
     ap.add_argument("--fit-rows", type=int, default=1_000_000_000)
     ap.add_argument("--ref-rows", type=int, default=2_000_000,
                     help="CPU reference arm: rows scored per step (bounded sample)")
+    ap.add_argument("--ref-py-samples", type=int, default=20_000,
+                    help="reference arm: samples for the unmodified Python reference "
+                         "(classify_sequential / classify_parallel); 0 skips it")
     ap.add_argument("--dist-backend", choices=("nccl", "gloo"), default="nccl",
                     help="gloo: exercise the multi-rank path with ranks sharing one GPU "
                          "(host-side collectives only; testing, not a bench number)")
@@ -73,6 +76,9 @@ def parse():
                     help="sweep/ragged int32 row pitch: packed = 16-B multiple, line = "
                          "128-B multiple (pad columns are never read)")
     return ap.parse_args()
+
+
+SPEC_HBM_GBS = 8000.0  # B200 HBM3e spec (DGX figure), the north star's denominator
 
 
 def peaks():
@@ -327,7 +333,9 @@ def run_ours(args, world, rank, local):
                 "traffic": round(tps * n) if tps else None,
                 "algorithmic_bytes_per_launch": n * bytes_per_sample,
                 "bytes_per_sample": f"{eb}F+4+{out_bytes} = {bytes_per_sample}",
-                "kernel": kernel}
+                "kernel": kernel,
+                # report the 8.0 TB/s spec figure beside the measured peak
+                "peak_spec": SPEC_HBM_GBS, "frac_spec": round(achieved / SPEC_HBM_GBS, 4)}
     if ncu:
         roofline["traffic_source"] = ncu.get("source")
 
@@ -461,6 +469,7 @@ def run_reference(args, world, rank):
         step()
     dt = time.perf_counter() - t0
     value = sample * args.steps / dt
+    ref_py = reference_python_leg(args.ref_py_samples, V) if args.ref_py_samples > 0 else None
     return {
         "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup,
@@ -476,7 +485,47 @@ def run_reference(args, world, rank):
                          "impl": "oracle/gnb_oracle.c"},
         "e2e": {"value": round(value, 1), "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
+        "reference_python": ref_py,
     }
+
+
+def reference_python_leg(n, V):
+    """The UNMODIFIED reference package (baseline/_ref, pip-installed from
+    /root/reference) through its own public API on a bounded sample: Tc =
+    classify_sequential (1 core), Tp = classify_parallel (all cores), both by the
+    reference's own elapsed_ns.  Reported beside the C port."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "groupnb")):
+        return {"unavailable": "baseline/_ref not installed (see DESIGN.md section 5)"}
+    try:
+        if ref not in sys.path:
+            sys.path.insert(0, ref)
+        from groupnb.corpus import GroupingConfig, partition_by_group
+        from groupnb.engine import Workload, classify_parallel, classify_sequential, train_bundle
+        from groupnb.synth import SyntheticSpec, generate_synthetic
+        t0 = time.perf_counter()
+        spec = SyntheticSpec(group_count=1, samples_per_group_per_class=n // 2,
+                             vocabulary_size=V, divergence=0.8, seed=0)
+        samples = generate_synthetic(spec)
+        grouped, _ = partition_by_group(samples, GroupingConfig())
+        t1 = time.perf_counter()
+        bundle = train_bundle(grouped, k=V)
+        t2 = time.perf_counter()
+        work = tuple(samples)
+        lanes = os.cpu_count() or 1
+        tc = classify_sequential(bundle, Workload(work, 1), warmup=False)
+        tp = classify_parallel(bundle, Workload(work, lanes), warmup=False)
+        return {"impl": "groupnb (reference pkg, unmodified)", "samples": len(work),
+                "features": V, "classes": 2,
+                "Tc_samples_per_s": round(len(work) / (tc.elapsed_ns / 1e9), 1),
+                "Tp_samples_per_s": round(len(work) / (tp.elapsed_ns / 1e9), 1),
+                "Tp_lanes": lanes,
+                "fit_samples_per_s": round(len(work) / (t2 - t1), 1),
+                "generate_s": round(t1 - t0, 2),
+                "labels_equal_Tc_Tp": [p.label for p in tc.predictions] ==
+                                      [p.label for p in tp.predictions]}
+    except Exception as e:  # reported, never fatal for the C-port arm
+        return {"unavailable": f"{type(e).__name__}: {e}"[:200]}
 
 
 # ---------------------------------------------------------------- secondary workloads

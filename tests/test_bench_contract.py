@@ -22,11 +22,14 @@ def _run(args, timeout):
 
 
 def test_reference_arm_contract():
-    d = _run(["--impl", "reference", "--steps", "2", "--warmup", "1", "--ref-rows", "20000"], 300)
+    d = _run(["--impl", "reference", "--steps", "2", "--warmup", "1", "--ref-rows", "20000",
+              "--ref-py-samples", "2000"], 300)
     assert BASE_KEYS <= set(d)
     assert d["impl"] == "reference" and d["value"] > 0 and d["higher_is_better"] is True
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
     assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1
+    ref = d["reference_python"]   # the unmodified reference pkg, when installed
+    assert "unavailable" in ref or (ref["Tc_samples_per_s"] > 0 and ref["labels_equal_Tc_Tp"])
 
 
 @pytest.mark.gpu
