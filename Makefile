@@ -3,7 +3,11 @@ NVCC ?= nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -O3
 PKG := paper_1905_13746_b200
-SRC := $(PKG)/csrc/predict.cu $(PKG)/csrc/fit.cu $(PKG)/csrc/gen.cu $(PKG)/csrc/gather.cu $(PKG)/csrc/sort.cu $(PKG)/csrc/fin_select.cu $(PKG)/csrc/api.cu $(PKG)/csrc/fin.cpp $(PKG)/csrc/ingest.cpp
+CU := predict predict_i32_exact predict_i32_fma predict_u16_exact predict_u16_fma \
+      predict_u8_exact predict_u8_fma fit gen gather sort fin_select api
+CXX_SRC := fin ingest
+OBJDIR := $(PKG)/csrc/build
+OBJ := $(CU:%=$(OBJDIR)/%.o) $(CXX_SRC:%=$(OBJDIR)/%.o)
 HDR := $(wildcard $(PKG)/csrc/*.h $(PKG)/csrc/*.cuh) include/gnb.h
 
 PYINC := $(shell python3 -c "import sysconfig; print(sysconfig.get_paths()['include'])")
@@ -15,14 +19,24 @@ all: $(PKG)/libgnb.so $(ADAPT) oracle
 $(ADAPT): $(PKG)/csrc/adapt.cpp
 	g++ -O3 -std=c++17 -fPIC -shared -I$(PYINC) -o $@ $<
 
-$(PKG)/libgnb.so: $(SRC) $(HDR)
-	$(NVCC) $(NVFLAGS) -shared -o $@ $(SRC)
+# one object per translation unit so `make -j` compiles the K-PRED instances in parallel
+$(OBJDIR)/%.o: $(PKG)/csrc/%.cu $(HDR)
+	@mkdir -p $(OBJDIR)
+	$(NVCC) $(NVFLAGS) -c -o $@ $<
+
+$(OBJDIR)/%.o: $(PKG)/csrc/%.cpp $(HDR)
+	@mkdir -p $(OBJDIR)
+	$(NVCC) $(NVFLAGS) -c -o $@ $<
+
+$(PKG)/libgnb.so: $(OBJ)
+	$(NVCC) $(NVFLAGS) -shared -o $@ $(OBJ)
 
 oracle:
 	$(MAKE) -C oracle
 
 clean:
 	rm -f $(PKG)/libgnb.so $(ADAPT)
+	rm -rf $(OBJDIR)
 	$(MAKE) -C oracle clean
 
 .PHONY: all oracle clean

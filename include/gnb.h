@@ -55,6 +55,9 @@ enum {
  * integer counts, stored in fewer bytes when they fit */
 enum { GNB_X_I32 = 0, GNB_X_U16 = 1, GNB_X_U8 = 2 };
 
+/* predict arithmetic (gnb_predict_mode) */
+enum { GNB_MODE_EXACT = 0, GNB_MODE_FMA = 1 };
+
 int gnb_abi_version(void);
 const char* gnb_strerror(int code);
 const char* gnb_last_error(void);
@@ -108,6 +111,22 @@ int gnb_predict_permuted(const void* x, int32_t x_type, int64_t n_rows, int32_t 
                          int32_t max_size_bytes, const int32_t* route, int32_t n_slots,
                          int32_t n_classes, const void* packed, const int32_t* perm,
                          int32_t* label_out, double* logpost_out, uintptr_t stream);
+
+/* All options in one call: any storage, optional perm (NULL = rows in order,
+ * else as gnb_predict_permuted), and the arithmetic mode:
+ *   GNB_MODE_EXACT  acc = acc + x*ll with the reference's two roundings
+ *                   (DMUL then DADD; bit-identical log-posteriors) -- default
+ *                   of every other entry point;
+ *   GNB_MODE_FMA    acc = fma(x, ll, acc), one rounding per term: log-posteriors
+ *                   within ~1e-12 relative of the reference (north star asks
+ *                   1e-5), labels identical except at top-two margins of that
+ *                   size; halves the FP64 work of compute-bound narrow rows.
+ * (SURVEY 8b `gnb_geom.mode`.) */
+int gnb_predict_mode(const void* x, int32_t x_type, int64_t n_rows, int32_t n_features,
+                     int64_t ldx, const int32_t* size_bytes, int32_t group_size_bytes,
+                     int32_t max_size_bytes, const int32_t* route, int32_t n_slots,
+                     int32_t n_classes, const void* packed, const int32_t* perm, int32_t mode,
+                     int32_t* label_out, double* logpost_out, uintptr_t stream);
 
 /* Same as gnb_predict but always uses the L1 (non-TMA) kernel; parity tests. */
 int gnb_predict_generic(const int32_t* x, int64_t n_rows, int32_t n_features, int64_t ldx,

@@ -19,6 +19,7 @@ LIB_PATH = os.path.join(_HERE, os.environ.get("GNB_LIB", "libgnb.so"))
 HEADER = os.path.join(os.path.dirname(_HERE), "include", "gnb.h")
 
 GNB_OK, GNB_EINVAL, GNB_ECUDA, GNB_EUNSUPPORTED, GNB_ENOMEM = 0, 1, 2, 3, 4
+GNB_MODE_EXACT, GNB_MODE_FMA = 0, 1
 ROW_OUT_OF_RANGE = -1
 ROW_NEGATIVE_COUNT = -2
 MAX_CLASSES = 16
@@ -56,6 +57,8 @@ _SIGS = {
     "gnb_slot_sort": ([_p, _i64, _i32, _i32, _p, _i32, _p, _p, _sz, _up], C.c_int),
     "gnb_predict_permuted": ([_p, _i32, _i64, _i32, _i64, _p, _i32, _i32, _p, _i32, _i32, _p, _p,
                               _p, _p, _up], C.c_int),
+    "gnb_predict_mode": ([_p, _i32, _i64, _i32, _i64, _p, _i32, _i32, _p, _i32, _i32, _p, _p,
+                          _i32, _p, _p, _up], C.c_int),
     "gnb_predict_generic": ([_p, _i64, _i32, _i64, _p, _i32, _i32, _p, _i32, _i32, _p, _p, _p,
                              _up], C.c_int),
     "gnb_predict_host": ([_p, _i64, _i32, _i64, _p, _i32, _i32, _p, _i32, _i32, _p, _p, _p, _p,

@@ -128,7 +128,7 @@ static constexpr int64_t kMaxRowsPerLaunch = int64_t(1) << 30;  // TMA coordinat
 
 extern "C" {
 
-int gnb_abi_version(void) { return 1; }
+int gnb_abi_version(void) { return 2; }
 
 const char* gnb_strerror(int code) {
   switch (code) {
@@ -183,7 +183,8 @@ static int predict_device(const void* x, int x_type, int64_t n_rows, int32_t F, 
                           const int32_t* size, int32_t width, int32_t limit,
                           const int32_t* route, int32_t S, int32_t C, const void* packed,
                           int32_t* label, double* logpost, cudaStream_t stream,
-                          int force_generic = 0, const int32_t* perm = nullptr) {
+                          int force_generic = 0, const int32_t* perm = nullptr,
+                          int mode = GNB_MODE_EXACT) {
   const bool use_tma = !force_generic && tma_ok(x, ldx, x_type) && encode_fn() != nullptr;
   if (perm != nullptr && n_rows > kMaxRowsPerLaunch)
     return fail(GNB_EUNSUPPORTED, "predict: permuted batches are limited to 2^30 rows");
@@ -206,6 +207,7 @@ static int predict_device(const void* x, int x_type, int64_t n_rows, int32_t F, 
     p.label = label + r0;
     p.logpost = logpost ? logpost + r0 * C : nullptr;
     p.perm = use_tma ? perm : nullptr;  // the L1 kernel walks rows in order
+    p.mode = mode;
     PredictMaps map;
     const PredictMaps* mp = nullptr;
     if (use_tma) {
@@ -354,6 +356,24 @@ int gnb_predict_permuted(const void* x, int32_t x_type, int64_t n_rows, int32_t 
   return predict_device(x, x_type, n_rows, n_features, ldx, size_bytes, group_size_bytes,
                         max_size_bytes, route, n_slots, n_classes, packed, label_out,
                         logpost_out, reinterpret_cast<cudaStream_t>(stream), 0, perm);
+}
+
+int gnb_predict_mode(const void* x, int32_t x_type, int64_t n_rows, int32_t n_features,
+                     int64_t ldx, const int32_t* size_bytes, int32_t group_size_bytes,
+                     int32_t max_size_bytes, const int32_t* route, int32_t n_slots,
+                     int32_t n_classes, const void* packed, const int32_t* perm, int32_t mode,
+                     int32_t* label_out, double* logpost_out, uintptr_t stream) {
+  if (x_type != GNB_X_I32 && x_type != GNB_X_U16 && x_type != GNB_X_U8)
+    return fail(GNB_EINVAL, "predict: unknown x_type %d", x_type);
+  if (mode != GNB_MODE_EXACT && mode != GNB_MODE_FMA)
+    return fail(GNB_EINVAL, "predict: unknown mode %d", mode);
+  int rc = check_predict(static_cast<const int32_t*>(x), n_rows, n_features, ldx, size_bytes,
+                         group_size_bytes, max_size_bytes, route, n_slots, n_classes, packed,
+                         label_out);
+  if (rc) return rc;
+  return predict_device(x, x_type, n_rows, n_features, ldx, size_bytes, group_size_bytes,
+                        max_size_bytes, route, n_slots, n_classes, packed, label_out,
+                        logpost_out, reinterpret_cast<cudaStream_t>(stream), 0, perm, mode);
 }
 
 // Test hook: force the L1 (non-TMA) predict kernel.

@@ -22,22 +22,11 @@
 //   * argmax (ties -> lowest class index = benign) and the out-of-range status
 //     are fused into the epilogue; label (+ optional log-posteriors) written
 //     once, coalesced.
-#include <cfloat>
-#include <climits>
-#include <cstdint>
-#include <cstdlib>
-
-#include "gnb_device.cuh"
-#include "gnb_internal.h"
+//
+// Kernels: predict_kernels.cuh.  This unit: table packing and the dispatch.
+#include "predict_kernels.cuh"
 
 namespace gnb {
-
-// ------------------------------------------------------------------ tables
-// packed = [prior: S][CP] | [tab: S][NB][32 features][CP] log-likelihoods.
-// NB = ceil(F/32) rounded up to a multiple of 4, so a 128-feature chunk (uint8
-// X) of any slot is one in-bounds contiguous block; padding entries are 0.
-constexpr int kTabBlockFeatures = 32;
-constexpr int kTabBlockAlign = 4;
 
 int table_blocks(int F) {
   const int nb = (F + kTabBlockFeatures - 1) / kTabBlockFeatures;
@@ -68,713 +57,6 @@ __global__ void pack_tables_kernel(const double* __restrict__ log_prior,
   }
 }
 
-// ------------------------------------------------------------------ element types
-template <typename T>
-struct Elem {
-  static constexpr int kPerQuad = 16 / static_cast<int>(sizeof(T));   // per 16-B chunk
-  static constexpr int kPerRow = 128 / static_cast<int>(sizeof(T));   // per 128-B box row
-  static constexpr bool kSigned = false;
-};
-template <>
-struct Elem<int32_t> {
-  static constexpr int kPerQuad = 4, kPerRow = 32;
-  static constexpr bool kSigned = true;  // negative counts are flagged, not scored
-};
-
-// Element e (0 <= e < kPerQuad) of a 16-B chunk as a double.  The conversion
-// is exact (counts < 2^32) and runs on the conversion unit (I2F.F64; for
-// uint8/uint16 with a byte/half-word source select), so the product below is
-// ONE DMUL rounding, exactly the reference's `n * ll` (a Python float multiply).
-template <typename T>
-__device__ __forceinline__ double converted(const uint4& v, int e) {
-  constexpr int sz = static_cast<int>(sizeof(T));
-  const uint32_t w = (e * sz) < 4 ? v.x : (e * sz) < 8 ? v.y : (e * sz) < 12 ? v.z : v.w;
-  if constexpr (sz == 4) {
-    return __uint2double_rn(w);
-  } else {
-    constexpr int bits = 8 * sz;
-    return __uint2double_rn((w >> ((e * bits) & 31)) & ((1u << bits) - 1u));
-  }
-}
-
-// ------------------------------------------------------------------ inner loops
-struct GlobalTab {
-  const double* p;
-  __device__ __forceinline__ double get(int idx) const { return __ldg(p + idx); }
-};
-
-// One 16-B chunk (kPerQuad consecutive features) of one row, all classes.
-template <int CP, typename T, typename Tab>
-__device__ __forceinline__ void score_quad(double (&acc)[CP], const uint4 v, const Tab& tab,
-                                           int feat0) {
-#pragma unroll
-  for (int e = 0; e < Elem<T>::kPerQuad; ++e) {
-    const double xd = converted<T>(v, e);
-#pragma unroll
-    for (int c = 0; c < CP; ++c)
-      acc[c] = __dadd_rn(acc[c], __dmul_rn(xd, tab.get((feat0 + e) * CP + c)));
-  }
-}
-
-template <int CP, typename T, typename Tab>
-__device__ __forceinline__ void score_chunk(double (&acc)[CP], const uint8_t* box, uint32_t row,
-                                            const Tab& tab, int nq, uint32_t& neg) {
-  constexpr int EQ = Elem<T>::kPerQuad;
-  if (nq == 8) {
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const uint4 v = *reinterpret_cast<const uint4*>(box + swz128(row, q));
-      if (Elem<T>::kSigned) neg |= v.x | v.y | v.z | v.w;
-      score_quad<CP, T>(acc, v, tab, EQ * q);
-    }
-  } else {
-#pragma unroll 1
-    for (int q = 0; q < nq; ++q) {
-      const uint4 v = *reinterpret_cast<const uint4*>(box + swz128(row, q));
-      if (Elem<T>::kSigned) neg |= v.x | v.y | v.z | v.w;
-      score_quad<CP, T>(acc, v, tab, EQ * q);
-    }
-  }
-}
-
-template <int CP>
-__device__ __forceinline__ void write_row(const PredictParams& p, int64_t r, int slot,
-                                          uint32_t neg, const double (&acc)[CP]) {
-  int lab;
-  if (slot < 0) {
-    lab = GNB_ROW_OUT_OF_RANGE;
-  } else if (neg & 0x80000000u) {
-    lab = GNB_ROW_NEGATIVE_COUNT;
-  } else {
-    lab = 0;
-    double best = acc[0];
-#pragma unroll
-    for (int c = 1; c < CP; ++c) {
-      if (acc[c] > best) {  // strict: ties keep the lower index (benign)
-        best = acc[c];
-        lab = c;
-      }
-    }
-  }
-  p.label[r] = lab;
-  if (p.logpost != nullptr) {
-    const double nan = __longlong_as_double(0x7ff8000000000000ll);
-    double* out = p.logpost + r * p.n_classes;
-    if (p.n_classes == 2 && CP == 2) {
-      const double2 v = slot < 0 ? make_double2(nan, nan) : make_double2(acc[0], acc[CP - 1]);
-      *reinterpret_cast<double2*>(out) = v;
-    } else {
-#pragma unroll
-      for (int c = 0; c < CP; ++c)
-        if (c < p.n_classes) out[c] = slot < 0 ? nan : acc[c];
-    }
-  }
-}
-
-// ------------------------------------------------------------------ TMA kernel
-// A consumer thread owns R rows of the tile (rows lane + 32*(w + NW*i)), so one
-// broadcast table read feeds R*CP independent accumulator chains.
-// A stage holds B consecutive 128-B column chunks of the tile (B boxes).
-template <int CP, typename T, int R, int NW, int STAGES, bool GATHER = false, int B = 1>
-struct PredictSmem {
-  static constexpr int kRows = NW * 32 * R;                          // rows per tile (<= 256)
-  static constexpr int kBox = kRows * kChunkBytesPerRow;               // one box
-  static constexpr int kXBytes = B * kBox;                             // one stage
-  static constexpr int kTabChunk = Elem<T>::kPerRow * CP * 8;          // one chunk's table
-  static constexpr int kTabBytes = B * kTabChunk;                      // one stage's tables
-  // tile_slot + row_slot[kRows] (+ row_id[kRows] in gather mode)
-  static constexpr int kHdrBytes = ((4 + kRows * 4 * (GATHER ? 2 : 1)) + 15) / 16 * 16;
-  static constexpr int kX = 0;
-  static constexpr int kTab = kX + STAGES * kXBytes;
-  static constexpr int kHdr = kTab + STAGES * kTabBytes;
-  static constexpr int kBar = kHdr + STAGES * kHdrBytes;
-  static constexpr int kTotal = kBar + 2 * STAGES * 8;
-  static constexpr int kAlloc = kTotal + 1024;  // slack for 1024-B alignment
-  static_assert(kRows <= 256, "TMA box rows <= 256");
-};
-
-struct StageHdr {
-  int tile_slot;  // >= 0: every valid row uses this slot; table slice staged
-  int row_slot[1];  // [kRows]; in gather mode followed by row_id[kRows]
-};
-
-// Table of slot s, chunk ch (kPerRow features per chunk).
-template <int CP, typename T>
-__device__ __forceinline__ const double* chunk_table(const PredictParams& p, int s, int ch) {
-  constexpr int blocks_per_chunk = Elem<T>::kPerRow / kTabBlockFeatures;
-  return p.tab + (static_cast<int64_t>(s) * p.n_tab_blocks + ch * blocks_per_chunk) *
-                     (kTabBlockFeatures * CP);
-}
-
-// Uniform tile: the chunk's table slice is in smem and shared by all R rows.
-template <int CP, typename T, int R>
-__device__ __forceinline__ void score_chunk_uniform(double (&acc)[R][CP], const uint8_t* box,
-                                                    const uint32_t (&rows)[R], const double* tab,
-                                                    int nq, uint32_t (&neg)[R]) {
-  constexpr int EQ = Elem<T>::kPerQuad;
-  auto quad = [&](int q) {
-    uint4 v[R];
-#pragma unroll
-    for (int i = 0; i < R; ++i) {
-      v[i] = *reinterpret_cast<const uint4*>(box + swz128(rows[i], q));
-      if (Elem<T>::kSigned) neg[i] |= v[i].x | v[i].y | v[i].z | v[i].w;
-    }
-#pragma unroll
-    for (int e = 0; e < EQ; ++e) {
-      double t[CP];  // one broadcast LDS.128 per 2 classes
-#pragma unroll
-      for (int c = 0; c < CP; c += 2) {
-        const double2 t2 = *reinterpret_cast<const double2*>(tab + (EQ * q + e) * CP + c);
-        t[c] = t2.x;
-        t[c + 1] = t2.y;
-      }
-#pragma unroll
-      for (int i = 0; i < R; ++i) {
-        const double xd = converted<T>(v[i], e);
-#pragma unroll
-        for (int c = 0; c < CP; ++c) acc[i][c] = __dadd_rn(acc[i][c], __dmul_rn(xd, t[c]));
-      }
-    }
-  };
-  if (nq == 8) {
-#pragma unroll
-    for (int q = 0; q < 8; ++q) quad(q);
-  } else {
-#pragma unroll 1
-    for (int q = 0; q < nq; ++q) quad(q);
-  }
-}
-
-// Mixed tile: every row reads its own slot's table through L1.
-template <int CP, typename T, int R>
-__device__ __forceinline__ void score_chunk_mixed(const PredictParams& p, double (&acc)[R][CP],
-                                                  const uint8_t* box, const uint32_t (&rows)[R],
-                                                  const int (&slot)[R], int ch, int nq,
-                                                  uint32_t (&neg)[R]) {
-#pragma unroll
-  for (int i = 0; i < R; ++i) {
-    const GlobalTab tab{chunk_table<CP, T>(p, max(slot[i], 0), ch)};
-    double a[CP];
-#pragma unroll
-    for (int c = 0; c < CP; ++c) a[c] = acc[i][c];
-    score_chunk<CP, T>(a, box, rows[i], tab, nq, neg[i]);
-#pragma unroll
-    for (int c = 0; c < CP; ++c) acc[i][c] = a[c];
-  }
-}
-
-// GATHER: tile rows are perm[tile*ROWS ...] (rows sorted by routed slot by
-// slot_sort), loaded with TMA tile::gather4 (4 arbitrary rows per
-// instruction, one instruction per producer lane) into the same swizzled box
-// layout; outputs go back to the original row index.
-template <int CP, typename T, int R, int NW, int STAGES, bool GATHER, int B = 1>
-__global__ void __launch_bounds__((NW + 1) * 32)
-    predict_tma_kernel(const __grid_constant__ PredictMaps maps, const PredictParams p) {
-  const CUtensorMap& xmap = maps.main;
-  using L = PredictSmem<CP, T, R, NW, STAGES, GATHER, B>;
-  constexpr int ROWS = L::kRows;
-  constexpr int CF = Elem<T>::kPerRow;
-  constexpr int EQ = Elem<T>::kPerQuad;
-  extern __shared__ uint8_t smem_raw[];
-  // 1024-B alignment for SWIZZLE_128B, keeping the pointer in the shared window
-  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::kBar);
-  uint64_t* empty = full + STAGES;
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], 32);   // all producer lanes arrive (lane 0 with tx)
-      mbar_init(&empty[s], NW);  // one arrive per consumer warp
-    }
-    mbar_fence_init();
-  }
-  if (warp == NW && lane == 0) {
-    prefetch_tensormap(&xmap);
-    if (GATHER) prefetch_tensormap(&maps.tail);
-  }
-  __syncthreads();
-
-  const int NCH = p.n_chunks;
-  const int NSC = (NCH + B - 1) / B;  // stages per tile
-  const int64_t n_tiles = p.n_tiles;
-
-  if (warp == NW) {
-    // ---------------------------------------------------------- producer
-    const uint64_t pol_x = p.x_policy == 1 ? policy_evict_first() : policy_evict_normal();
-    const uint64_t pol_t = policy_evict_last();
-    int stage = 0;
-    uint32_t phase = 0;
-    for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-      const int64_t r0 = tile * ROWS;
-      int slots[ROWS / 32], ids[ROWS / 32];
-      int lo = INT_MAX, hi = INT_MIN;
-#pragma unroll
-      for (int i = 0; i < ROWS / 32; ++i) {
-        int64_t r = r0 + lane + 32 * i;
-        int s = -1;
-        if (GATHER) r = r < p.n_rows ? __ldg(p.perm + r) : -1;
-        ids[i] = static_cast<int>(GATHER ? r : 0);
-        if (r >= 0 && r < p.n_rows) {
-          const int sz = __ldg(p.size + r);
-          if (sz >= 0 && sz < p.limit) {
-            s = __ldg(p.route + sz / p.width);
-            lo = min(lo, s);
-            hi = max(hi, s);
-          }
-        }
-        slots[i] = s;
-      }
-      lo = __reduce_min_sync(0xffffffffu, lo);
-      hi = __reduce_max_sync(0xffffffffu, hi);
-      const int tile_slot = (lo == INT_MAX) ? 0 : (lo == hi ? lo : -1);
-      for (int sc = 0; sc < NSC; ++sc) {
-        const int ch = sc * B;
-        const int nb = min(B, NCH - ch);
-        mbar_wait(&empty[stage], phase ^ 1);
-        StageHdr* hdr = reinterpret_cast<StageHdr*>(smem + L::kHdr + stage * L::kHdrBytes);
-        if (ch == 0) {
-#pragma unroll
-          for (int i = 0; i < ROWS / 32; ++i) {
-            hdr->row_slot[lane + 32 * i] = slots[i];
-            if (GATHER) hdr->row_slot[ROWS + lane + 32 * i] = ids[i];
-          }
-        }
-        if (lane == 0) hdr->tile_slot = tile_slot;
-        __syncwarp();
-        uint8_t* box = smem + L::kX + stage * L::kXBytes;
-        if (lane == 0) {
-          const uint32_t bytes = nb * (L::kBox + (tile_slot >= 0 ? L::kTabChunk : 0));
-          mbar_arrive_expect_tx(&full[stage], bytes);
-          if (!GATHER)
-            for (int b = 0; b < nb; ++b)
-              tma_load_2d(box + b * L::kBox, &xmap, (ch + b) * CF, static_cast<int32_t>(r0),
-                          &full[stage], pol_x);
-          if (tile_slot >= 0)
-            bulk_load(smem + L::kTab + stage * L::kTabBytes, chunk_table<CP, T>(p, tile_slot, ch),
-                      nb * L::kTabChunk, &full[stage], pol_t);
-        }
-        if (GATHER) {
-          __syncwarp();  // expect_tx precedes every completion
-#pragma unroll
-          for (int g = lane; g < ROWS / 4; g += 32) {
-            int rr[4];
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              const int64_t pos = r0 + 4 * g + k;
-              rr[k] = __ldg(p.perm + (pos < p.n_rows ? pos : p.n_rows - 1));
-            }
-            for (int b = 0; b < nb; ++b)
-              tma_gather4(box + b * L::kBox + 4 * g * kChunkBytesPerRow,
-                          ch + b == NCH - 1 ? &maps.tail : &xmap, (ch + b) * CF, rr,
-                          &full[stage]);
-          }
-        }
-        if (lane != 0) mbar_arrive(&full[stage]);
-        if (++stage == STAGES) {
-          stage = 0;
-          phase ^= 1;
-        }
-      }
-    }
-  } else {
-    // ---------------------------------------------------------- consumers
-    uint32_t rows[R];
-#pragma unroll
-    for (int i = 0; i < R; ++i) rows[i] = lane + 32 * (warp + NW * i);
-    int stage = 0;
-    uint32_t phase = 0;
-    for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-      double acc[R][CP];
-      int slot[R], rid[R];
-      uint32_t neg[R];
-#pragma unroll
-      for (int i = 0; i < R; ++i) neg[i] = 0;
-      for (int sc = 0; sc < NSC; ++sc) {
-        mbar_wait(&full[stage], phase);
-        const StageHdr* hdr =
-            reinterpret_cast<const StageHdr*>(smem + L::kHdr + stage * L::kHdrBytes);
-        const int ts = hdr->tile_slot;
-        if (sc == 0) {
-#pragma unroll
-          for (int i = 0; i < R; ++i) {
-            slot[i] = hdr->row_slot[rows[i]];
-            rid[i] = GATHER ? hdr->row_slot[ROWS + rows[i]] : 0;
-            const int s = ts >= 0 ? ts : max(slot[i], 0);
-#pragma unroll
-            for (int c = 0; c < CP; ++c) acc[i][c] = __ldg(p.prior + s * CP + c);
-          }
-        }
-#pragma unroll
-        for (int b = 0; b < B; ++b) {
-          const int ch = sc * B + b;
-          if (B > 1 && ch >= NCH) break;
-          const int nf = min(CF, p.n_features - ch * CF);
-          const int nq = (nf + EQ - 1) / EQ;
-          const uint8_t* box = smem + L::kX + stage * L::kXBytes + b * L::kBox;
-          if (ts >= 0) {
-            score_chunk_uniform<CP, T, R>(
-                acc, box, rows,
-                reinterpret_cast<const double*>(smem + L::kTab + stage * L::kTabBytes +
-                                                b * L::kTabChunk),
-                nq, neg);
-          } else {
-            score_chunk_mixed<CP, T, R>(p, acc, box, rows, slot, ch, nq, neg);
-          }
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[stage]);
-        if (++stage == STAGES) {
-          stage = 0;
-          phase ^= 1;
-        }
-      }
-#pragma unroll
-      for (int i = 0; i < R; ++i) {
-        if (GATHER) {
-          if (tile * ROWS + rows[i] < p.n_rows) write_row<CP>(p, rid[i], slot[i], neg[i], acc[i]);
-        } else {
-          const int64_t r = tile * ROWS + rows[i];
-          if (r < p.n_rows) write_row<CP>(p, r, slot[i], neg[i], acc[i]);
-        }
-      }
-    }
-  }
-}
-
-// ------------------------------------------------------------------ row-box kernel
-// Short rows (F <= ~100 int32 features): one TMA box holds kRowBoxRows whole
-// rows, unswizzled, WQ 16-B quads per smem row with WQ odd so the 8 lanes of an
-// LDS.128 phase (consecutive rows, stride WQ*16 B) hit 8 distinct bank groups.
-// One stage per tile, no partial 128-B chunks: the 128-B-box kernel above
-// spends a whole 16-KB stage on e.g. the 18 trailing features of F=50, so short
-// rows kept too few bytes in flight per SM.  Ring depth and CTAs per SM follow
-// the box size (predict_launch).  Same arithmetic and order as every path.
-struct RowBoxSmem {
-  uint32_t x_bytes, tab_bytes, hdr_bytes, x, tab, hdr, sizes, bar, total;
-  // ahead: tiles whose row sizes are in flight ahead of routing
-  __host__ __device__ RowBoxSmem(int wq, int tab_feats, int cp, int stages, int ahead) {
-    x_bytes = static_cast<uint32_t>(kRowBoxRows) * wq * 16;
-    tab_bytes = static_cast<uint32_t>(tab_feats) * cp * 8;
-    hdr_bytes = (4 + kRowBoxRows * 4 + 15) / 16 * 16;
-    x = 0;
-    tab = x + stages * x_bytes;
-    hdr = tab + stages * tab_bytes;
-    sizes = hdr + stages * hdr_bytes;  // [ahead][kRowBoxRows] prefetched sizes
-    bar = sizes + ahead * kRowBoxRows * 4;
-    total = bar + 2 * stages * 8;
-  }
-};
-
-__host__ __device__ inline int rowbox_tab_feats(int F, int EQ, int n_tab_blocks) {
-  const int nq = (F + EQ - 1) / EQ;
-  const int want = nq * EQ, have = n_tab_blocks * kTabBlockFeatures;
-  return want < have ? want : have;
-}
-
-template <int CP, typename T, int kRowBoxAhead>
-__global__ void __launch_bounds__(5 * 32)
-    predict_rowbox_kernel(const __grid_constant__ PredictMaps maps, const PredictParams p) {
-  const CUtensorMap& xmap = maps.main;
-  constexpr int NW = 4, ROWS = kRowBoxRows, EQ = Elem<T>::kPerQuad;
-  static_assert(ROWS == NW * 32, "one row per consumer thread");
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
-  const int ST = p.rowbox_stages, WQ = p.rowbox_quads;
-  const int tab_feats = rowbox_tab_feats(p.n_features, EQ, p.n_tab_blocks);
-  const RowBoxSmem L(WQ, tab_feats, CP, ST, kRowBoxAhead);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.bar);
-  uint64_t* empty = full + ST;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < ST; ++s) {
-      mbar_init(&full[s], 32);
-      mbar_init(&empty[s], NW);
-    }
-    mbar_fence_init();
-  }
-  if (warp == NW && lane == 0) prefetch_tensormap(&xmap);
-  __syncthreads();
-  const int64_t n_tiles = p.n_tiles;
-  const int64_t slot_tab = static_cast<int64_t>(p.n_tab_blocks) * kTabBlockFeatures * CP;
-
-  if (warp == NW) {
-    // ---------------------------------------------------------- producer
-    const uint64_t pol_x = p.x_policy == 1 ? policy_evict_first() : policy_evict_normal();
-    const uint64_t pol_t = policy_evict_last();
-    int stage = 0;
-    uint32_t phase = 0;
-    // Row sizes travel kRowBoxAhead tiles ahead of routing (LDGSTS into a
-    // smem ring, each lane reading back only its own entries): with one stage
-    // per tile, a size load per tile on the critical path capped the rate at
-    // one tile per loaded-HBM round trip.
-    int* szr = reinterpret_cast<int*>(smem + L.sizes);
-    auto fetch_sizes = [&](int64_t tile, int k) {
-      if (tile < n_tiles) {
-#pragma unroll
-        for (int i = 0; i < ROWS / 32; ++i) {
-          const int64_t r = tile * ROWS + lane + 32 * i;
-          cp_async4(szr + k * ROWS + lane + 32 * i, p.size + (r < p.n_rows ? r : p.n_rows - 1));
-        }
-      }
-      cp_async_commit();
-    };
-#pragma unroll
-    for (int k = 0; k < kRowBoxAhead; ++k) fetch_sizes(blockIdx.x + int64_t(k) * gridDim.x, k);
-    int k_cur = 0;
-    for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-      const int64_t r0 = tile * ROWS;
-      int slots[ROWS / 32];
-      int lo = INT_MAX, hi = INT_MIN;
-      cp_async_wait<kRowBoxAhead - 1>();
-#pragma unroll
-      for (int i = 0; i < ROWS / 32; ++i) {
-        const int64_t r = r0 + lane + 32 * i;
-        const int sz = szr[k_cur * ROWS + lane + 32 * i];
-        int s = -1;
-        if (r < p.n_rows && sz >= 0 && sz < p.limit) {
-          s = __ldg(p.route + sz / p.width);
-          lo = min(lo, s);
-          hi = max(hi, s);
-        }
-        slots[i] = s;
-      }
-      fetch_sizes(tile + int64_t(kRowBoxAhead) * gridDim.x, k_cur);
-      if (++k_cur == kRowBoxAhead) k_cur = 0;
-      lo = __reduce_min_sync(0xffffffffu, lo);
-      hi = __reduce_max_sync(0xffffffffu, hi);
-      const int tile_slot = (lo == INT_MAX) ? 0 : (lo == hi ? lo : -1);
-      mbar_wait(&empty[stage], phase ^ 1);
-      int* hdr = reinterpret_cast<int*>(smem + L.hdr + stage * L.hdr_bytes);
-#pragma unroll
-      for (int i = 0; i < ROWS / 32; ++i) hdr[1 + lane + 32 * i] = slots[i];
-      if (lane == 0) hdr[0] = tile_slot;
-      __syncwarp();
-      if (lane == 0) {
-        mbar_arrive_expect_tx(&full[stage], L.x_bytes + (tile_slot >= 0 ? L.tab_bytes : 0));
-        tma_load_2d(smem + L.x + stage * L.x_bytes, &xmap, 0, static_cast<int32_t>(r0),
-                    &full[stage], pol_x);
-        if (tile_slot >= 0)
-          bulk_load(smem + L.tab + stage * L.tab_bytes, p.tab + tile_slot * slot_tab,
-                    L.tab_bytes, &full[stage], pol_t);
-      } else {
-        mbar_arrive(&full[stage]);
-      }
-      if (++stage == ST) {
-        stage = 0;
-        phase ^= 1;
-      }
-    }
-  } else {
-    // ---------------------------------------------------------- consumers
-    const int row = lane + 32 * warp;
-    const int nq = (p.n_features + EQ - 1) / EQ;
-    int stage = 0;
-    uint32_t phase = 0;
-    for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-      mbar_wait(&full[stage], phase);
-      const int* hdr = reinterpret_cast<const int*>(smem + L.hdr + stage * L.hdr_bytes);
-      const int ts = hdr[0];
-      const int slot = hdr[1 + row];
-      const int s = ts >= 0 ? ts : max(slot, 0);
-      double acc[CP];
-#pragma unroll
-      for (int c = 0; c < CP; ++c) acc[c] = __ldg(p.prior + s * CP + c);
-      uint32_t neg = 0;
-      const uint8_t* xrow = smem + L.x + stage * L.x_bytes + row * (WQ * 16);
-      if (ts >= 0) {
-        const double* tab = reinterpret_cast<const double*>(smem + L.tab + stage * L.tab_bytes);
-#pragma unroll 2
-        for (int q = 0; q < nq; ++q) {
-          const uint4 v = *reinterpret_cast<const uint4*>(xrow + 16 * q);
-          if (Elem<T>::kSigned) neg |= v.x | v.y | v.z | v.w;
-#pragma unroll
-          for (int e = 0; e < EQ; ++e) {
-            const double xd = converted<T>(v, e);
-#pragma unroll
-            for (int c = 0; c < CP; c += 2) {  // broadcast LDS.128 per 2 classes
-              const double2 t2 = *reinterpret_cast<const double2*>(tab + (EQ * q + e) * CP + c);
-              acc[c] = __dadd_rn(acc[c], __dmul_rn(xd, t2.x));
-              acc[c + 1] = __dadd_rn(acc[c + 1], __dmul_rn(xd, t2.y));
-            }
-          }
-        }
-      } else {
-        const GlobalTab tab{p.tab + s * slot_tab};
-#pragma unroll 1
-        for (int q = 0; q < nq; ++q) {
-          const uint4 v = *reinterpret_cast<const uint4*>(xrow + 16 * q);
-          if (Elem<T>::kSigned) neg |= v.x | v.y | v.z | v.w;
-          score_quad<CP, T>(acc, v, tab, EQ * q);
-        }
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[stage]);
-      if (++stage == ST) {
-        stage = 0;
-        phase ^= 1;
-      }
-      const int64_t r = tile * ROWS + row;
-      if (r < p.n_rows) write_row<CP>(p, r, slot, neg, acc);
-    }
-  }
-}
-
-// ------------------------------------------------------------------ generic kernel
-// Any layout (unaligned X, row pitch not a multiple of 16 B): one thread per
-// row, loads through L1.  Same arithmetic, same results; slower.
-template <int CP, typename T>
-__global__ void __launch_bounds__(256) predict_generic_kernel(const PredictParams p) {
-  const T* xbase = static_cast<const T*>(p.x);
-  for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r < p.n_rows;
-       r += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int sz = p.size[r];
-    const int slot = (sz >= 0 && sz < p.limit) ? p.route[sz / p.width] : -1;
-    const int s = max(slot, 0);
-    double acc[CP];
-#pragma unroll
-    for (int c = 0; c < CP; ++c) acc[c] = p.prior[s * CP + c];
-    const T* row = xbase + r * p.ldx;
-    uint32_t neg = 0;
-    const GlobalTab tab{p.tab + static_cast<int64_t>(s) * p.n_tab_blocks *
-                                    (kTabBlockFeatures * CP)};
-    for (int j = 0; j < p.n_features; ++j) {
-      const uint32_t x = static_cast<uint32_t>(__ldg(row + j));
-      if (Elem<T>::kSigned) neg |= x;
-      const double xd = __uint2double_rn(x);
-#pragma unroll
-      for (int c = 0; c < CP; ++c) acc[c] = __dadd_rn(acc[c], __dmul_rn(xd, tab.get(j * CP + c)));
-    }
-    write_row<CP>(p, r, slot, neg, acc);
-  }
-}
-
-// ------------------------------------------------------------------ launchers
-template <int CP, typename T, int R, int NW, int STAGES, bool GATHER, int B = 1>
-static cudaError_t launch_tma_mode(const PredictMaps& map, PredictParams p, cudaStream_t stream) {
-  using L = PredictSmem<CP, T, R, NW, STAGES, GATHER, B>;
-  auto kern = predict_tma_kernel<CP, T, R, NW, STAGES, GATHER, B>;
-  p.n_tiles = (p.n_rows + L::kRows - 1) / L::kRows;
-  p.n_chunks = (p.n_features + Elem<T>::kPerRow - 1) / Elem<T>::kPerRow;
-  static int per_sm = 0;  // resident CTAs per SM for this instantiation
-  static int sms = 0;
-  if (per_sm == 0) {
-    cudaError_t e =
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kAlloc);
-    if (e != cudaSuccess) return e;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, (NW + 1) * 32, L::kAlloc);
-    if (e != cudaSuccess) return e;
-    if (per_sm < 1) per_sm = 1;
-  }
-  const int64_t want = static_cast<int64_t>(sms) * per_sm;
-  const int grid = static_cast<int>(p.n_tiles < want ? p.n_tiles : want);
-  if (grid == 0) return cudaSuccess;
-  kern<<<grid, (NW + 1) * 32, L::kAlloc, stream>>>(map, p);
-  return cudaGetLastError();
-}
-
-// Gather mode: GNB_GATHER_B=2 stages two chunks of each gathered row (A/B).
-static int gather_boxes() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("GNB_GATHER_B");
-    v = e ? atoi(e) : 1;
-  }
-  return v;
-}
-
-template <int CP, typename T, int R, int NW, int STAGES, int B = 1>
-static cudaError_t launch_tma(const PredictMaps& map, const PredictParams& p,
-                              cudaStream_t stream) {
-  if (p.perm != nullptr)
-    return gather_boxes() == 2 ? launch_tma_mode<CP, T, R, NW, STAGES, true, 2>(map, p, stream)
-                               : launch_tma_mode<CP, T, R, NW, STAGES, true, 1>(map, p, stream);
-  return launch_tma_mode<CP, T, R, NW, STAGES, false, B>(map, p, stream);
-}
-
-// Row-box eligibility: whole rows of <= kRowBoxMaxQuads 16-B quads (odd-padded)
-// and at most 256 box columns (TMA limit).  GNB_PRED_ROWBOX=0 disables (A/B).
-constexpr int kRowBoxMaxQuads = 26;       // 128 rows x 26 x 16 B = 52 KB per stage
-constexpr uint32_t kRowBoxRingBytes = 53248;  // ring depth: stages x box ~ 52 KB
-
-int predict_rowbox_quads(int n_features, int x_type, int n_classes) {
-  static int enabled = -1;
-  if (enabled < 0) {
-    const char* e = getenv("GNB_PRED_ROWBOX");
-    enabled = e ? atoi(e) != 0 : 1;
-  }
-  (void)n_classes;
-  if (!enabled || n_features < 1) return 0;
-  const int eb = x_type == GNB_X_U8 ? 1 : x_type == GNB_X_U16 ? 2 : 4;
-  const int nq = (n_features * eb + 15) / 16;
-  const int wq = nq | 1;
-  if (wq > kRowBoxMaxQuads || wq * 16 / eb > 256) return 0;
-  return wq;
-}
-
-template <int CP, typename T, int AHEAD>
-static cudaError_t launch_rowbox_a(const PredictMaps& map, PredictParams p, cudaStream_t stream) {
-  auto kern = predict_rowbox_kernel<CP, T, AHEAD>;
-  static int sms = 0;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         227 * 1024);
-    if (e != cudaSuccess) return e;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    attr = true;
-  }
-  p.n_tiles = (p.n_rows + kRowBoxRows - 1) / kRowBoxRows;
-  const uint32_t box = static_cast<uint32_t>(kRowBoxRows) * p.rowbox_quads * 16;
-  int st = static_cast<int>(kRowBoxRingBytes / box);
-  static int st_env = -1;
-  if (st_env < 0) {
-    const char* e = getenv("GNB_ROWBOX_STAGES");
-    st_env = e ? atoi(e) : 0;
-  }
-  if (st_env > 0) st = st_env;
-  p.rowbox_stages = st < 2 ? 2 : st > 8 ? 8 : st;
-  const RowBoxSmem L(p.rowbox_quads,
-                     rowbox_tab_feats(p.n_features, Elem<T>::kPerQuad, p.n_tab_blocks), CP,
-                     p.rowbox_stages, AHEAD);
-  const size_t smem = L.total + 128;
-  int per_sm = 0;
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 5 * 32, smem);
-  if (e != cudaSuccess) return e;
-  if (per_sm < 1) return cudaErrorInvalidConfiguration;
-  const int64_t want = static_cast<int64_t>(sms) * per_sm;
-  const int grid = static_cast<int>(p.n_tiles < want ? p.n_tiles : want);
-  if (grid == 0) return cudaSuccess;
-  kern<<<grid, 5 * 32, smem, stream>>>(map, p);
-  return cudaGetLastError();
-}
-
-template <int CP, typename T>
-static cudaError_t launch_rowbox(const PredictMaps& map, const PredictParams& p,
-                                 cudaStream_t stream) {
-  static int ahead = -1;  // GNB_ROWBOX_AHEAD=4: deeper size prefetch (A/B)
-  if (ahead < 0) {
-    const char* e = getenv("GNB_ROWBOX_AHEAD");
-    ahead = e ? atoi(e) : 2;
-  }
-  return ahead == 4 ? launch_rowbox_a<CP, T, 4>(map, p, stream)
-                    : launch_rowbox_a<CP, T, 2>(map, p, stream);
-}
-
-template <int CP, typename T>
-static cudaError_t launch_generic(const PredictParams& p, cudaStream_t stream) {
-  const int64_t blocks64 = (p.n_rows + 255) / 256;
-  const int blocks = static_cast<int>(blocks64 < 148 * 16 ? blocks64 : 148 * 16);
-  if (blocks == 0) return cudaSuccess;
-  predict_generic_kernel<CP, T><<<blocks, 256, 0, stream>>>(p);
-  return cudaGetLastError();
-}
-
 int class_pad(int C) { return C <= 2 ? 2 : C <= 4 ? 4 : C <= 8 ? 8 : 16; }
 
 size_t packed_bytes(int S, int C, int F) {
@@ -796,24 +78,19 @@ cudaError_t pack_tables(const double* log_prior, const double* log_lik, int S, i
   return cudaGetLastError();
 }
 
-// K-PRED geometry for C = 2: rows per thread (R), consumer warps (NW), ring
-// stages; a few variants selectable with GNB_PRED_VARIANT (profiling only).
-// Default (variant 0) measured best on B200 for int32 X
-// (profiles/r01_tuning.md): 16-KB stages, 2 deep, 6 CTAs per SM.
-struct PredVariant {
-  int R, NW, STAGES;
-};
-static const PredVariant kCp2Variants[] = {{1, 4, 2}, {1, 4, 3}, {2, 2, 2}, {2, 4, 2},
-                                           {1, 4, 2}, {1, 4, 3}, {1, 4, 2}};  // 4-6: B=2,2,4
-
-static int cp2_variant() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("GNB_PRED_VARIANT");
-    v = e ? atoi(e) : 0;
-    if (v < 0 || v >= static_cast<int>(sizeof(kCp2Variants) / sizeof(kCp2Variants[0]))) v = 0;
+int predict_rowbox_quads(int n_features, int x_type, int n_classes) {
+  static int enabled = -1;
+  if (enabled < 0) {
+    const char* e = getenv("GNB_PRED_ROWBOX");
+    enabled = e ? atoi(e) != 0 : 1;
   }
-  return v;
+  (void)n_classes;
+  if (!enabled || n_features < 1) return 0;
+  const int eb = x_type == GNB_X_U8 ? 1 : x_type == GNB_X_U16 ? 2 : 4;
+  const int nq = (n_features * eb + 15) / 16;
+  const int wq = nq | 1;
+  if (wq > kRowBoxMaxQuads || wq * 16 / eb > 256) return 0;
+  return wq;
 }
 
 int predict_box_rows(int n_classes) {
@@ -823,49 +100,6 @@ int predict_box_rows(int n_classes) {
     return v.R * v.NW * 32;
   }
   return CP == 4 ? 2 * 4 * 32 : 128;
-}
-
-template <typename T>
-static cudaError_t launch_typed(const PredictMaps* map, const PredictParams& p, int CP,
-                                cudaStream_t stream) {
-  if (map != nullptr && p.rowbox_quads > 0 && p.perm == nullptr) {
-    switch (CP) {
-      case 2: return launch_rowbox<2, T>(*map, p, stream);
-      case 4: return launch_rowbox<4, T>(*map, p, stream);
-      case 8: return launch_rowbox<8, T>(*map, p, stream);
-      default: return launch_rowbox<16, T>(*map, p, stream);
-    }
-  }
-  if (map != nullptr) {
-    switch (CP) {
-      case 2:
-        switch (cp2_variant()) {
-          case 1: return launch_tma<2, T, 1, 4, 3>(*map, p, stream);
-          case 2: return launch_tma<2, T, 2, 2, 2>(*map, p, stream);
-          case 3: return launch_tma<2, T, 2, 4, 2>(*map, p, stream);
-          case 4: return launch_tma<2, T, 1, 4, 2, 2>(*map, p, stream);
-          case 5: return launch_tma<2, T, 1, 4, 3, 2>(*map, p, stream);
-          case 6: return launch_tma<2, T, 1, 4, 2, 4>(*map, p, stream);
-          default: {
-            // long rows (>= 12 chunks, e.g. int32 F >= 353): 2 chunks per stage
-            // (3 CTAs/SM), F=500/1000 0.85/0.90 -> 0.91/0.96 of HBM; shorter
-            // rows keep 1-chunk stages (F=200: 0.89 vs 0.77), r01_tuning.md
-            const int nch = (p.n_features + Elem<T>::kPerRow - 1) / Elem<T>::kPerRow;
-            if (nch >= 12) return launch_tma<2, T, 1, 4, 2, 2>(*map, p, stream);
-            return launch_tma<2, T, 1, 4, 2>(*map, p, stream);
-          }
-        }
-      case 4: return launch_tma<4, T, 2, 4, 3>(*map, p, stream);
-      case 8: return launch_tma<8, T, 1, 4, 4>(*map, p, stream);
-      default: return launch_tma<16, T, 1, 4, 4>(*map, p, stream);
-    }
-  }
-  switch (CP) {
-    case 2: return launch_generic<2, T>(p, stream);
-    case 4: return launch_generic<4, T>(p, stream);
-    case 8: return launch_generic<8, T>(p, stream);
-    default: return launch_generic<16, T>(p, stream);
-  }
 }
 
 cudaError_t predict_launch(const PredictMaps* map, PredictParams p, cudaStream_t stream,
@@ -880,10 +114,17 @@ cudaError_t predict_launch(const PredictMaps* map, PredictParams p, cudaStream_t
   p.n_tab_blocks = table_blocks(p.n_features);
   p.tab = p.prior + static_cast<int64_t>(p.n_slots) * CP;
   if (force_generic) map = nullptr;
+  const bool fma = p.mode == GNB_MODE_FMA;
   switch (p.x_type) {
-    case GNB_X_U16: return launch_typed<uint16_t>(map, p, CP, stream);
-    case GNB_X_U8: return launch_typed<uint8_t>(map, p, CP, stream);
-    default: return launch_typed<int32_t>(map, p, CP, stream);
+    case GNB_X_U16:
+      return fma ? launch_typed<uint16_t, true>(map, p, CP, stream)
+                 : launch_typed<uint16_t, false>(map, p, CP, stream);
+    case GNB_X_U8:
+      return fma ? launch_typed<uint8_t, true>(map, p, CP, stream)
+                 : launch_typed<uint8_t, false>(map, p, CP, stream);
+    default:
+      return fma ? launch_typed<int32_t, true>(map, p, CP, stream)
+                 : launch_typed<int32_t, false>(map, p, CP, stream);
   }
 }
 

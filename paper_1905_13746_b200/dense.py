@@ -112,7 +112,7 @@ def slot_sort(size_bytes: torch.Tensor, tables: DeviceTables, *, stream=None) ->
 
 def predict(x: torch.Tensor, size_bytes: torch.Tensor, tables: DeviceTables, *,
             logpost: bool = True, label_out=None, logpost_out=None, stream=None,
-            generic: bool = False, perm: torch.Tensor | None = None):
+            generic: bool = False, perm: torch.Tensor | None = None, mode: str = "exact"):
     """Score every row: label[N] int32 (class index, or -1 size out of range,
     -2 negative count) and, if requested, log-posteriors [N, C] fp64.
 
@@ -120,7 +120,11 @@ def predict(x: torch.Tensor, size_bytes: torch.Tensor, tables: DeviceTables, *,
     (extra columns beyond the model's features must be 0).  x may be int32,
     uint16 or uint8 (the same counts in fewer bytes; identical results).
     perm (from slot_sort): score in slot-grouped order -- for ragged batches
-    whose rows are not grouped by size group; results are identical."""
+    whose rows are not grouped by size group; results are identical.
+    mode: "exact" (default; the reference's mul-then-add roundings, bit-identical
+    log-posteriors) or "fma" (one fused rounding per term, ~1e-12 relative)."""
+    if mode not in ("exact", "fma"):
+        raise InvalidConfigError(f"mode must be 'exact' or 'fma', got {mode!r}")
     xp, n, F, ldx = _rows(x, dtypes=tuple(_X_TYPES))
     if F != tables.n_features:
         raise InvalidConfigError(f"x has {F} columns, tables have {tables.n_features} features")
@@ -135,7 +139,12 @@ def predict(x: torch.Tensor, size_bytes: torch.Tensor, tables: DeviceTables, *,
             tables.route.data_ptr(), tables.n_slots, tables.n_classes, tables.packed.data_ptr(),
             _vec(label, n, "label_out"), lp.data_ptr() if lp is not None else None,
             _stream(stream))
-    if generic:
+    if mode == "fma":
+        pp = _vec(perm, n, "perm") if perm is not None else None
+        a = list(args)
+        a[10:10] = [pp, N.GNB_MODE_FMA]   # after packed
+        N.check(N.lib.gnb_predict_mode(xp, _X_TYPES[x.dtype], *a), "gnb_predict_mode")
+    elif generic:
         if x.dtype != torch.int32:
             raise InvalidConfigError("generic=True is the int32 L1 test path")
         N.check(N.lib.gnb_predict_generic(xp, *args), "gnb_predict_generic")

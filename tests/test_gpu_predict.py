@@ -323,3 +323,53 @@ def test_slot_sort_and_permuted_predict(dtype, N):
     assert lab.cpu().numpy().tolist() == want.tolist()
     ok = want >= 0
     assert lp.cpu().numpy()[ok].tobytes() == wlp[ok].tobytes()
+
+
+@pytest.mark.parametrize("dtype", [torch.int32, torch.uint16, torch.uint8])
+@pytest.mark.parametrize("F,C", [(50, 2), (100, 3), (256, 2), (500, 2), (40, 16)])
+@pytest.mark.parametrize("order", ["grouped", "shuffled", "permuted"])
+def test_fma_mode_within_tolerance(dtype, F, C, order):
+    """GNB_MODE_FMA: one rounding per term.  Bar (north star):
+    log-posteriors within 1e-5 relative -- asserted far tighter, 1e-11 -- and
+    labels identical except where the top-two margin is below that error."""
+    rng = np.random.default_rng(F * 7 + C)
+    G = 6
+    prior, ll, route = _tables(rng, G, C, F, G)
+    N = 5000
+    size = np.sort(rng.integers(-100, G * 1000 + 100, size=N))
+    if order != "grouped":
+        size = rng.permutation(size)
+    hi = 200 if dtype == torch.uint8 else 3000
+    x = rng.integers(0, hi, size=(N, F))
+    x[rng.random((N, F)) < 0.5] = 0
+    dev = torch.device("cuda")
+    xd = torch.from_numpy(x.astype(np.int64)).to(dev).to(dtype)
+    sd = torch.from_numpy(size.astype(np.int32)).to(dev)
+    t = dense.DeviceTables.build(prior, ll, route, group_size_bytes=1000, max_size_bytes=G * 1000)
+    perm = dense.slot_sort(sd, t) if order == "permuted" else None
+    lab_e, lp_e = dense.predict(xd, sd, t, perm=perm)
+    lab_f, lp_f = dense.predict(xd, sd, t, perm=perm, mode="fma")
+    torch.cuda.synchronize()
+    lab_e, lp_e, lab_f, lp_f = (a.cpu().numpy() for a in (lab_e, lp_e, lab_f, lp_f))
+    want, wlp = O.predict_dense(x, size, route, prior, ll, width=1000, limit=G * 1000)
+    assert lab_e.tolist() == want.tolist()              # exact mode stays bit-exact
+    ok = want >= 0
+    assert lp_e[ok].tobytes() == wlp[ok].tobytes()
+    assert (lab_f[~ok] == want[~ok]).all() and np.isnan(lp_f[~ok]).all()
+    rel = np.abs(lp_f[ok] - wlp[ok]) / np.maximum(np.abs(wlp[ok]), 1e-300)
+    assert rel.max() < 1e-11
+    srt = np.sort(wlp[ok], axis=1)
+    margin = srt[:, -1] - srt[:, -2]
+    close = margin <= 1e-11 * np.abs(srt[:, -1]) * 4
+    assert (lab_f[ok][~close] == want[ok][~close]).all()
+
+
+def test_mode_rejects_unknown():
+    from paper_1905_13746_b200.errors import InvalidConfigError
+    rng = np.random.default_rng(0)
+    prior, ll, route = _tables(rng, 1, 2, 8, 1)
+    t = dense.DeviceTables.build(prior, ll, route, group_size_bytes=10, max_size_bytes=10)
+    x = torch.zeros((4, 8), dtype=torch.int32, device="cuda")
+    s = torch.zeros(4, dtype=torch.int32, device="cuda")
+    with pytest.raises(InvalidConfigError):
+        dense.predict(x, s, t, mode="fast")
