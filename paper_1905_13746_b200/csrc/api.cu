@@ -179,6 +179,17 @@ static int check_predict(const int32_t* x, int64_t n_rows, int32_t F, int64_t ld
   return GNB_OK;
 }
 
+// GNB_ROWBOX_BULK=0: row-box tiles through the 2-D tensor map even when the
+// rows are contiguous (A/B of the 1-D bulk copy).
+static bool rowbox_bulk() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("GNB_ROWBOX_BULK");
+    v = e ? atoi(e) != 0 : 1;
+  }
+  return v != 0;
+}
+
 static int predict_device(const void* x, int x_type, int64_t n_rows, int32_t F, int64_t ldx,
                           const int32_t* size, int32_t width, int32_t limit,
                           const int32_t* route, int32_t S, int32_t C, const void* packed,
@@ -223,6 +234,7 @@ static int predict_device(const void* x, int x_type, int64_t n_rows, int32_t F, 
         ok = encode_map(&map.tail, p.x, n, F, ldx, 1, true, x_type, 0, gather_tail_promo());
       if (!ok) return fail(GNB_ECUDA, "predict: cuTensorMapEncodeTiled failed");
       p.rowbox_quads = wq;
+      p.rowbox_contig = wq > 0 && ldx * eb == int64_t(wq) * 16 && rowbox_bulk();
       mp = &map;
     }
     GNB_CUDA(predict_launch(mp, p, stream, force_generic), "predict launch");

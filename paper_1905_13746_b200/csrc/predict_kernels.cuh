@@ -63,16 +63,27 @@ struct Elem<int32_t> {
 // is exact (counts < 2^32) and runs on the conversion unit (I2F.F64; for
 // uint8/uint16 with a byte/half-word source select), so the product below is
 // ONE DMUL rounding, exactly the reference's `n * ll` (a Python float multiply).
-template <typename T>
+//
+// CVT selects the conversion unit (row-box kernel): 0 = I2F.F64 (XU pipe) for
+// every element; 1 = the exact magic-number form (2^52 + x) - 2^52 built with
+// an integer move and one DADD (FP64 pipe), no XU; 2 = alternate the two by
+// element parity, splitting the conversions between the XU and FP64 pipes.
+// All three give the same double (x < 2^32 is exact in every form).
+__device__ __forceinline__ double u32_to_double_magic(uint32_t x) {
+  return __dsub_rn(__hiloint2double(0x43300000, static_cast<int>(x)), 4503599627370496.0);
+}
+
+template <typename T, int CVT = 0>
 __device__ __forceinline__ double converted(const uint4& v, int e) {
   constexpr int sz = static_cast<int>(sizeof(T));
   const uint32_t w = (e * sz) < 4 ? v.x : (e * sz) < 8 ? v.y : (e * sz) < 12 ? v.z : v.w;
-  if constexpr (sz == 4) {
-    return __uint2double_rn(w);
-  } else {
+  uint32_t x = w;
+  if constexpr (sz != 4) {
     constexpr int bits = 8 * sz;
-    return __uint2double_rn((w >> ((e * bits) & 31)) & ((1u << bits) - 1u));
+    x = (w >> ((e * bits) & 31)) & ((1u << bits) - 1u);
   }
+  if (CVT == 1 || (CVT == 2 && (e & 1))) return u32_to_double_magic(x);
+  return __uint2double_rn(x);
 }
 
 // ------------------------------------------------------------------ inner loops
@@ -167,7 +178,8 @@ struct PredictSmem {
   static constexpr int kBox = kRows * kChunkBytesPerRow;               // one box
   static constexpr int kXBytes = B * kBox;                             // one stage
   static constexpr int kTabChunk = Elem<T>::kPerRow * CP * 8;          // one chunk's table
-  static constexpr int kTabBytes = B * kTabChunk;                      // one stage's tables
+  static constexpr int kPrior = CP * 8;                                // the slot's prior
+  static constexpr int kTabBytes = kPrior + B * kTabChunk;             // prior + tables
   // tile_slot + row_slot[kRows] (+ row_id[kRows] in gather mode)
   static constexpr int kHdrBytes = ((4 + kRows * 4 * (GATHER ? 2 : 1)) + 15) / 16 * 16;
   static constexpr int kX = 0;
@@ -330,15 +342,20 @@ __global__ void __launch_bounds__((NW + 1) * 32)
         __syncwarp();
         uint8_t* box = smem + L::kX + stage * L::kXBytes;
         if (lane == 0) {
-          const uint32_t bytes = nb * (L::kBox + (tile_slot >= 0 ? L::kTabChunk : 0));
+          const uint32_t bytes = nb * (L::kBox + (tile_slot >= 0 ? L::kTabChunk : 0)) +
+                                 (tile_slot >= 0 && ch == 0 ? L::kPrior : 0);
           mbar_arrive_expect_tx(&full[stage], bytes);
           if (!GATHER)
             for (int b = 0; b < nb; ++b)
               tma_load_2d(box + b * L::kBox, &xmap, (ch + b) * CF, static_cast<int32_t>(r0),
                           &full[stage], pol_x);
-          if (tile_slot >= 0)
-            bulk_load(smem + L::kTab + stage * L::kTabBytes, chunk_table<CP, T>(p, tile_slot, ch),
-                      nb * L::kTabChunk, &full[stage], pol_t);
+          if (tile_slot >= 0) {
+            uint8_t* dst = smem + L::kTab + stage * L::kTabBytes;
+            if (ch == 0)  // first stage of the tile: the slot's prior too
+              bulk_load(dst, p.prior + tile_slot * CP, L::kPrior, &full[stage], pol_t);
+            bulk_load(dst + L::kPrior, chunk_table<CP, T>(p, tile_slot, ch), nb * L::kTabChunk,
+                      &full[stage], pol_t);
+          }
         }
         if (GATHER) {
           __syncwarp();  // expect_tx precedes every completion
@@ -387,8 +404,10 @@ __global__ void __launch_bounds__((NW + 1) * 32)
             slot[i] = hdr->row_slot[rows[i]];
             rid[i] = GATHER ? hdr->row_slot[ROWS + rows[i]] : 0;
             const int s = ts >= 0 ? ts : max(slot[i], 0);
+            const double* sp =
+                reinterpret_cast<const double*>(smem + L::kTab + stage * L::kTabBytes);
 #pragma unroll
-            for (int c = 0; c < CP; ++c) acc[i][c] = __ldg(p.prior + s * CP + c);
+            for (int c = 0; c < CP; ++c) acc[i][c] = ts >= 0 ? sp[c] : __ldg(p.prior + s * CP + c);
           }
         }
 #pragma unroll
@@ -402,7 +421,7 @@ __global__ void __launch_bounds__((NW + 1) * 32)
             score_chunk_uniform<CP, T, R, FMA>(
                 acc, box, rows,
                 reinterpret_cast<const double*>(smem + L::kTab + stage * L::kTabBytes +
-                                                b * L::kTabChunk),
+                                                L::kPrior + b * L::kTabChunk),
                 nq, neg);
           } else {
             score_chunk_mixed<CP, T, R, FMA>(p, acc, box, rows, slot, ch, nq, neg);
@@ -441,7 +460,8 @@ struct RowBoxSmem {
   // ahead: tiles whose row sizes are in flight ahead of routing
   __host__ __device__ RowBoxSmem(int wq, int tab_feats, int cp, int stages, int ahead) {
     x_bytes = static_cast<uint32_t>(kRowBoxRows) * wq * 16;
-    tab_bytes = static_cast<uint32_t>(tab_feats) * cp * 8;
+    // [prior: cp doubles][tab_feats x cp log-likelihoods] per stage
+    tab_bytes = static_cast<uint32_t>(cp) * 8 + static_cast<uint32_t>(tab_feats) * cp * 8;
     hdr_bytes = (4 + kRowBoxRows * 4 + 15) / 16 * 16;
     x = 0;
     tab = x + stages * x_bytes;
@@ -458,7 +478,7 @@ __host__ __device__ inline int rowbox_tab_feats(int F, int EQ, int n_tab_blocks)
   return want < have ? want : have;
 }
 
-template <int CP, typename T, int kRowBoxAhead, bool FMA>
+template <int CP, typename T, int kRowBoxAhead, bool FMA, int CVT>
 __global__ void __launch_bounds__(5 * 32)
     predict_rowbox_kernel(const __grid_constant__ PredictMaps maps, const PredictParams p) {
   const CUtensorMap& xmap = maps.main;
@@ -537,12 +557,25 @@ __global__ void __launch_bounds__(5 * 32)
       if (lane == 0) hdr[0] = tile_slot;
       __syncwarp();
       if (lane == 0) {
-        mbar_arrive_expect_tx(&full[stage], L.x_bytes + (tile_slot >= 0 ? L.tab_bytes : 0));
-        tma_load_2d(smem + L.x + stage * L.x_bytes, &xmap, 0, static_cast<int32_t>(r0),
-                    &full[stage], pol_x);
-        if (tile_slot >= 0)
-          bulk_load(smem + L.tab + stage * L.tab_bytes, p.tab + tile_slot * slot_tab,
-                    L.tab_bytes, &full[stage], pol_t);
+        if (p.rowbox_contig) {
+          // rows are contiguous in HBM with the smem pitch: the tile is ONE
+          // 1-D bulk copy (no per-row box traffic); only the valid rows
+          const int64_t nr = p.n_rows - r0 < ROWS ? p.n_rows - r0 : ROWS;
+          const uint32_t xb = static_cast<uint32_t>(nr) * WQ * 16;
+          mbar_arrive_expect_tx(&full[stage], xb + (tile_slot >= 0 ? L.tab_bytes : 0));
+          bulk_load(smem + L.x + stage * L.x_bytes,
+                    static_cast<const uint8_t*>(p.x) + r0 * (WQ * 16), xb, &full[stage], pol_x);
+        } else {
+          mbar_arrive_expect_tx(&full[stage], L.x_bytes + (tile_slot >= 0 ? L.tab_bytes : 0));
+          tma_load_2d(smem + L.x + stage * L.x_bytes, &xmap, 0, static_cast<int32_t>(r0),
+                      &full[stage], pol_x);
+        }
+        if (tile_slot >= 0) {  // the slot's prior, then its table
+          uint8_t* dst = smem + L.tab + stage * L.tab_bytes;
+          bulk_load(dst, p.prior + tile_slot * CP, CP * 8, &full[stage], pol_t);
+          bulk_load(dst + CP * 8, p.tab + tile_slot * slot_tab, L.tab_bytes - CP * 8,
+                    &full[stage], pol_t);
+        }
       } else {
         mbar_arrive(&full[stage]);
       }
@@ -564,19 +597,22 @@ __global__ void __launch_bounds__(5 * 32)
       const int slot = hdr[1 + row];
       const int s = ts >= 0 ? ts : max(slot, 0);
       double acc[CP];
+      const double* stab = reinterpret_cast<const double*>(smem + L.tab + stage * L.tab_bytes);
+      // uniform tile: the prior came with the table (smem broadcast, no global
+      // round trip in front of the first DADD); mixed tile: per-row L1 load
 #pragma unroll
-      for (int c = 0; c < CP; ++c) acc[c] = __ldg(p.prior + s * CP + c);
+      for (int c = 0; c < CP; ++c) acc[c] = ts >= 0 ? stab[c] : __ldg(p.prior + s * CP + c);
       uint32_t neg = 0;
       const uint8_t* xrow = smem + L.x + stage * L.x_bytes + row * (WQ * 16);
       if (ts >= 0) {
-        const double* tab = reinterpret_cast<const double*>(smem + L.tab + stage * L.tab_bytes);
+        const double* tab = stab + CP;
 #pragma unroll 2
         for (int q = 0; q < nq; ++q) {
           const uint4 v = *reinterpret_cast<const uint4*>(xrow + 16 * q);
           if (Elem<T>::kSigned) neg |= v.x | v.y | v.z | v.w;
 #pragma unroll
           for (int e = 0; e < EQ; ++e) {
-            const double xd = converted<T>(v, e);
+            const double xd = converted<T, CVT>(v, e);
 #pragma unroll
             for (int c = 0; c < CP; c += 2) {  // broadcast LDS.128 per 2 classes
               const double2 t2 = *reinterpret_cast<const double2*>(tab + (EQ * q + e) * CP + c);
@@ -687,9 +723,9 @@ static cudaError_t launch_tma(const PredictMaps& map, const PredictParams& p,
 inline constexpr int kRowBoxMaxQuads = 26;       // 128 rows x 26 x 16 B = 52 KB per stage
 inline constexpr uint32_t kRowBoxRingBytes = 53248;  // ring depth: stages x box ~ 52 KB
 
-template <int CP, typename T, int AHEAD, bool FMA>
+template <int CP, typename T, int AHEAD, bool FMA, int CVT>
 static cudaError_t launch_rowbox_a(const PredictMaps& map, PredictParams p, cudaStream_t stream) {
-  auto kern = predict_rowbox_kernel<CP, T, AHEAD, FMA>;
+  auto kern = predict_rowbox_kernel<CP, T, AHEAD, FMA, CVT>;
   static int sms = 0;
   static bool attr = false;
   if (!attr) {
@@ -726,16 +762,27 @@ static cudaError_t launch_rowbox_a(const PredictMaps& map, PredictParams p, cuda
   return cudaGetLastError();
 }
 
+inline int rowbox_cvt() {  // GNB_ROWBOX_CVT=0/1/2: conversion unit (A/B), see converted()
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("GNB_ROWBOX_CVT");
+    v = e ? atoi(e) : 0;
+    if (v < 0 || v > 2) v = 0;
+  }
+  return v;
+}
+
 template <int CP, typename T, bool FMA>
 static cudaError_t launch_rowbox(const PredictMaps& map, const PredictParams& p,
                                  cudaStream_t stream) {
-  static int ahead = -1;  // GNB_ROWBOX_AHEAD=4: deeper size prefetch (A/B)
-  if (ahead < 0) {
-    const char* e = getenv("GNB_ROWBOX_AHEAD");
-    ahead = e ? atoi(e) : 2;
+  if constexpr (CP == 2) {
+    switch (rowbox_cvt()) {
+      case 1: return launch_rowbox_a<CP, T, 2, FMA, 1>(map, p, stream);
+      case 2: return launch_rowbox_a<CP, T, 2, FMA, 2>(map, p, stream);
+      default: break;
+    }
   }
-  return ahead == 4 ? launch_rowbox_a<CP, T, 4, FMA>(map, p, stream)
-                    : launch_rowbox_a<CP, T, 2, FMA>(map, p, stream);
+  return launch_rowbox_a<CP, T, 2, FMA, 0>(map, p, stream);
 }
 
 template <int CP, typename T, bool FMA>
