@@ -550,7 +550,8 @@ def _timed_launches(fn, steps, warmup, flush_bytes=512 << 20):
     """Mean device time (ms) of fn() over `steps` launches, L2 flushed before each
     (a 512 MB write, > 126 MB L2; in "clean" mode followed by a 256 MB read of a
     second buffer so the flush's dirty lines are written back before the timed
-    region, not inside it), CUDA events on the launching stream."""
+    region, not inside it), CUDA events on the launching stream, with the
+    launch already queued behind a short device sleep when the first event fires."""
     import torch
     flush = torch.empty(flush_bytes // 4, dtype=torch.int32, device="cuda")
     clean = torch.ones(flush_bytes // 8, dtype=torch.int32, device="cuda")
@@ -563,6 +564,10 @@ def _timed_launches(fn, steps, warmup, flush_bytes=512 << 20):
         flush.zero_()
         if FLUSH_MODE == "clean":
             torch.sum(clean, 0, out=sink)
+        # keep the GPU busy ~50 us so the host has enqueued fn()'s launch before
+        # event a fires: the events then bracket device time only, not the
+        # Python/ctypes launch path of a 40-700 us kernel
+        torch.cuda._sleep(100_000)
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(s)
         fn()

@@ -34,6 +34,7 @@ struct PredictParams {
   int32_t rowbox_quads;  // > 0: row-box mode, smem row = this many 16-B quads (odd)
   int32_t rowbox_stages; // row-box ring depth, set by predict_launch
   int32_t rowbox_contig; // row box: HBM row pitch == smem row pitch -> 1-D bulk tile copy
+  int32_t rowbox_resident; // row box: all slot tables resident in smem, set by predict_launch
   int32_t mode;          // GNB_MODE_EXACT (reference roundings) or GNB_MODE_FMA
 };
 

@@ -63,27 +63,16 @@ struct Elem<int32_t> {
 // is exact (counts < 2^32) and runs on the conversion unit (I2F.F64; for
 // uint8/uint16 with a byte/half-word source select), so the product below is
 // ONE DMUL rounding, exactly the reference's `n * ll` (a Python float multiply).
-//
-// CVT selects the conversion unit (row-box kernel): 0 = I2F.F64 (XU pipe) for
-// every element; 1 = the exact magic-number form (2^52 + x) - 2^52 built with
-// an integer move and one DADD (FP64 pipe), no XU; 2 = alternate the two by
-// element parity, splitting the conversions between the XU and FP64 pipes.
-// All three give the same double (x < 2^32 is exact in every form).
-__device__ __forceinline__ double u32_to_double_magic(uint32_t x) {
-  return __dsub_rn(__hiloint2double(0x43300000, static_cast<int>(x)), 4503599627370496.0);
-}
-
-template <typename T, int CVT = 0>
+template <typename T>
 __device__ __forceinline__ double converted(const uint4& v, int e) {
   constexpr int sz = static_cast<int>(sizeof(T));
   const uint32_t w = (e * sz) < 4 ? v.x : (e * sz) < 8 ? v.y : (e * sz) < 12 ? v.z : v.w;
-  uint32_t x = w;
-  if constexpr (sz != 4) {
+  if constexpr (sz == 4) {
+    return __uint2double_rn(w);
+  } else {
     constexpr int bits = 8 * sz;
-    x = (w >> ((e * bits) & 31)) & ((1u << bits) - 1u);
+    return __uint2double_rn((w >> ((e * bits) & 31)) & ((1u << bits) - 1u));
   }
-  if (CVT == 1 || (CVT == 2 && (e & 1))) return u32_to_double_magic(x);
-  return __uint2double_rn(x);
 }
 
 // ------------------------------------------------------------------ inner loops
@@ -448,23 +437,40 @@ __global__ void __launch_bounds__((NW + 1) * 32)
 }
 
 // ------------------------------------------------------------------ row-box kernel
-// Short rows (F <= ~100 int32 features): one TMA box holds kRowBoxRows whole
-// rows, unswizzled, WQ 16-B quads per smem row with WQ odd so the 8 lanes of an
-// LDS.128 phase (consecutive rows, stride WQ*16 B) hit 8 distinct bank groups.
-// One stage per tile, no partial 128-B chunks: the 128-B-box kernel above
-// spends a whole 16-KB stage on e.g. the 18 trailing features of F=50, so short
-// rows kept too few bytes in flight per SM.  Ring depth and CTAs per SM follow
-// the box size (predict_launch).  Same arithmetic and order as every path.
+// Short rows (F <= ~100 int32 features): one stage holds kRowBoxRows whole
+// rows, WQ 16-B quads per smem row with WQ odd so the 8 lanes of an LDS.128
+// phase (consecutive rows, stride WQ*16 B) hit 8 distinct bank groups.  When
+// the HBM row pitch equals WQ*16 B the tile is one contiguous 1-D bulk copy;
+// otherwise a 2-D tensor box (unswizzled).  One stage per tile, no partial
+// 128-B chunks: the 128-B-box kernel above spends a whole 16-KB stage on e.g.
+// the 18 trailing features of F=50, so short rows kept too few bytes in flight
+// per SM.  Same arithmetic and order as every path.
+//
+// Resident tables (p.rowbox_resident): every slot's prior + table is copied
+// into smem once per CTA, so a stage carries X only.  Rows of <= kRegQuads
+// quads are then moved to registers and the stage is released BEFORE the
+// DMUL/DADD chain runs: a stage is held for a few LDS instead of the whole
+// scoring time, which is what bounds the bytes in flight per SM for short rows.
+// Register budget (__launch_bounds__(160, 4): <= 102 per thread): 13 quads of
+// X next to 2 accumulators (14 spill), 8 next to 4; wider class pads keep the
+// stage.
+template <int CP>
+inline constexpr int kRegQuads = CP <= 2 ? 13 : CP == 4 ? 8 : 0;
+
 struct RowBoxSmem {
-  uint32_t x_bytes, tab_bytes, hdr_bytes, x, tab, hdr, sizes, bar, total;
-  // ahead: tiles whose row sizes are in flight ahead of routing
-  __host__ __device__ RowBoxSmem(int wq, int tab_feats, int cp, int stages, int ahead) {
+  uint32_t x_bytes, tab_bytes, hdr_bytes, res_stride, x, res, tab, hdr, sizes, bar, total;
+  // ahead: tiles whose row sizes are in flight ahead of routing;
+  // resident_slots > 0: all slot tables resident (no per-stage tables)
+  __host__ __device__ RowBoxSmem(int wq, int tab_feats, int cp, int stages, int ahead,
+                                 int resident_slots) {
     x_bytes = static_cast<uint32_t>(kRowBoxRows) * wq * 16;
-    // [prior: cp doubles][tab_feats x cp log-likelihoods] per stage
-    tab_bytes = static_cast<uint32_t>(cp) * 8 + static_cast<uint32_t>(tab_feats) * cp * 8;
+    // one slot = [prior: cp doubles][tab_feats x cp log-likelihoods]
+    res_stride = static_cast<uint32_t>(1 + tab_feats) * cp;  // doubles
+    tab_bytes = resident_slots > 0 ? 0u : res_stride * 8;
     hdr_bytes = (4 + kRowBoxRows * 4 + 15) / 16 * 16;
     x = 0;
-    tab = x + stages * x_bytes;
+    res = x + stages * x_bytes;
+    tab = res + static_cast<uint32_t>(resident_slots) * res_stride * 8;
     hdr = tab + stages * tab_bytes;
     sizes = hdr + stages * hdr_bytes;  // [ahead][kRowBoxRows] prefetched sizes
     bar = sizes + ahead * kRowBoxRows * 4;
@@ -478,8 +484,30 @@ __host__ __device__ inline int rowbox_tab_feats(int F, int EQ, int n_tab_blocks)
   return want < have ? want : have;
 }
 
-template <int CP, typename T, int kRowBoxAhead, bool FMA, int CVT>
-__global__ void __launch_bounds__(5 * 32)
+// the nq quads of one row against one slot's smem table (prior excluded)
+template <int CP, typename T, bool FMA>
+__device__ __forceinline__ void rowbox_score_smem(double (&acc)[CP], const uint8_t* xrow,
+                                                  const double* tab, int nq, uint32_t& neg) {
+  constexpr int EQ = Elem<T>::kPerQuad;
+#pragma unroll 2
+  for (int q = 0; q < nq; ++q) {
+    const uint4 v = *reinterpret_cast<const uint4*>(xrow + 16 * q);
+    if (Elem<T>::kSigned) neg |= v.x | v.y | v.z | v.w;
+#pragma unroll
+    for (int e = 0; e < EQ; ++e) {
+      const double xd = converted<T>(v, e);
+#pragma unroll
+      for (int c = 0; c < CP; c += 2) {  // broadcast LDS.128 per 2 classes
+        const double2 t2 = *reinterpret_cast<const double2*>(tab + (EQ * q + e) * CP + c);
+        acc[c] = madd<FMA>(acc[c], xd, t2.x);
+        acc[c + 1] = madd<FMA>(acc[c + 1], xd, t2.y);
+      }
+    }
+  }
+}
+
+template <int CP, typename T, int kRowBoxAhead, bool FMA>
+__global__ void __launch_bounds__(5 * 32, 4)
     predict_rowbox_kernel(const __grid_constant__ PredictMaps maps, const PredictParams p) {
   const CUtensorMap& xmap = maps.main;
   constexpr int NW = 4, ROWS = kRowBoxRows, EQ = Elem<T>::kPerQuad;
@@ -488,21 +516,39 @@ __global__ void __launch_bounds__(5 * 32)
   uint8_t* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
   const int ST = p.rowbox_stages, WQ = p.rowbox_quads;
   const int tab_feats = rowbox_tab_feats(p.n_features, EQ, p.n_tab_blocks);
-  const RowBoxSmem L(WQ, tab_feats, CP, ST, kRowBoxAhead);
+  const bool resident = p.rowbox_resident != 0;
+  const RowBoxSmem L(WQ, tab_feats, CP, ST, kRowBoxAhead, resident ? p.n_slots : 0);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.bar);
   uint64_t* empty = full + ST;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < ST; ++s) {
-      mbar_init(&full[s], 32);
-      mbar_init(&empty[s], NW);
-    }
-    mbar_fence_init();
-  }
-  if (warp == NW && lane == 0) prefetch_tensormap(&xmap);
-  __syncthreads();
-  const int64_t n_tiles = p.n_tiles;
   const int64_t slot_tab = static_cast<int64_t>(p.n_tab_blocks) * kTabBlockFeatures * CP;
+  // Prologue: the producer initialises the barriers and starts streaming at
+  // once; the consumers copy the resident tables meanwhile and wait (named
+  // barrier 1) for the producer's init and each other's copies -- the first X
+  // copies do not queue behind the table loads.
+  if (warp == NW) {
+    if (lane == 0) {
+      for (int s = 0; s < ST; ++s) {
+        mbar_init(&full[s], 32);
+        mbar_init(&empty[s], NW);
+      }
+      mbar_fence_init();
+      prefetch_tensormap(&xmap);
+    }
+    __syncwarp();
+    named_bar_arrive(1, (NW + 1) * 32);
+  } else {
+    if (resident) {  // all slots' [prior | table] once per CTA
+      double* res = reinterpret_cast<double*>(smem + L.res);
+      const int stride = static_cast<int>(L.res_stride);
+      for (int i = threadIdx.x; i < p.n_slots * stride; i += NW * 32) {
+        const int s = i / stride, k = i - s * stride;
+        res[i] = k < CP ? __ldg(p.prior + s * CP + k) : __ldg(p.tab + s * slot_tab + (k - CP));
+      }
+    }
+    named_bar_sync(1, (NW + 1) * 32);
+  }
+  const int64_t n_tiles = p.n_tiles;
 
   if (warp == NW) {
     // ---------------------------------------------------------- producer
@@ -530,6 +576,25 @@ __global__ void __launch_bounds__(5 * 32)
     int k_cur = 0;
     for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
       const int64_t r0 = tile * ROWS;
+      // X first: it does not depend on routing, so the copy is in flight while
+      // the producer waits for the tile's sizes and routes them (this also
+      // takes the size + route round trips out of the kernel's ramp).
+      mbar_wait(&empty[stage], phase ^ 1);
+      if (lane == 0) {
+        if (p.rowbox_contig) {
+          // rows are contiguous in HBM with the smem pitch: the tile is ONE
+          // 1-D bulk copy (no per-row box traffic); only the valid rows
+          const int64_t nr = p.n_rows - r0 < ROWS ? p.n_rows - r0 : ROWS;
+          const uint32_t xb = static_cast<uint32_t>(nr) * WQ * 16;
+          mbar_expect_tx(&full[stage], xb);
+          bulk_load(smem + L.x + stage * L.x_bytes,
+                    static_cast<const uint8_t*>(p.x) + r0 * (WQ * 16), xb, &full[stage], pol_x);
+        } else {
+          mbar_expect_tx(&full[stage], L.x_bytes);
+          tma_load_2d(smem + L.x + stage * L.x_bytes, &xmap, 0, static_cast<int32_t>(r0),
+                      &full[stage], pol_x);
+        }
+      }
       int slots[ROWS / 32];
       int lo = INT_MAX, hi = INT_MIN;
       cp_async_wait<kRowBoxAhead - 1>();
@@ -550,27 +615,15 @@ __global__ void __launch_bounds__(5 * 32)
       lo = __reduce_min_sync(0xffffffffu, lo);
       hi = __reduce_max_sync(0xffffffffu, hi);
       const int tile_slot = (lo == INT_MAX) ? 0 : (lo == hi ? lo : -1);
-      mbar_wait(&empty[stage], phase ^ 1);
       int* hdr = reinterpret_cast<int*>(smem + L.hdr + stage * L.hdr_bytes);
 #pragma unroll
       for (int i = 0; i < ROWS / 32; ++i) hdr[1 + lane + 32 * i] = slots[i];
       if (lane == 0) hdr[0] = tile_slot;
       __syncwarp();
       if (lane == 0) {
-        if (p.rowbox_contig) {
-          // rows are contiguous in HBM with the smem pitch: the tile is ONE
-          // 1-D bulk copy (no per-row box traffic); only the valid rows
-          const int64_t nr = p.n_rows - r0 < ROWS ? p.n_rows - r0 : ROWS;
-          const uint32_t xb = static_cast<uint32_t>(nr) * WQ * 16;
-          mbar_arrive_expect_tx(&full[stage], xb + (tile_slot >= 0 ? L.tab_bytes : 0));
-          bulk_load(smem + L.x + stage * L.x_bytes,
-                    static_cast<const uint8_t*>(p.x) + r0 * (WQ * 16), xb, &full[stage], pol_x);
-        } else {
-          mbar_arrive_expect_tx(&full[stage], L.x_bytes + (tile_slot >= 0 ? L.tab_bytes : 0));
-          tma_load_2d(smem + L.x + stage * L.x_bytes, &xmap, 0, static_cast<int32_t>(r0),
-                      &full[stage], pol_x);
-        }
-        if (tile_slot >= 0) {  // the slot's prior, then its table
+        const bool stage_tab = !resident && tile_slot >= 0;
+        mbar_arrive_expect_tx(&full[stage], stage_tab ? L.tab_bytes : 0);
+        if (stage_tab) {  // the slot's prior, then its table
           uint8_t* dst = smem + L.tab + stage * L.tab_bytes;
           bulk_load(dst, p.prior + tile_slot * CP, CP * 8, &full[stage], pol_t);
           bulk_load(dst + CP * 8, p.tab + tile_slot * slot_tab, L.tab_bytes - CP * 8,
@@ -588,6 +641,9 @@ __global__ void __launch_bounds__(5 * 32)
     // ---------------------------------------------------------- consumers
     const int row = lane + 32 * warp;
     const int nq = (p.n_features + EQ - 1) / EQ;
+    constexpr int RQ = kRegQuads<CP>;
+    const bool early = RQ > 0 && resident && nq <= RQ;
+    const double* res = reinterpret_cast<const double*>(smem + L.res);
     int stage = 0;
     uint32_t phase = 0;
     for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
@@ -597,41 +653,70 @@ __global__ void __launch_bounds__(5 * 32)
       const int slot = hdr[1 + row];
       const int s = ts >= 0 ? ts : max(slot, 0);
       double acc[CP];
-      const double* stab = reinterpret_cast<const double*>(smem + L.tab + stage * L.tab_bytes);
-      // uniform tile: the prior came with the table (smem broadcast, no global
-      // round trip in front of the first DADD); mixed tile: per-row L1 load
-#pragma unroll
-      for (int c = 0; c < CP; ++c) acc[c] = ts >= 0 ? stab[c] : __ldg(p.prior + s * CP + c);
       uint32_t neg = 0;
       const uint8_t* xrow = smem + L.x + stage * L.x_bytes + row * (WQ * 16);
-      if (ts >= 0) {
-        const double* tab = stab + CP;
-#pragma unroll 2
-        for (int q = 0; q < nq; ++q) {
-          const uint4 v = *reinterpret_cast<const uint4*>(xrow + 16 * q);
-          if (Elem<T>::kSigned) neg |= v.x | v.y | v.z | v.w;
+      bool released = false;
+      if constexpr (RQ > 0) {
+        if (early) {
+          // row -> registers, release the stage, then score from registers
+          uint4 v[RQ];
 #pragma unroll
-          for (int e = 0; e < EQ; ++e) {
-            const double xd = converted<T, CVT>(v, e);
+          for (int q = 0; q < RQ; ++q)
+            if (q < nq) v[q] = *reinterpret_cast<const uint4*>(xrow + 16 * q);
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty[stage]);
+          released = true;
+          const double* st = res + s * static_cast<int>(L.res_stride);
 #pragma unroll
-            for (int c = 0; c < CP; c += 2) {  // broadcast LDS.128 per 2 classes
-              const double2 t2 = *reinterpret_cast<const double2*>(tab + (EQ * q + e) * CP + c);
-              acc[c] = madd<FMA>(acc[c], xd, t2.x);
-              acc[c + 1] = madd<FMA>(acc[c + 1], xd, t2.y);
+          for (int c = 0; c < CP; ++c) acc[c] = st[c];
+          const double* tab = st + CP;
+#pragma unroll
+          for (int q = 0; q < RQ; ++q) {
+            if (q < nq) {
+              if (Elem<T>::kSigned) neg |= v[q].x | v[q].y | v[q].z | v[q].w;
+#pragma unroll
+              for (int e = 0; e < EQ; ++e) {
+                const double xd = converted<T>(v[q], e);
+#pragma unroll
+                for (int c = 0; c < CP; c += 2) {
+                  const double2 t2 =
+                      *reinterpret_cast<const double2*>(tab + (EQ * q + e) * CP + c);
+                  acc[c] = madd<FMA>(acc[c], xd, t2.x);
+                  acc[c + 1] = madd<FMA>(acc[c + 1], xd, t2.y);
+                }
+              }
             }
           }
         }
-      } else {
-        const GlobalTab tab{p.tab + s * slot_tab};
-#pragma unroll 1
-        for (int q = 0; q < nq; ++q) {
-          const uint4 v = *reinterpret_cast<const uint4*>(xrow + 16 * q);
-          if (Elem<T>::kSigned) neg |= v.x | v.y | v.z | v.w;
-          score_quad<CP, T, GlobalTab, FMA>(acc, v, tab, EQ * q);
-        }
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[stage]);
+      if (!released) {
+        if (resident) {
+          const double* st = res + s * static_cast<int>(L.res_stride);
+#pragma unroll
+          for (int c = 0; c < CP; ++c) acc[c] = st[c];
+          rowbox_score_smem<CP, T, FMA>(acc, xrow, st + CP, nq, neg);
+        } else {
+          const double* stab =
+              reinterpret_cast<const double*>(smem + L.tab + stage * L.tab_bytes);
+          // uniform tile: the prior came with the table (smem broadcast, no
+          // global round trip in front of the first DADD); mixed tile: L1 loads
+#pragma unroll
+          for (int c = 0; c < CP; ++c) acc[c] = ts >= 0 ? stab[c] : __ldg(p.prior + s * CP + c);
+          if (ts >= 0) {
+            rowbox_score_smem<CP, T, FMA>(acc, xrow, stab + CP, nq, neg);
+          } else {
+            const GlobalTab tab{p.tab + s * slot_tab};
+#pragma unroll 1
+            for (int q = 0; q < nq; ++q) {
+              const uint4 v = *reinterpret_cast<const uint4*>(xrow + 16 * q);
+              if (Elem<T>::kSigned) neg |= v.x | v.y | v.z | v.w;
+              score_quad<CP, T, GlobalTab, FMA>(acc, v, tab, EQ * q);
+            }
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[stage]);
+      }
       if (++stage == ST) {
         stage = 0;
         phase ^= 1;
@@ -723,9 +808,9 @@ static cudaError_t launch_tma(const PredictMaps& map, const PredictParams& p,
 inline constexpr int kRowBoxMaxQuads = 26;       // 128 rows x 26 x 16 B = 52 KB per stage
 inline constexpr uint32_t kRowBoxRingBytes = 53248;  // ring depth: stages x box ~ 52 KB
 
-template <int CP, typename T, int AHEAD, bool FMA, int CVT>
+template <int CP, typename T, int AHEAD, bool FMA>
 static cudaError_t launch_rowbox_a(const PredictMaps& map, PredictParams p, cudaStream_t stream) {
-  auto kern = predict_rowbox_kernel<CP, T, AHEAD, FMA, CVT>;
+  auto kern = predict_rowbox_kernel<CP, T, AHEAD, FMA>;
   static int sms = 0;
   static bool attr = false;
   if (!attr) {
@@ -747,13 +832,33 @@ static cudaError_t launch_rowbox_a(const PredictMaps& map, PredictParams p, cuda
   }
   if (st_env > 0) st = st_env;
   p.rowbox_stages = st < 2 ? 2 : st > 8 ? 8 : st;
-  const RowBoxSmem L(p.rowbox_quads,
-                     rowbox_tab_feats(p.n_features, Elem<T>::kPerQuad, p.n_tab_blocks), CP,
-                     p.rowbox_stages, AHEAD);
-  const size_t smem = L.total + 128;
+  const int tf = rowbox_tab_feats(p.n_features, Elem<T>::kPerQuad, p.n_tab_blocks);
+  // resident tables unless they would cost CTAs per SM (GNB_ROWBOX_RESIDENT=0: never)
+  static int res_env = -1;
+  if (res_env < 0) {
+    const char* e = getenv("GNB_ROWBOX_RESIDENT");
+    res_env = e ? atoi(e) != 0 : 1;
+  }
   int per_sm = 0;
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 5 * 32, smem);
+  const RowBoxSmem Ls(p.rowbox_quads, tf, CP, p.rowbox_stages, AHEAD, 0);
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 5 * 32,
+                                                                Ls.total + 128);
   if (e != cudaSuccess) return e;
+  size_t smem = Ls.total + 128;
+  p.rowbox_resident = 0;
+  if (res_env) {
+    const RowBoxSmem Lr(p.rowbox_quads, tf, CP, p.rowbox_stages, AHEAD, p.n_slots);
+    int per_sm_r = 0;
+    if (Lr.total + 128 <= 227u * 1024u) {
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_r, kern, 5 * 32, Lr.total + 128);
+      if (e != cudaSuccess) return e;
+    }
+    if (per_sm_r >= per_sm && per_sm_r > 0) {
+      p.rowbox_resident = 1;
+      smem = Lr.total + 128;
+      per_sm = per_sm_r;
+    }
+  }
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
   const int64_t want = static_cast<int64_t>(sms) * per_sm;
   const int grid = static_cast<int>(p.n_tiles < want ? p.n_tiles : want);
@@ -762,27 +867,10 @@ static cudaError_t launch_rowbox_a(const PredictMaps& map, PredictParams p, cuda
   return cudaGetLastError();
 }
 
-inline int rowbox_cvt() {  // GNB_ROWBOX_CVT=0/1/2: conversion unit (A/B), see converted()
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("GNB_ROWBOX_CVT");
-    v = e ? atoi(e) : 0;
-    if (v < 0 || v > 2) v = 0;
-  }
-  return v;
-}
-
 template <int CP, typename T, bool FMA>
 static cudaError_t launch_rowbox(const PredictMaps& map, const PredictParams& p,
                                  cudaStream_t stream) {
-  if constexpr (CP == 2) {
-    switch (rowbox_cvt()) {
-      case 1: return launch_rowbox_a<CP, T, 2, FMA, 1>(map, p, stream);
-      case 2: return launch_rowbox_a<CP, T, 2, FMA, 2>(map, p, stream);
-      default: break;
-    }
-  }
-  return launch_rowbox_a<CP, T, 2, FMA, 0>(map, p, stream);
+  return launch_rowbox_a<CP, T, 2, FMA>(map, p, stream);
 }
 
 template <int CP, typename T, bool FMA>

@@ -87,6 +87,24 @@ def test_class_counts(C):
     _check(x, size, prior, ll, route, 1000, 5000)
 
 
+@pytest.mark.parametrize("F,ldx", [(13, 16), (50, 52), (50, 56), (52, 52), (64, 64), (100, 100)])
+@pytest.mark.parametrize("S,C", [(1, 2), (3, 2), (64, 2), (3, 4), (2, 16)])
+def test_rowbox_paths(F, ldx, S, C):
+    """Row-box K-PRED: contiguous rows (1-D bulk tile) and padded pitches (2-D
+    box); tables resident in smem (few slots) or staged per tile (64 slots);
+    row-in-registers early release (C=2 up to 13 quads, C=4 up to 8); uniform
+    (grouped) and mixed (shuffled) tiles."""
+    rng = np.random.default_rng(F * 1000 + S * 10 + C)
+    width, G = 100, max(S, 4)
+    prior, ll, route = _tables(rng, S, C, F, G)
+    N = 4 * 128 * 3 + 77
+    size = np.sort(rng.integers(0, width * G, size=N))
+    x = rng.poisson(3.0, size=(N, F))
+    _check(x, size, prior, ll, route, width, width * G, ldx=ldx)
+    perm = rng.permutation(N)
+    _check(x[perm], size[perm], prior, ll, route, width, width * G, ldx=ldx)
+
+
 def test_ragged_groups_sorted_and_shuffled():
     rng = np.random.default_rng(7)
     G, F = 32, 200
