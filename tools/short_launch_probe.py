@@ -2,8 +2,8 @@
 
 Times the row-box K-PRED (F=50 int32) at several row counts and, for scale,
 a device-to-device copy of the same rows, both with bench.py's flush + event
-method.  The
-intercept of time vs. bytes is the fixed cost (launch + ramp + tail).
+method.  The intercept of time vs. bytes is the fixed cost (launch + ramp +
+tail).
 
   gpurun -- 'python tools/short_launch_probe.py'
 """
