@@ -59,24 +59,26 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 // (profiles/r01_tuning.md): the promoted neighbour sector is the same row's
 // next 32-column chunk, which the next stage of the same CTA reads.
 CUtensorMapL2promotion l2_promotion() {
-  static int v = -1;
-  if (v < 0) {
+  static const int v = [] {  // read once (thread-safe static init)
+    int v = -1;
     const char* e = getenv("GNB_L2_PROMO");
     v = e ? atoi(e) : 3;
     if (v < 0 || v > 3) v = 3;
-  }
+    return v;
+  }();
   return static_cast<CUtensorMapL2promotion>(v);
 }
 
 // L2 promotion of the last chunk of gathered rows (GNB_GATHER_TAIL: -1 = same
 // map as the other chunks, else a CUtensorMapL2promotion value; default 0).
 int gather_tail_promo() {
-  static int v = -2;
-  if (v == -2) {
+  static const int v = [] {  // read once (thread-safe static init)
+    int v = -2;
     const char* e = getenv("GNB_GATHER_TAIL");
     v = e ? atoi(e) : 0;
     if (v < -1 || v > 3) v = 0;
-  }
+    return v;
+  }();
   return v;
 }
 
@@ -182,11 +184,12 @@ static int check_predict(const int32_t* x, int64_t n_rows, int32_t F, int64_t ld
 // GNB_ROWBOX_BULK=0: row-box tiles through the 2-D tensor map even when the
 // rows are contiguous (A/B of the 1-D bulk copy).
 static bool rowbox_bulk() {
-  static int v = -1;
-  if (v < 0) {
+  static const int v = [] {  // read once (thread-safe static init)
+    int v = -1;
     const char* e = getenv("GNB_ROWBOX_BULK");
     v = e ? atoi(e) != 0 : 1;
-  }
+    return v;
+  }();
   return v != 0;
 }
 

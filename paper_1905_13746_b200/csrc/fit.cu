@@ -481,12 +481,13 @@ static cudaError_t launch_fit_np(const CUtensorMap& map, FitParams p, cudaStream
 // sort is a latency-bound dependent chain (~7k cycles per 128-row tile under
 // load) that capped K-FIT at ~85 % of HBM with int32 rows (profiles/).
 static int fit_producers() {
-  static int v = -1;
-  if (v < 0) {
+  static const int v = [] {  // read once (thread-safe static init)
+    int v = -1;
     const char* e = getenv("GNB_FIT_NP");
     v = e ? atoi(e) : 2;
     if (v != 1) v = 2;
-  }
+    return v;
+  }();
   return v;
 }
 
@@ -507,23 +508,25 @@ int fit_box_rows(int x_type) {
 // best on B200, profiles/r01_tuning.md), 1 = 4 stages x 1 CTA/SM,
 // 2 = one-box (16 KB) stages x 4 x 2 CTAs/SM, 3 = one-box stages x 3 x 2 CTAs/SM.
 static int fit_variant() {
-  static int v = -1;
-  if (v < 0) {
+  static const int v = [] {  // read once (thread-safe static init)
+    int v = -1;
     const char* e = getenv("GNB_FIT_VARIANT");
     v = e ? atoi(e) : 0;
     if (v < 0 || v > 3) v = 0;
-  }
+    return v;
+  }();
   return v;
 }
 
 // CTAs per SM the partial-sum budget is sized for, narrow rows (GNB_FIT_CTAS).
 static int narrow_ctas() {
-  static int v = -1;
-  if (v < 0) {
+  static const int v = [] {  // read once (thread-safe static init)
+    int v = -1;
     const char* e = getenv("GNB_FIT_CTAS");
     v = e ? atoi(e) : 2;
     if (v < 1 || v > 8) v = 2;
-  }
+    return v;
+  }();
   return v;
 }
 
@@ -541,11 +544,12 @@ template <typename T>
 static cudaError_t launch_fit_typed(const CUtensorMap& map, const FitParams& p,
                                    cudaStream_t stream) {
   // keys are dealt to warps round-robin: no more warps than keys
-  static int nw8 = -1;  // GNB_FIT_NW8=0 disables the 8-consumer-warp CTA (profiling)
-  if (nw8 < 0) {
+  static const int nw8 = [] {  // read once (thread-safe static init)  // GNB_FIT_NW8=0 disables the 8-consumer-warp CTA (profiling)
+    int nw8 = -1;
     const char* e = getenv("GNB_FIT_NW8");
     nw8 = e ? atoi(e) : 1;
-  }
+    return nw8;
+  }();
   // 8 consumer warps pay off for int32 rows (32-KB stages, consumer-bound); for
   // uint8/uint16 tiles the producer's sort is the limit (profiles/r01_tuning.md)
   if ((sizeof(T) == 4 || nw8 == 2) && p.n_keys >= 8 && nw8)  // 2: any storage (A/B)

@@ -79,11 +79,12 @@ cudaError_t pack_tables(const double* log_prior, const double* log_lik, int S, i
 }
 
 int predict_rowbox_quads(int n_features, int x_type, int n_classes) {
-  static int enabled = -1;
-  if (enabled < 0) {
+  static const int enabled = [] {  // read once (thread-safe static init)
+    int enabled = -1;
     const char* e = getenv("GNB_PRED_ROWBOX");
     enabled = e ? atoi(e) != 0 : 1;
-  }
+    return enabled;
+  }();
   (void)n_classes;
   if (!enabled || n_features < 1) return 0;
   const int eb = x_type == GNB_X_U8 ? 1 : x_type == GNB_X_U16 ? 2 : 4;
@@ -105,11 +106,12 @@ int predict_box_rows(int n_classes) {
 cudaError_t predict_launch(const PredictMaps* map, PredictParams p, cudaStream_t stream,
                            int force_generic) {
   const int CP = class_pad(p.n_classes);
-  static int x_policy = -1;  // GNB_X_POLICY=1: X loads evict_first (profiling; default normal)
-  if (x_policy < 0) {
+  static const int x_policy = [] {  // read once (thread-safe static init)  // GNB_X_POLICY=1: X loads evict_first (profiling; default normal)
+    int x_policy = -1;
     const char* e = getenv("GNB_X_POLICY");
     x_policy = e ? atoi(e) : 0;
-  }
+    return x_policy;
+  }();
   p.x_policy = x_policy;
   p.n_tab_blocks = table_blocks(p.n_features);
   p.tab = p.prior + static_cast<int64_t>(p.n_slots) * CP;

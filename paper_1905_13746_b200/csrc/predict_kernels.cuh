@@ -27,6 +27,7 @@
 // units predict_<storage>_<mode>.cu instantiate launch_typed<T, FMA> (so the
 // build compiles them in parallel) and predict.cu holds the dispatch.
 #pragma once
+#include <atomic>
 #include <cfloat>
 #include <climits>
 #include <cstdint>
@@ -757,25 +758,36 @@ __global__ void __launch_bounds__(256) predict_generic_kernel(const PredictParam
 }
 
 // ------------------------------------------------------------------ launchers
+// Opt kernel K into 227 KB of dynamic smem once per device (the attribute
+// lives in each device's context, so a process driving several GPUs sets it
+// on each) and return the current device's SM count.
+template <auto K>
+cudaError_t kernel_prepare(int* sms) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  static std::atomic<uint64_t> ready{0};
+  const uint64_t bit = 1ull << (dev & 63);
+  if (!(ready.load(std::memory_order_acquire) & bit)) {
+    e = cudaFuncSetAttribute(K, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (e != cudaSuccess) return e;
+    ready.fetch_or(bit, std::memory_order_acq_rel);
+  }
+  return cudaDeviceGetAttribute(sms, cudaDevAttrMultiProcessorCount, dev);
+}
+
 template <int CP, typename T, int R, int NW, int STAGES, bool GATHER, int B, bool FMA>
 static cudaError_t launch_tma_mode(const PredictMaps& map, PredictParams p, cudaStream_t stream) {
   using L = PredictSmem<CP, T, R, NW, STAGES, GATHER, B>;
-  auto kern = predict_tma_kernel<CP, T, R, NW, STAGES, GATHER, B, FMA>;
+  constexpr auto kern = predict_tma_kernel<CP, T, R, NW, STAGES, GATHER, B, FMA>;
   p.n_tiles = (p.n_rows + L::kRows - 1) / L::kRows;
   p.n_chunks = (p.n_features + Elem<T>::kPerRow - 1) / Elem<T>::kPerRow;
-  static int per_sm = 0;  // resident CTAs per SM for this instantiation
-  static int sms = 0;
-  if (per_sm == 0) {
-    cudaError_t e =
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kAlloc);
-    if (e != cudaSuccess) return e;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, (NW + 1) * 32, L::kAlloc);
-    if (e != cudaSuccess) return e;
-    if (per_sm < 1) per_sm = 1;
-  }
+  int sms = 0, per_sm = 0;  // resident CTAs per SM for this instantiation
+  cudaError_t e = kernel_prepare<kern>(&sms);
+  if (e != cudaSuccess) return e;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, (NW + 1) * 32, L::kAlloc);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) per_sm = 1;
   const int64_t want = static_cast<int64_t>(sms) * per_sm;
   const int grid = static_cast<int>(p.n_tiles < want ? p.n_tiles : want);
   if (grid == 0) return cudaSuccess;
@@ -785,11 +797,12 @@ static cudaError_t launch_tma_mode(const PredictMaps& map, PredictParams p, cuda
 
 // Gather mode: GNB_GATHER_B=2 stages two chunks of each gathered row (A/B).
 inline int gather_boxes() {
-  static int v = -1;
-  if (v < 0) {
+  static const int v = [] {  // read once (thread-safe static init)
+    int v = -1;
     const char* e = getenv("GNB_GATHER_B");
     v = e ? atoi(e) : 1;
-  }
+    return v;
+  }();
   return v;
 }
 
@@ -810,39 +823,32 @@ inline constexpr uint32_t kRowBoxRingBytes = 53248;  // ring depth: stages x box
 
 template <int CP, typename T, int AHEAD, bool FMA>
 static cudaError_t launch_rowbox_a(const PredictMaps& map, PredictParams p, cudaStream_t stream) {
-  auto kern = predict_rowbox_kernel<CP, T, AHEAD, FMA>;
-  static int sms = 0;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         227 * 1024);
-    if (e != cudaSuccess) return e;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    attr = true;
-  }
+  constexpr auto kern = predict_rowbox_kernel<CP, T, AHEAD, FMA>;
+  int sms = 0;
+  cudaError_t e = kernel_prepare<kern>(&sms);
+  if (e != cudaSuccess) return e;
   p.n_tiles = (p.n_rows + kRowBoxRows - 1) / kRowBoxRows;
   const uint32_t box = static_cast<uint32_t>(kRowBoxRows) * p.rowbox_quads * 16;
   int st = static_cast<int>(kRowBoxRingBytes / box);
-  static int st_env = -1;
-  if (st_env < 0) {
+  static const int st_env = [] {  // read once (thread-safe static init)
+    int st_env = -1;
     const char* e = getenv("GNB_ROWBOX_STAGES");
     st_env = e ? atoi(e) : 0;
-  }
+    return st_env;
+  }();
   if (st_env > 0) st = st_env;
   p.rowbox_stages = st < 2 ? 2 : st > 8 ? 8 : st;
   const int tf = rowbox_tab_feats(p.n_features, Elem<T>::kPerQuad, p.n_tab_blocks);
   // resident tables unless they would cost CTAs per SM (GNB_ROWBOX_RESIDENT=0: never)
-  static int res_env = -1;
-  if (res_env < 0) {
+  static const int res_env = [] {  // read once (thread-safe static init)
+    int res_env = -1;
     const char* e = getenv("GNB_ROWBOX_RESIDENT");
     res_env = e ? atoi(e) != 0 : 1;
-  }
+    return res_env;
+  }();
   int per_sm = 0;
   const RowBoxSmem Ls(p.rowbox_quads, tf, CP, p.rowbox_stages, AHEAD, 0);
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 5 * 32,
-                                                                Ls.total + 128);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 5 * 32, Ls.total + 128);
   if (e != cudaSuccess) return e;
   size_t smem = Ls.total + 128;
   p.rowbox_resident = 0;
@@ -893,12 +899,13 @@ inline constexpr PredVariant kCp2Variants[] = {{1, 4, 2}, {1, 4, 3}, {2, 2, 2}, 
                                            {1, 4, 2}, {1, 4, 3}, {1, 4, 2}};  // 4-6: B=2,2,4
 
 inline int cp2_variant() {
-  static int v = -1;
-  if (v < 0) {
+  static const int v = [] {  // read once (thread-safe static init)
+    int v = -1;
     const char* e = getenv("GNB_PRED_VARIANT");
     v = e ? atoi(e) : 0;
     if (v < 0 || v >= static_cast<int>(sizeof(kCp2Variants) / sizeof(kCp2Variants[0]))) v = 0;
-  }
+    return v;
+  }();
   return v;
 }
 
