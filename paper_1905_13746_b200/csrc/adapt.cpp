@@ -163,11 +163,18 @@ PyObject* gather_into(PyObject*, PyObject* args) {
       Py_DECREF(seq);
       return nullptr;
     }
+    // Walk the smaller of the two dicts: the model's k features looked up in
+    // the histogram (the reference's own `hist.get(op)` per feature,
+    // classifier.py:143-147) when k < nnz, else the histogram's entries looked
+    // up in the column map.  Same counts either way.
+    const bool by_feature = PyDict_GET_SIZE(columns) < PyDict_GET_SIZE(e);
+    PyObject* walk = by_feature ? columns : e;
+    PyObject* probe = by_feature ? e : columns;
     Py_ssize_t pos = 0;
     PyObject *k, *v;
-    while (PyDict_Next(e, &pos, &k, &v)) {
-      PyObject* col = PyDict_GetItemWithError(columns, k);
-      if (!col) {
+    while (PyDict_Next(walk, &pos, &k, &v)) {
+      PyObject* hit = PyDict_GetItemWithError(probe, k);
+      if (!hit) {
         if (PyErr_Occurred()) {
           Py_DECREF(e);
           Py_DECREF(seq);
@@ -175,8 +182,10 @@ PyObject* gather_into(PyObject*, PyObject* args) {
         }
         continue;
       }
+      PyObject* col = by_feature ? v : hit;
+      PyObject* cnt = by_feature ? hit : v;
       const Py_ssize_t j = PyLong_AsSsize_t(col);
-      if (j < 0 || j >= width || !put_count(x + i * width, j, v)) {
+      if (j < 0 || j >= width || !put_count(x + i * width, j, cnt)) {
         if (!PyErr_Occurred()) PyErr_SetString(PyExc_IndexError, "column out of range");
         Py_DECREF(e);
         Py_DECREF(seq);
@@ -187,6 +196,84 @@ PyObject* gather_into(PyObject*, PyObject* args) {
   }
   Py_DECREF(seq);
   Py_RETURN_NONE;
+}
+
+// predictions(label int32 [N], logpost float64 [N, 2], eff int32 [N], Prediction,
+//             classes (index -> Label), MALWARE, BENIGN) -> list
+// The TimedRun.predictions of classify_* (engine.py:187-206): None where the
+// row's label is negative (error rows), else Prediction(label,
+// {MALWARE: lp[i,1], BENIGN: lp[i,0]}, eff[i]).  Instances are made like the
+// frozen dataclass's own __init__ makes them (object.__setattr__ per field).
+PyObject* s_f_label = nullptr;
+PyObject* s_f_logpost = nullptr;
+PyObject* s_f_group = nullptr;
+
+PyObject* predictions(PyObject*, PyObject* args) {
+  PyObject *lab_o, *lp_o, *eff_o, *type_o, *classes, *malware, *benign;
+  if (!PyArg_ParseTuple(args, "OOOO!O!OO", &lab_o, &lp_o, &eff_o, &PyType_Type, &type_o,
+                        &PyTuple_Type, &classes, &malware, &benign))
+    return nullptr;
+  Py_buffer bl{}, bp{}, be{};
+  if (PyObject_GetBuffer(lab_o, &bl, PyBUF_C_CONTIGUOUS) != 0) return nullptr;
+  const Py_ssize_t n = bl.len / 4;
+  if (PyObject_GetBuffer(lp_o, &bp, PyBUF_C_CONTIGUOUS) != 0) {
+    PyBuffer_Release(&bl);
+    return nullptr;
+  }
+  if (PyObject_GetBuffer(eff_o, &be, PyBUF_C_CONTIGUOUS) != 0) {
+    PyBuffer_Release(&bl);
+    PyBuffer_Release(&bp);
+    return nullptr;
+  }
+  PyObject* out = nullptr;
+  PyTypeObject* tp = reinterpret_cast<PyTypeObject*>(type_o);
+  PyObject* empty = PyTuple_New(0);
+  const Py_ssize_t nc = PyTuple_GET_SIZE(classes);
+  if (bl.itemsize != 4 || be.itemsize != 4 || bp.itemsize != 8 || bp.len < n * 16 ||
+      be.len < n * 4 || !empty) {
+    if (!PyErr_Occurred()) PyErr_SetString(PyExc_ValueError, "bad prediction buffers");
+  } else {
+    // no cyclic-GC passes while allocating ~2 containers per row (they cost
+    // more than the construction itself); the previous state is restored
+    const int gc_was_on = PyGC_Disable();
+    out = PyList_New(n);
+    const int32_t* lab = static_cast<const int32_t*>(bl.buf);
+    const double* lp = static_cast<const double*>(bp.buf);
+    const int32_t* eff = static_cast<const int32_t*>(be.buf);
+    for (Py_ssize_t i = 0; out && i < n; ++i) {
+      if (lab[i] < 0 || lab[i] >= nc) {
+        Py_INCREF(Py_None);
+        PyList_SET_ITEM(out, i, Py_None);
+        continue;
+      }
+      PyObject* obj = tp->tp_new(tp, empty, nullptr);
+      PyObject* d = PyDict_New();
+      PyObject* fm = PyFloat_FromDouble(lp[2 * i + 1]);
+      PyObject* fb = PyFloat_FromDouble(lp[2 * i]);
+      PyObject* g = PyLong_FromLong(eff[i]);
+      bool ok = obj && d && fm && fb && g && PyDict_SetItem(d, malware, fm) == 0 &&
+                PyDict_SetItem(d, benign, fb) == 0 &&
+                PyObject_GenericSetAttr(obj, s_f_label, PyTuple_GET_ITEM(classes, lab[i])) == 0 &&
+                PyObject_GenericSetAttr(obj, s_f_logpost, d) == 0 &&
+                PyObject_GenericSetAttr(obj, s_f_group, g) == 0;
+      Py_XDECREF(d);
+      Py_XDECREF(fm);
+      Py_XDECREF(fb);
+      Py_XDECREF(g);
+      if (!ok) {
+        Py_XDECREF(obj);
+        Py_CLEAR(out);
+        break;
+      }
+      PyList_SET_ITEM(out, i, obj);
+    }
+    if (gc_was_on) PyGC_Enable();
+  }
+  Py_XDECREF(empty);
+  PyBuffer_Release(&bl);
+  PyBuffer_Release(&bp);
+  PyBuffer_Release(&be);
+  return out;
 }
 
 // meta_into(samples, limit, malware, benign, sizes_out int32 [N], labels_out int32 [N])
@@ -237,6 +324,8 @@ PyMethodDef kMethods[] = {
      "gather_into(samples, route, colmaps, width, group_width, limit, out, sizes_out)."},
     {"meta_into", meta_into, METH_VARARGS,
      "meta_into(samples, limit, MALWARE, BENIGN, sizes_out, labels_out)."},
+    {"predictions", predictions, METH_VARARGS,
+     "predictions(label, logpost, eff, Prediction, classes, MALWARE, BENIGN) -> list."},
     {nullptr, nullptr, 0, nullptr}};
 
 PyModuleDef kModule = {PyModuleDef_HEAD_INIT, "_adapt",
@@ -249,5 +338,8 @@ PyMODINIT_FUNC PyInit__adapt(void) {
   s_entries = PyUnicode_InternFromString("entries");
   s_size_bytes = PyUnicode_InternFromString("size_bytes");
   s_label = PyUnicode_InternFromString("label");
+  s_f_label = s_label;
+  s_f_logpost = PyUnicode_InternFromString("log_posterior");
+  s_f_group = PyUnicode_InternFromString("effective_group");
   return PyModule_Create(&kModule);
 }

@@ -10,6 +10,7 @@ JSONL parsing, splitting, bundle JSON and the CLI stay in the reference.
 from __future__ import annotations
 
 import math
+import sys
 from bisect import bisect_left
 from dataclasses import dataclass, field
 from enum import Enum
@@ -50,7 +51,7 @@ class OpcodeHistogram:
             if isinstance(n, bool) or not isinstance(n, int) or n < 0:
                 raise ValueError(f"count for {op!r} must be a non-negative integer, got {n!r}")
             if n:
-                key = op.lower()
+                key = sys.intern(op.lower())  # shared key objects: identity hits in lookups
                 merged[key] = merged.get(key, 0) + n
         return cls(merged)
 

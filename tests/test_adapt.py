@@ -62,3 +62,44 @@ def test_counts_beyond_int32_rejected():
     s = [SampleRecord("a", Label.MALWARE, 1, OpcodeHistogram({"op": 2**31}))]
     with pytest.raises(OverflowError):
         _adapt.densify_into(s, {"op": 0}, np.zeros((1, 1), np.int32), 1)
+
+
+def test_gather_walks_either_dict():
+    """gather_into gives the same rows whether it walks the model's features
+    (k < nnz) or the histogram entries (k >= nnz)."""
+    rng = np.random.default_rng(3)
+    s = _samples(rng, 400)
+    route = np.array([0, 1], np.int32)
+    small = [{"op1": 0, "op5": 1}, {"op2": 1, "op7": 0}]                 # k=2 < most nnz
+    large = [{f"op{i}": (i * 7) % 30 for i in range(30)}, {f"op{i}": 29 - i for i in range(30)}]
+    for maps, width in ((small, 2), (large, 30)):
+        x = np.zeros((400, width), np.int32)
+        sz = np.zeros(400, np.int32)
+        _adapt.gather_into(s, route, maps, width, 30000, 60000, x, sz)
+        for i, r in enumerate(s):
+            if not 0 <= r.size_bytes < 60000:
+                assert sz[i] == -1 and not x[i].any()
+                continue
+            want = np.zeros(width, np.int32)
+            for op, j in maps[r.size_bytes // 30000].items():
+                want[j] = r.histogram.entries.get(op, 0)
+            assert sz[i] == r.size_bytes and np.array_equal(x[i], want)
+
+
+def test_predictions_match_python_construction():
+    import gc
+    from paper_1905_13746_b200.model import INDEX_CLASS, Prediction
+    rng = np.random.default_rng(4)
+    n = 1000
+    lab = rng.integers(-2, 2, size=n).astype(np.int32)
+    lp = rng.standard_normal((n, 2))
+    eff = rng.integers(0, 100, size=n).astype(np.int32)
+    got = _adapt.predictions(lab, lp, eff, Prediction, INDEX_CLASS, Label.MALWARE, Label.BENIGN)
+    want = [None if lab[i] < 0 else Prediction(
+        INDEX_CLASS[lab[i]], {Label.MALWARE: float(lp[i, 1]), Label.BENIGN: float(lp[i, 0])},
+        int(eff[i])) for i in range(n)]
+    assert got == want
+    assert gc.isenabled()
+    p = next(x for x in got if x is not None)
+    with pytest.raises(Exception):
+        p.label = Label.BENIGN        # still a frozen dataclass instance
