@@ -914,10 +914,6 @@ int gnb_fit_stats_host(const int32_t* x, int64_t n_rows, int32_t n_cols, int64_t
   }
   // chunks on different streams may run concurrently: every chunk adds exact
   // integer-valued partials with RED.ADD.F64, so the order does not matter.
-  // The clock starts once the context's buffers exist (the reference, too,
-  // builds its worker pool before its timer, engine.py:273-285): a first call
-  // -- or one larger than any before -- allocates device buffers here.
-  if (elapsed_ns) t0 = std::chrono::steady_clock::now();
   int64_t chunk = 0;
   for (int64_t r0 = 0; r0 < n_rows; r0 += rows, ++chunk) {
     const int lane = static_cast<int>(chunk % kLanes);
