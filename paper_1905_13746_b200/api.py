@@ -64,6 +64,26 @@ def _densify(samples: Sequence[SampleRecord], columns: dict[str, int], width: in
     return x
 
 
+def _dense_vocab(samples: Sequence[SampleRecord]):
+    """[N, max(V, 1)] int32 counts over the sorted union of opcodes (the
+    vocabulary score_opcodes ranges over, features.py:71) and that vocabulary:
+    one C-API walk of the histograms discovers the opcodes (first-seen columns)
+    while densifying; the columns are then put in mnemonic order."""
+    width = 512
+    while True:
+        columns: dict[str, int] = {}
+        ops: list[str] = []
+        raw = np.zeros((len(samples), width), dtype=np.int32)
+        if _adapt.discover_into(samples, columns, ops, raw, width):
+            break
+        width *= 4
+    order = np.asarray(sorted(range(len(ops)), key=ops.__getitem__), dtype=np.int64)
+    x = np.zeros((len(samples), max(len(ops), 1)), dtype=np.int32)
+    if len(ops):
+        _adapt.permute_columns(raw, width, order, x)
+    return x, [ops[j] for j in order.tolist()]
+
+
 def _fit_stats_host(x: np.ndarray, size: np.ndarray, label: np.ndarray, *, n_classes: int,
                     width: int, limit: int, device: int):
     G = limit // width
@@ -123,8 +143,7 @@ def train_bundle(train: GroupedCorpus, k: int, alpha: float = 1.0, *, seed: int 
     the host finalize (scores, top-k, libm logs) per group."""
     config = train.config
     samples = train.all_samples()
-    vocab = sorted({op for s in samples for op in s.histogram.entries})
-    x = _densify(samples, {op: j for j, op in enumerate(vocab)}, max(len(vocab), 1))
+    x, vocab = _dense_vocab(samples)
     size = np.array([s.size_bytes for s in samples], dtype=object)
     size64 = np.array([v if -2**63 <= v < 2**63 else -1 for v in size], dtype=np.int64)
     _, label = _meta(samples, config.max_size_bytes)

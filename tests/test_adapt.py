@@ -103,3 +103,24 @@ def test_predictions_match_python_construction():
     p = next(x for x in got if x is not None)
     with pytest.raises(Exception):
         p.label = Label.BENIGN        # still a frozen dataclass instance
+
+
+@pytest.mark.parametrize("n_ops", [30, 700])   # 700 > the first 512-column guess: retry
+def test_dense_vocab_matches_sorted_union(n_ops):
+    from paper_1905_13746_b200.api import _dense_vocab
+    rng = np.random.default_rng(n_ops)
+    ops = [f"m{rng.integers(0, 10**6)}_{i}" for i in range(n_ops)]
+    samples = []
+    for i in range(300):
+        pick = rng.choice(n_ops, int(rng.integers(0, 40)), replace=False)
+        samples.append(SampleRecord(f"s{i}", Label.BENIGN, 10, OpcodeHistogram.from_counts(
+            {ops[j]: int(rng.integers(1, 50)) for j in pick})))
+    x, vocab = _dense_vocab(samples)
+    want_vocab = sorted({op for s in samples for op in s.histogram.entries})
+    assert vocab == want_vocab
+    want = np.zeros((300, max(len(vocab), 1)), np.int32)
+    col = {op: j for j, op in enumerate(vocab)}
+    for i, s in enumerate(samples):
+        for op, c in s.histogram.entries.items():
+            want[i, col[op]] = c
+    assert np.array_equal(x, want)
