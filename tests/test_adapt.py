@@ -112,7 +112,7 @@ def test_dense_vocab_matches_sorted_union(n_ops):
     ops = [f"m{rng.integers(0, 10**6)}_{i}" for i in range(n_ops)]
     samples = []
     for i in range(300):
-        pick = rng.choice(n_ops, int(rng.integers(0, 40)), replace=False)
+        pick = rng.choice(n_ops, int(rng.integers(0, min(40, n_ops))), replace=False)
         samples.append(SampleRecord(f"s{i}", Label.BENIGN, 10, OpcodeHistogram.from_counts(
             {ops[j]: int(rng.integers(1, 50)) for j in pick})))
     x, vocab = _dense_vocab(samples)
