@@ -64,7 +64,8 @@ def parse():
                          "(host-side collectives only; testing, not a bench number)")
     ap.add_argument("--x-dtype", choices=("int32", "uint16", "uint8"), default="int32",
                     help="storage of the predict matrix (same counts; narrower = fewer bytes)")
-    ap.add_argument("--workload", choices=("predict", "sweep", "ragged", "fit"), default="predict",
+    ap.add_argument("--workload", choices=("predict", "sweep", "ragged", "fit", "fin"),
+                    default="predict",
                     help="predict = cfg4 (driver default); sweep = cfg2 F sweep at 1M rows; "
                          "ragged = cfg3 32 size groups in one launch; fit = cfg5 1B x 128, C=16")
     ap.add_argument("--flush", choices=("clean", "write"), default="clean",
@@ -750,6 +751,53 @@ def run_fit(args, world, rank, local):
             "stats_bytes_allreduced": int(st.packed().numel() * 8)}
 
 
+def run_fin(args, world, rank, local):
+    """FIN: feature scoring + top-k + logs for every size
+    group from the fitted statistics, host C++ (gnb_fin_train) vs device
+    (gnb_fin_train_device, scoring + bitonic top-k on the GPU, logs on the
+    host); outputs must be identical.  Wall time per call, median of `steps`."""
+    import numpy as np
+    import torch
+    from paper_1905_13746_b200 import dense
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    rows = []
+    for G, V, k in ((32, 256, 100), (32, 1024, 200), (8, 16384, 256)):
+        n = 20_000 * G if V <= 1024 else 4_000 * G
+        x, size, lab = dense.generate(n, V, group_rows=[n // G] * G, divergence=0.8, seed=1,
+                                      device=dev)
+        st = dense.fit_stats(x, size, lab, n_classes=2, group_size_bytes=5120,
+                             max_size_bytes=5120 * G)
+        S, cnt = st.sums.cpu().numpy(), st.counts.cpu().numpy()
+        del x, size, lab
+
+        def host():
+            return dense.fin_train(S, cnt, k=k, alpha=1.0, min_per_class=6)
+
+        def device():
+            r = dense.fin_train_device(st, k=k, alpha=1.0, min_per_class=6)
+            torch.cuda.synchronize()
+            return r
+
+        h, d = host(), device()
+        same = all(np.array_equal(getattr(h, f), getattr(d, f))
+                   for f in ("state", "n_features", "features", "log_prior", "log_lik"))
+        th, td = [], []
+        for _ in range(max(args.steps, 5)):
+            t0 = time.perf_counter()
+            host()
+            th.append(time.perf_counter() - t0)
+            t0 = time.perf_counter()
+            device()
+            td.append(time.perf_counter() - t0)
+        rows.append({"groups": G, "vocab": V, "k": k, "host_ms": round(statistics.median(th) * 1e3, 3),
+                     "device_ms": round(statistics.median(td) * 1e3, 3), "identical": same})
+        del st
+    return {"metric": "FIN wall time per call (feature scoring + top-k + log tables, all groups)",
+            "workload": "fin: G groups x V vocabulary statistics from K-FIT on synthetic rows",
+            "unit": "ms", "rows": rows}
+
+
 def main():
     global FLUSH_MODE
     args = parse()
@@ -761,6 +809,8 @@ def main():
         out = run_sweep(args, world, rank, local)
     elif args.workload == "ragged":
         out = run_ragged(args, world, rank, local)
+    elif args.workload == "fin":
+        out = run_fin(args, world, rank, local)
     elif args.workload == "fit":
         out = run_fit(args, world, rank, local)
     else:
