@@ -133,9 +133,10 @@ class DenseCorpus:
 
 def read_corpus(source, *, allow_unlabeled: bool = False, threads: int = 0) -> DenseCorpus:
     """Parse JSONL text / bytes / a path into a DenseCorpus (parse_corpus contract)."""
-    if isinstance(source, (str, os.PathLike)) and os.path.exists(str(source)) and \
-            not str(source).lstrip().startswith("{"):
-        with open(source, "rb") as fh:
+    if isinstance(source, os.PathLike) or (
+            isinstance(source, str) and "\n" not in source[:4096]
+            and not source[:4096].lstrip().startswith("{") and os.path.exists(source)):
+        with open(source, "rb") as fh:     # a path (text is JSONL: '{' or several lines)
             data = fh.read()
     elif isinstance(source, str):
         data = source.encode()
