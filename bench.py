@@ -559,9 +559,20 @@ def _timed_launches(fn, steps, warmup, flush_bytes=512 << 20):
     sink = torch.empty((), dtype=torch.int64, device="cuda")
     for _ in range(warmup):
         fn()
+    # and at least ~0.3 s of back-to-back work, so SM/memory clocks have left
+    # any idle state before the first timed launch of a short kernel
+    torch.cuda.synchronize()
+    t_end = time.perf_counter() + 0.3
+    while time.perf_counter() < t_end:
+        for _ in range(20):
+            fn()
+        torch.cuda.synchronize()
     times = []
     s = torch.cuda.current_stream()
-    for _ in range(steps):
+    # `warmup` untimed rounds of the exact measured sequence (flush, clean
+    # read, sleep, launch) first: the first rounds on freshly allocated
+    # buffers ran ~8 % slower than every later one
+    for it in range(warmup + steps):
         flush.zero_()
         if FLUSH_MODE == "clean":
             torch.sum(clean, 0, out=sink)
@@ -574,7 +585,8 @@ def _timed_launches(fn, steps, warmup, flush_bytes=512 << 20):
         fn()
         b.record(s)
         b.synchronize()
-        times.append(a.elapsed_time(b))
+        if it >= warmup:
+            times.append(a.elapsed_time(b))
     return sum(times) / len(times), statistics.median(times)
 
 

@@ -452,11 +452,14 @@ __global__ void __launch_bounds__((NW + 1) * 32)
 // quads are then moved to registers and the stage is released BEFORE the
 // DMUL/DADD chain runs: a stage is held for a few LDS instead of the whole
 // scoring time, which is what bounds the bytes in flight per SM for short rows.
-// Register budget (__launch_bounds__(160, 4): <= 102 per thread): 13 quads of
-// X next to 2 accumulators (14 spill), 8 next to 4; wider class pads keep the
-// stage.
+// Register budget: the default instance (__launch_bounds__(160, 4): <= 102
+// per thread) holds 13 quads of X next to 2 accumulators (14 spill), 8 next to
+// 4; wider class pads keep the stage.  Rows of 14-26 quads at C=2 (int32
+// F <= 104: 2-3 CTAs/SM anyway, 30-55-KB tiles) take a second instance with
+// __launch_bounds__(160, 2) and 26 quads of registers.
 template <int CP>
 inline constexpr int kRegQuads = CP <= 2 ? 13 : CP == 4 ? 8 : 0;
+inline constexpr int kRegQuadsWide = 26;
 
 struct RowBoxSmem {
   uint32_t x_bytes, tab_bytes, hdr_bytes, res_stride, x, res, tab, hdr, sizes, bar, total;
@@ -507,8 +510,8 @@ __device__ __forceinline__ void rowbox_score_smem(double (&acc)[CP], const uint8
   }
 }
 
-template <int CP, typename T, int kRowBoxAhead, bool FMA>
-__global__ void __launch_bounds__(5 * 32, 4)
+template <int CP, typename T, int kRowBoxAhead, bool FMA, int RQ = kRegQuads<CP>, int MINB = 4>
+__global__ void __launch_bounds__(5 * 32, MINB)
     predict_rowbox_kernel(const __grid_constant__ PredictMaps maps, const PredictParams p) {
   const CUtensorMap& xmap = maps.main;
   constexpr int NW = 4, ROWS = kRowBoxRows, EQ = Elem<T>::kPerQuad;
@@ -642,7 +645,6 @@ __global__ void __launch_bounds__(5 * 32, 4)
     // ---------------------------------------------------------- consumers
     const int row = lane + 32 * warp;
     const int nq = (p.n_features + EQ - 1) / EQ;
-    constexpr int RQ = kRegQuads<CP>;
     const bool early = RQ > 0 && resident && nq <= RQ;
     const double* res = reinterpret_cast<const double*>(smem + L.res);
     int stage = 0;
@@ -821,9 +823,9 @@ static cudaError_t launch_tma(const PredictMaps& map, const PredictParams& p,
 inline constexpr int kRowBoxMaxQuads = 26;       // 128 rows x 26 x 16 B = 52 KB per stage
 inline constexpr uint32_t kRowBoxRingBytes = 53248;  // ring depth: stages x box ~ 52 KB
 
-template <int CP, typename T, int AHEAD, bool FMA>
+template <int CP, typename T, int AHEAD, bool FMA, int RQ = kRegQuads<CP>, int MINB = 4>
 static cudaError_t launch_rowbox_a(const PredictMaps& map, PredictParams p, cudaStream_t stream) {
-  constexpr auto kern = predict_rowbox_kernel<CP, T, AHEAD, FMA>;
+  constexpr auto kern = predict_rowbox_kernel<CP, T, AHEAD, FMA, RQ, MINB>;
   int sms = 0;
   cudaError_t e = kernel_prepare<kern>(&sms);
   if (e != cudaSuccess) return e;
@@ -873,9 +875,47 @@ static cudaError_t launch_rowbox_a(const PredictMaps& map, PredictParams p, cuda
   return cudaGetLastError();
 }
 
+// GNB_ROWBOX_WIDE=0: rows of 14-26 quads keep their stage while scoring (A/B).
+inline bool rowbox_wide() {
+  static const int v = [] {  // read once (thread-safe static init)
+    const char* e = getenv("GNB_ROWBOX_WIDE");
+    return e ? atoi(e) : 1;
+  }();
+  return v != 0;
+}
+
+// CTAs per SM of a row-box kernel instance for this shape (per-stage table
+// layout: the larger of the two smem footprints).
+template <auto K, typename T>
+int rowbox_occupancy(const PredictParams& p, int cp) {
+  const uint32_t box = static_cast<uint32_t>(kRowBoxRows) * p.rowbox_quads * 16;
+  int st = static_cast<int>(kRowBoxRingBytes / box);
+  st = st < 2 ? 2 : st > 8 ? 8 : st;
+  const int tf = rowbox_tab_feats(p.n_features, Elem<T>::kPerQuad, table_blocks(p.n_features));
+  const RowBoxSmem L(p.rowbox_quads, tf, cp, st, 2, 0);
+  int sms = 0, per_sm = 0;
+  if (kernel_prepare<K>(&sms) != cudaSuccess ||
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, K, 5 * 32, L.total + 128) !=
+          cudaSuccess)
+    return 0;
+  return per_sm;
+}
+
 template <int CP, typename T, bool FMA>
 static cudaError_t launch_rowbox(const PredictMaps& map, const PredictParams& p,
                                  cudaStream_t stream) {
+  if constexpr (CP == 2) {
+    // rows of 14-26 quads: the register-staged instance when its register
+    // budget does not cost a CTA per SM (F=100 int32: 2 CTAs/SM either way,
+    // 0.90 -> 1.04 of HBM; F=64 int32: 3 -> 2 CTAs/SM, slower -- keep default)
+    const int nq = (p.n_features + Elem<T>::kPerQuad - 1) / Elem<T>::kPerQuad;
+    if (nq > kRegQuads<CP> && nq <= kRegQuadsWide && rowbox_wide()) {
+      constexpr auto wide = predict_rowbox_kernel<CP, T, 2, FMA, kRegQuadsWide, 2>;
+      constexpr auto base = predict_rowbox_kernel<CP, T, 2, FMA>;
+      if (rowbox_occupancy<wide, T>(p, CP) >= rowbox_occupancy<base, T>(p, CP))
+        return launch_rowbox_a<CP, T, 2, FMA, kRegQuadsWide, 2>(map, p, stream);
+    }
+  }
   return launch_rowbox_a<CP, T, 2, FMA>(map, p, stream);
 }
 
