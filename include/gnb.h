@@ -287,6 +287,30 @@ int gnb_generate(int32_t* x, int64_t n_rows, int32_t n_cols, int64_t ldx, int32_
                  double divergence, uint64_t seed, const int32_t* col_map,
                  int32_t vocab_cols, uintptr_t stream);
 
+/* ------------------------------------------------------------------ fit exchange (NCCL)
+ * The sharded fit's only exchange step: each device's packed fp64
+ * statistics buffer {sums | sumsq | counts} summed in place across devices
+ * over NCCL (NVLink / NVSwitch).  The statistics are integer-valued, so the
+ * bundle is bit-identical for any device count.  NCCL is loaded at run time
+ * (dlopen "libnccl.so.2": the process's own copy, e.g. torch's, else the
+ * system one); GNB_EUNSUPPORTED if it cannot be.
+ *   one process, several GPUs: gnb_comms_init(&c, ndev, devs)   (ncclCommInitAll)
+ *   one process per GPU:       rank 0 gnb_comms_unique_id(id), share the
+ *                              GNB_COMMS_ID_BYTES, every rank
+ *                              gnb_comms_init_rank(&c, nranks, rank, id, device)
+ * gnb_fit_allreduce takes one buffer and one stream per local device of the
+ * communicator (gnb_comms_size), stream-ordered, no synchronisation. */
+#define GNB_COMMS_ID_BYTES 128
+typedef struct gnb_comms gnb_comms;
+int gnb_comms_unique_id(uint8_t* id);
+int gnb_comms_init(gnb_comms** comms, int32_t ndev, const int32_t* devs);
+int gnb_comms_init_rank(gnb_comms** comms, int32_t nranks, int32_t rank, const uint8_t* id,
+                        int32_t device);
+int32_t gnb_comms_size(const gnb_comms* comms);
+void gnb_comms_destroy(gnb_comms* comms);
+int gnb_fit_allreduce(gnb_comms* comms, double* const* packed_stats, int64_t elems,
+                      const uintptr_t* streams);
+
 #ifdef __cplusplus
 }
 #endif

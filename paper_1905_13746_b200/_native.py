@@ -80,6 +80,12 @@ _SIGS = {
     "gnb_generate": ([_p, _i64, _i32, _i64, _p, _p, _i64, _p, _i32, _i32, _i32, _f64, _u64, _p,
                       _i32, _up],
                      C.c_int),
+    "gnb_comms_unique_id": ([_p], C.c_int),
+    "gnb_comms_init": ([C.POINTER(_p), _i32, _p], C.c_int),
+    "gnb_comms_init_rank": ([C.POINTER(_p), _i32, _i32, _p, _i32], C.c_int),
+    "gnb_comms_size": ([_p], _i32),
+    "gnb_comms_destroy": ([_p], None),
+    "gnb_fit_allreduce": ([_p, _p, _i64, _p], C.c_int),
 }
 
 for _name, (_args, _res) in _SIGS.items():

@@ -40,6 +40,14 @@ int cuda_fail(cudaError_t e, const char* what) {
     if (e_ != cudaSuccess) return cuda_fail(e_, what); \
   } while (0)
 
+}  // namespace
+
+namespace gnb {
+int set_error(int code, const char* msg) { return fail(code, "%s", msg); }
+}  // namespace gnb
+
+namespace {
+
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   static std::once_flag once;

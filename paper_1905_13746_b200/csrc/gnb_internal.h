@@ -10,6 +10,9 @@
 
 namespace gnb {
 
+// Records `msg` for gnb_last_error() (thread-local) and returns `code`.
+int set_error(int code, const char* msg);
+
 struct PredictParams {
   const void* x;     // generic kernel only (TMA path reads through the tensor map)
   int32_t x_type;    // GNB_X_I32 / GNB_X_U16 / GNB_X_U8

@@ -52,3 +52,13 @@ def test_check_maps_errors():
         N.check(N.GNB_EINVAL, "x")
     with pytest.raises(N.NativeError):
         N.check(N.GNB_ECUDA, "x")
+
+
+def test_comms_argument_validation():
+    """gnb_comms_* reject bad arguments before touching NCCL or CUDA."""
+    h = ctypes.c_void_p()
+    assert N.lib.gnb_comms_init(ctypes.byref(h), 0, None) == N.GNB_EINVAL
+    assert N.lib.gnb_comms_init_rank(ctypes.byref(h), 2, 2, None, 0) == N.GNB_EINVAL
+    assert N.lib.gnb_fit_allreduce(None, None, 0, None) == N.GNB_EINVAL
+    assert N.lib.gnb_comms_size(None) == 0
+    N.lib.gnb_comms_destroy(None)

@@ -146,3 +146,25 @@ def test_device_fin_matches_host_fin(V, G, k):
         assert dev.features[g, :F].tolist() == host.features[g, :F].tolist()
     assert dev.log_prior.tobytes() == host.log_prior.tobytes()
     assert dev.log_lik.tobytes() == host.log_lik.tobytes()
+
+
+def test_library_comms_allreduce_single_device():
+    """gnb_comms_* / gnb_fit_allreduce (NCCL, dlopen'ed) on the one GPU of this
+    box: local communicator and rank communicator of size 1; the SUM of one
+    device's statistics is those statistics, bit for bit."""
+    from paper_1905_13746_b200.sharding import Comms
+    dev = torch.device("cuda")
+    x, size, lab = dense.generate(5000, 64, n_classes=3, seed=5, device=dev)
+    st = dense.fit_stats(x, size, lab, n_classes=3, group_size_bytes=5120, max_size_bytes=5120)
+    want = st.packed().clone()
+    c = Comms.local([torch.cuda.current_device()])
+    assert len(c) == 1
+    c.allreduce([st])
+    torch.cuda.synchronize()
+    assert torch.equal(st.packed(), want)
+    c.close()
+    r = Comms.rank(1, 0, Comms.unique_id(), torch.cuda.current_device())
+    r.allreduce([st])
+    torch.cuda.synchronize()
+    assert torch.equal(st.packed(), want)
+    r.close()
