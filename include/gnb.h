@@ -54,6 +54,10 @@ enum {
 /* element type of X for the typed entry points: the same non-negative
  * integer counts, stored in fewer bytes when they fit */
 enum { GNB_X_I32 = 0, GNB_X_U16 = 1, GNB_X_U8 = 2 };
+/* host-side storage for gnb_predict_host_typed only: counts < 16 packed two per
+ * byte, feature 2j in the low nibble of byte j, 2j+1 in the high nibble; ldx
+ * in features (even).  Unpacked to uint8 rows on the device. */
+enum { GNB_X_U4 = 3 };
 
 /* predict arithmetic (gnb_predict_mode) */
 enum { GNB_MODE_EXACT = 0, GNB_MODE_FMA = 1 };
@@ -159,8 +163,8 @@ int gnb_gather_features(const int32_t* x_vocab, int64_t n_rows, int32_t n_vocab,
                         const int32_t* n_features, int32_t n_slots, int32_t max_features,
                         int32_t* x_out, int64_t ldo, uintptr_t stream);
 
-/* gnb_predict_host for host rows stored as x_type (GNB_X_I32/U16/U8), ldx in
- * elements: narrow storage moves 2x/4x fewer bytes over PCIe. */
+/* gnb_predict_host for host rows stored as x_type (GNB_X_I32/U16/U8/U4), ldx
+ * in elements (features): narrow storage moves 2x/4x/8x fewer bytes over PCIe. */
 int gnb_predict_host_typed(const void* x, int32_t x_type, int64_t n_rows, int32_t n_features,
                            int64_t ldx, const int32_t* size_bytes, int32_t group_size_bytes,
                            int32_t max_size_bytes, const int32_t* route, int32_t n_slots,

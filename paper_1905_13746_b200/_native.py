@@ -23,7 +23,7 @@ GNB_MODE_EXACT, GNB_MODE_FMA = 0, 1
 ROW_OUT_OF_RANGE = -1
 ROW_NEGATIVE_COUNT = -2
 MAX_CLASSES = 16
-X_I32, X_U16, X_U8 = 0, 1, 2
+X_I32, X_U16, X_U8, X_U4 = 0, 1, 2, 3
 
 
 class NativeError(RuntimeError):

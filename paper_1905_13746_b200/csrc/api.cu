@@ -629,7 +629,7 @@ struct HostCtx {
   cudaEvent_t ev[kLanes] = {};
   cudaEvent_t copied[kLanes] = {};  // staging buffer of the lane may be reused
   DevBuf x[kLanes], size[kLanes], aux[kLanes], label[kLanes], logpost[kLanes];
-  DevBuf perm[kLanes], sortws[kLanes];
+  DevBuf perm[kLanes], sortws[kLanes], x4[kLanes];
   PinBuf stage[kLanes];
   DevBuf route, prior, lik, packed, sums, sumsq, counts, status;
   Pool* pool = nullptr;
@@ -746,6 +746,7 @@ static int predict_host_impl(const void* xv, int x_type, int64_t n_rows, int32_t
   for (int i = 0; i < kLanes; ++i) {
     GNB_CUDA(c->x[i].ensure(size_t(rows) * ld * 4), "malloc");
     if (narrow) GNB_CUDA(c->stage[i].ensure(size_t(rows) * ld16 * 2), "cudaHostAlloc");
+    if (x_type == GNB_X_U4) GNB_CUDA(c->x4[i].ensure(size_t(rows) * ld8 / 2), "malloc");
     GNB_CUDA(c->size[i].ensure(size_t(rows) * 4), "malloc");
     GNB_CUDA(c->label[i].ensure(size_t(rows) * 4), "malloc");
     if (logpost_out) GNB_CUDA(c->logpost[i].ensure(size_t(rows) * n_classes * 8), "malloc");
@@ -762,7 +763,21 @@ static int predict_host_impl(const void* xv, int x_type, int64_t n_rows, int32_t
     void* dx = c->x[lane].p;
     int xt = GNB_X_I32;
     int64_t dld = ld;
-    if (x_type != GNB_X_I32) {  // caller's narrow rows: copy as they are
+    if (x_type == GNB_X_U4) {  // nibble rows: copy packed, unpack to uint8 on the device
+      xt = GNB_X_U8;
+      dld = ld8;
+      const int64_t pb = ld8 / 2, sb = ldx / 2, wb = (n_features + 1) / 2;
+      const uint8_t* src = static_cast<const uint8_t*>(xv) + r0 * sb;
+      if (sb == pb)
+        GNB_CUDA(cudaMemcpyAsync(c->x4[lane].p, src, size_t(n) * pb, cudaMemcpyHostToDevice, s),
+                 "H2D");
+      else
+        GNB_CUDA(cudaMemcpy2DAsync(c->x4[lane].p, pb, src, sb, wb, n, cudaMemcpyHostToDevice, s),
+                 "H2D 2D");
+      GNB_CUDA(unpack_u4_launch(static_cast<const uint8_t*>(c->x4[lane].p), n, pb,
+                                static_cast<uint8_t*>(dx), s),
+               "unpack_u4");
+    } else if (x_type != GNB_X_I32) {  // caller's narrow rows: copy as they are
       xt = x_type;
       const int eb = elem_bytes(xt);
       dld = xt == GNB_X_U8 ? ld8 : ld16;
@@ -873,8 +888,10 @@ int gnb_predict_host_typed(const void* x, int32_t x_type, int64_t n_rows, int32_
                            int32_t n_classes, const double* log_prior, const double* log_lik,
                            int32_t* label_out, double* logpost_out, int32_t device,
                            int64_t* elapsed_ns) {
-  if (x_type != GNB_X_I32 && x_type != GNB_X_U16 && x_type != GNB_X_U8)
+  if (x_type != GNB_X_I32 && x_type != GNB_X_U16 && x_type != GNB_X_U8 && x_type != GNB_X_U4)
     return fail(GNB_EINVAL, "predict_host: unknown x_type %d", x_type);
+  if (x_type == GNB_X_U4 && (ldx & 1))
+    return fail(GNB_EINVAL, "predict_host: GNB_X_U4 rows need an even ldx (features)");
   return predict_host_impl(x, x_type, n_rows, n_features, ldx, size_bytes, group_size_bytes,
                            max_size_bytes, route, n_slots, n_classes, log_prior, log_lik,
                            label_out, logpost_out, device, elapsed_ns);

@@ -49,4 +49,33 @@ cudaError_t gather_launch(const int32_t* x, int64_t n_rows, int32_t V, int64_t l
   return cudaGetLastError();
 }
 
+// UNPACK-U4: one thread per 8 packed bytes (16 counts) -> one 16-B store.
+// Byte j holds feature 2j (low nibble) and 2j+1 (high nibble).
+__global__ void __launch_bounds__(256)
+    unpack_u4_kernel(const uint2* __restrict__ in, int64_t words, uint4* __restrict__ out) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < words;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const uint2 w = __ldg(in + i);
+    // spread the 8 nibbles of each 32-bit half into 8 bytes (low nibble first)
+    auto spread = [](uint32_t v, uint32_t& lo, uint32_t& hi) {
+      lo = __byte_perm(v & 0x0f0f0f0fu, (v >> 4) & 0x0f0f0f0fu, 0x5140);
+      hi = __byte_perm(v & 0x0f0f0f0fu, (v >> 4) & 0x0f0f0f0fu, 0x7362);
+    };
+    uint4 o;
+    spread(w.x, o.x, o.y);
+    spread(w.y, o.z, o.w);
+    out[i] = o;
+  }
+}
+
+cudaError_t unpack_u4_launch(const uint8_t* packed, int64_t n_rows, int64_t packed_pitch,
+                             uint8_t* out, cudaStream_t stream) {
+  const int64_t words = n_rows * (packed_pitch / 8);
+  if (words == 0) return cudaSuccess;
+  const int64_t b = (words + 255) / 256;
+  unpack_u4_kernel<<<static_cast<int>(b < 148 * 16 ? b : 148 * 16), 256, 0, stream>>>(
+      reinterpret_cast<const uint2*>(packed), words, reinterpret_cast<uint4*>(out));
+  return cudaGetLastError();
+}
+
 }  // namespace gnb

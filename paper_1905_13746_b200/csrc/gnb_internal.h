@@ -107,6 +107,11 @@ cudaError_t gather_launch(const int32_t* x, int64_t n_rows, int32_t V, int64_t l
                           const int32_t* n_features, int32_t F, int32_t* out, int64_t ldo,
                           cudaStream_t stream);
 
+// Nibble-packed rows (GNB_X_U4, `packed_pitch` bytes per row, a multiple of 8)
+// -> uint8 rows (pitch 2 * packed_pitch): the host pipeline's PCIe format.
+cudaError_t unpack_u4_launch(const uint8_t* packed, int64_t n_rows, int64_t packed_pitch,
+                             uint8_t* out, cudaStream_t stream);
+
 size_t slot_sort_workspace(int64_t n, int S);
 cudaError_t slot_sort(const int32_t* size, int64_t n, int width, int limit, const int32_t* route,
                       int S, int32_t* perm, void* workspace, cudaStream_t stream);

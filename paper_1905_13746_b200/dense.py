@@ -173,6 +173,26 @@ def narrowest(x: torch.Tensor) -> torch.Tensor:
     return x
 
 
+def pack_u4(x: torch.Tensor, out: torch.Tensor = None) -> torch.Tensor:
+    """Host rows of counts < 16 packed two per byte (GNB_X_U4: feature 2j in the
+    low nibble of byte j, 2j+1 in the high nibble), each row padded to a
+    multiple of 8 bytes -- the layout gnb_predict_host_typed copies in one piece
+    and unpacks on the device.  Pass `ldx = 2 * result.shape[1]` (features).
+    Raises if a count is outside [0, 16): the storage is lossless or refused."""
+    n, F = x.shape
+    if x.numel() and (int(x.min()) < 0 or int(x.max()) > 15):
+        raise ValueError("pack_u4: counts must be in [0, 16)")
+    pb = (F + 15) // 16 * 8
+    if out is None:
+        out = torch.empty((n, pb), dtype=torch.uint8, pin_memory=torch.cuda.is_available())
+    if out.shape != (n, pb) or out.dtype != torch.uint8:
+        raise ValueError(f"pack_u4: out must be uint8 [{n}, {pb}]")
+    w = torch.zeros((n, 2 * pb), dtype=torch.uint8)
+    w[:, :F] = x
+    out.copy_(w[:, 0::2] | (w[:, 1::2] << 4))
+    return out
+
+
 def gather_features(x_vocab: torch.Tensor, size_bytes: torch.Tensor, tables: DeviceTables,
                     features, n_features, *, out=None, stream=None) -> torch.Tensor:
     """[N, V] full-vocabulary counts -> [N, F] predict layout (routed FeatureSet order).

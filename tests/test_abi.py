@@ -62,3 +62,24 @@ def test_comms_argument_validation():
     assert N.lib.gnb_fit_allreduce(None, None, 0, None) == N.GNB_EINVAL
     assert N.lib.gnb_comms_size(None) == 0
     N.lib.gnb_comms_destroy(None)
+
+
+def test_pack_u4_layout_and_odd_ldx():
+    """pack_u4: feature 2j in the low nibble of byte j, rows padded to 8 bytes;
+    out-of-range counts refused; GNB_X_U4 with an odd ldx rejected before CUDA."""
+    import numpy as np
+    import torch
+    from paper_1905_13746_b200 import dense
+    x = np.random.default_rng(0).integers(0, 16, size=(5, 19))
+    p = dense.pack_u4(torch.from_numpy(x)).numpy()
+    assert p.shape == (5, 16)
+    un = np.stack([p & 15, p >> 4], axis=2).reshape(5, 32)
+    assert (un[:, :19] == x).all() and (un[:, 19:] == 0).all()
+    with pytest.raises(ValueError):
+        dense.pack_u4(torch.tensor([[16]]))
+    with pytest.raises(ValueError):
+        dense.pack_u4(torch.tensor([[-1]]))
+    assert N.lib.gnb_predict_host_typed(None, N.X_U4, 1, 3, 3, None, 1, 1, None, 1, 2, None,
+                                        None, None, None, 0, None) == N.GNB_EINVAL
+    assert N.lib.gnb_predict_host_typed(None, 9, 1, 3, 3, None, 1, 1, None, 1, 2, None,
+                                        None, None, None, 0, None) == N.GNB_EINVAL

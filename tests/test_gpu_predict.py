@@ -391,3 +391,35 @@ def test_mode_rejects_unknown():
     s = torch.zeros(4, dtype=torch.int32, device="cuda")
     with pytest.raises(InvalidConfigError):
         dense.predict(x, s, t, mode="fast")
+
+
+@pytest.mark.parametrize("F,pad,n", [(37, 0, 50_000), (37, 6, 30_001), (256, 0, 200_000),
+                                     (1, 0, 7), (100, 2, 1_000_003)])
+def test_host_u4_entry(F, pad, n):
+    """GNB_X_U4 host rows (two counts per byte, unpacked on the device): labels
+    and log-posteriors bit-identical to the oracle, contiguous (one copy) and
+    padded (2-D copy) pitches, odd F, several pipeline chunks, ragged slots."""
+    import ctypes
+    from paper_1905_13746_b200 import _native as N
+    rng = np.random.default_rng(F + pad)
+    S, C, G = 3, 2, 4
+    prior, ll, route = _tables(rng, S, C, F, G)
+    x = rng.integers(0, 16, size=(n, F))
+    packed = dense.pack_u4(torch.from_numpy(x.astype(np.int32))).numpy()
+    if pad:
+        wide = np.zeros((n, packed.shape[1] + pad), np.uint8)
+        wide[:, :packed.shape[1]] = packed
+        packed = wide
+    ldx = 2 * packed.shape[1]
+    size = rng.integers(-5, G * 100 + 5, size=n).astype(np.int32)
+    lab = np.empty(n, np.int32)
+    lp = np.empty((n, C))
+    pr, lk = np.ascontiguousarray(prior), np.ascontiguousarray(ll)
+    N.check(N.lib.gnb_predict_host_typed(packed.ctypes.data, N.X_U4, n, F, ldx, size.ctypes.data,
+                                         100, G * 100, route.ctypes.data, S, C, pr.ctypes.data,
+                                         lk.ctypes.data, lab.ctypes.data, lp.ctypes.data, 0,
+                                         None))
+    want, wlp = O.predict_dense(x, size, route, prior, ll, width=100, limit=G * 100)
+    assert lab.tolist() == want.tolist()
+    ok = want >= 0
+    assert lp[ok].tobytes() == wlp[ok].tobytes()
