@@ -689,8 +689,18 @@ bool narrowing_enabled() {
   return e != nullptr && atoi(e) != 0;
 }
 
+// MiB of X crossing PCIe per pipeline chunk (GNB_HOST_CHUNK_MB, read once).
+int64_t host_chunk_bytes() {
+  static const int64_t v = [] {
+    const char* e = getenv("GNB_HOST_CHUNK_MB");
+    const int64_t mb = e ? atoll(e) : 64;
+    return (mb >= 1 && mb <= 4096 ? mb : 64) << 20;
+  }();
+  return v;
+}
+
 int64_t chunk_rows_for(int64_t row_bytes) {
-  const int64_t target = int64_t(64) << 20;  // ~64 MiB of X per chunk
+  const int64_t target = host_chunk_bytes();
   int64_t r = std::max<int64_t>(1024, target / std::max<int64_t>(row_bytes, 1));
   return (r + 127) / 128 * 128;
 }
@@ -741,10 +751,15 @@ static int predict_host_impl(const void* xv, int x_type, int64_t n_rows, int32_t
   // measured slower on the B200 box, profiles/r01_tuning.md).
   const int64_t ld = (n_features + 3) / 4 * 4;  // device rows padded for TMA (int32)
   const int64_t ld8 = (n_features + 15) / 16 * 16, ld16 = (n_features + 7) / 8 * 8;
-  const int64_t rows = std::min<int64_t>(chunk_rows_for(ld * 4), std::max<int64_t>(n_rows, 1));
+  // chunk rows from the bytes each row moves over PCIe; device rows as stored
+  const int64_t wire_b = x_type == GNB_X_U4 ? ld8 / 2 : x_type == GNB_X_U8 ? ld8
+                         : x_type == GNB_X_U16 ? ld16 * 2 : ld * 4;
+  const int64_t dev_b = x_type == GNB_X_U4 || x_type == GNB_X_U8 ? ld8
+                        : x_type == GNB_X_U16 ? ld16 * 2 : ld * 4;
+  const int64_t rows = std::min<int64_t>(chunk_rows_for(wire_b), std::max<int64_t>(n_rows, 1));
   const bool narrow = x_type == GNB_X_I32 && narrowing_enabled();
   for (int i = 0; i < kLanes; ++i) {
-    GNB_CUDA(c->x[i].ensure(size_t(rows) * ld * 4), "malloc");
+    GNB_CUDA(c->x[i].ensure(size_t(rows) * dev_b), "malloc");
     if (narrow) GNB_CUDA(c->stage[i].ensure(size_t(rows) * ld16 * 2), "cudaHostAlloc");
     if (x_type == GNB_X_U4) GNB_CUDA(c->x4[i].ensure(size_t(rows) * ld8 / 2), "malloc");
     GNB_CUDA(c->size[i].ensure(size_t(rows) * 4), "malloc");
