@@ -10,8 +10,12 @@
 #define PY_SSIZE_T_CLEAN
 #include <Python.h>
 
+#include <algorithm>
+#include <atomic>
 #include <cstdint>
 #include <cstring>
+#include <thread>
+#include <vector>
 
 namespace {
 
@@ -109,11 +113,213 @@ PyObject* densify_into(PyObject*, PyObject* args) {
   Py_RETURN_NONE;
 }
 
+PyObject* gather_into_serial(PyObject*, PyObject* args);
+
+// ------------------------------------------------------------------ parallel gather
+// The dict walk of gather_into is ~3 us per sample (~85 entries) on one core,
+// 20x the device call.  gather_into splits it in two:
+//   1. serial, GIL held: per sample size_bytes -> slot, and a new reference
+//      to its entries dict (the only steps that touch reference counts);
+//   2. host threads walk the dicts with PyDict_Next and look each key up in a
+//      C++ table built from the model column maps (exact str keys compared by
+//      identity, then by cached hash + code points).
+// The calling thread keeps the GIL for the whole call, so no Python code runs
+// while the workers read: they only read dict storage, str data and compact
+// int values -- no reference counts, no allocation, no exceptions.  Anything
+// outside that (non-str keys, uncached hashes, non-int or out-of-range
+// counts) makes the call redo the rows with the serial walk above, which
+// raises exactly the serial path's errors.
+struct KeyTable {
+  std::vector<PyObject*> slot_key;  // open addressing, power-of-two size
+  std::vector<int32_t> slot_id;
+  size_t mask = 0;
+
+  static Py_hash_t cached_hash(PyObject* k) {
+    return reinterpret_cast<PyASCIIObject*>(k)->hash;
+  }
+  static bool same(PyObject* a, PyObject* b) {
+    if (a == b) return true;
+    const Py_ssize_t n = PyUnicode_GET_LENGTH(a);
+    const int kind = PyUnicode_KIND(a);
+    return n == PyUnicode_GET_LENGTH(b) && kind == PyUnicode_KIND(b) &&
+           memcmp(PyUnicode_DATA(a), PyUnicode_DATA(b), size_t(n) * kind) == 0;
+  }
+  void reserve(size_t n) {
+    size_t cap = 16;
+    while (cap < 2 * n) cap <<= 1;
+    slot_key.assign(cap, nullptr);
+    slot_id.assign(cap, -1);
+    mask = cap - 1;
+  }
+  // GIL held; k exact str with its hash computed.  Returns the id of k.
+  int32_t insert(PyObject* k, int32_t next_id) {
+    for (size_t i = size_t(cached_hash(k)) & mask;; i = (i + 1) & mask) {
+      if (!slot_key[i]) {
+        slot_key[i] = k;
+        slot_id[i] = next_id;
+        return next_id;
+      }
+      if (same(slot_key[i], k)) return slot_id[i];
+    }
+  }
+  // worker-safe (reads only); -1 = not present
+  int32_t find(PyObject* k, Py_hash_t h) const {
+    for (size_t i = size_t(h) & mask;; i = (i + 1) & mask) {
+      PyObject* q = slot_key[i];
+      if (!q) return -1;
+      if (q == k || (cached_hash(q) == h && same(q, k))) return slot_id[i];
+    }
+  }
+};
+
+PyObject* gather_into(PyObject* self, PyObject* args) {
+  PyObject *samples, *route_o, *colmaps, *out, *sizes_o;
+  Py_ssize_t width, group_width, limit;
+  if (!PyArg_ParseTuple(args, "OOO!nnnOO", &samples, &route_o, &PyList_Type, &colmaps, &width,
+                        &group_width, &limit, &out, &sizes_o))
+    return nullptr;
+  const unsigned hw = std::thread::hardware_concurrency();
+  const int W = static_cast<int>(std::min(hw ? hw : 1u, 32u));
+  const Py_ssize_t n_hint = PyObject_Length(samples);
+  if (n_hint < 0) PyErr_Clear();
+  if (W < 2 || n_hint < 8192 || group_width <= 0) return gather_into_serial(self, args);
+
+  // column maps -> one key table (union of every model's features) and a
+  // per-slot uid -> column array; anything but exact str keys / int columns:
+  // serial path
+  const Py_ssize_t S = PyList_GET_SIZE(colmaps);
+  Py_ssize_t total = 0;
+  for (Py_ssize_t s = 0; s < S; ++s) {
+    PyObject* cm = PyList_GET_ITEM(colmaps, s);
+    if (!PyDict_Check(cm)) return gather_into_serial(self, args);
+    total += PyDict_GET_SIZE(cm);
+  }
+  KeyTable tab;
+  tab.reserve(size_t(total) + 1);
+  std::vector<std::vector<std::pair<int32_t, int32_t>>> slot_pairs(static_cast<size_t>(S));
+  int32_t uids = 0;
+  for (Py_ssize_t s = 0; s < S; ++s) {
+    Py_ssize_t pos = 0;
+    PyObject *k, *v;
+    while (PyDict_Next(PyList_GET_ITEM(colmaps, s), &pos, &k, &v)) {
+      if (!PyUnicode_CheckExact(k) || !PyLong_CheckExact(v)) return gather_into_serial(self, args);
+      if (PyObject_Hash(k) == -1) return nullptr;
+      const Py_ssize_t j = PyLong_AsSsize_t(v);
+      if (j < 0 || j >= width) return gather_into_serial(self, args);  // raises IndexError
+      const int32_t id = tab.insert(k, uids);
+      if (id == uids) ++uids;
+      slot_pairs[size_t(s)].emplace_back(id, static_cast<int32_t>(j));
+    }
+  }
+  std::vector<int32_t> slot_col(size_t(S) * std::max<int32_t>(uids, 1), -1);
+  for (Py_ssize_t s = 0; s < S; ++s)
+    for (auto [id, j] : slot_pairs[size_t(s)]) slot_col[size_t(s) * uids + id] = j;
+
+  PyObject* seq = PySequence_Fast(samples, "samples must be a sequence");
+  if (!seq) return nullptr;
+  const Py_ssize_t n = PySequence_Fast_GET_SIZE(seq);
+  Buf bx, bs, br;
+  const Py_ssize_t G = limit / group_width;
+  if (!bx.get(out, 4, n * width) || !bs.get(sizes_o, 4, n) || !br.get(route_o, 4, G)) {
+    Py_DECREF(seq);
+    return nullptr;
+  }
+  int32_t* x = static_cast<int32_t*>(bx.view.buf);
+  int32_t* sz = static_cast<int32_t*>(bs.view.buf);
+  const int32_t* route = static_cast<const int32_t*>(br.view.buf);
+
+  // 1. serial: sizes, slots, entries dicts (new references, released below)
+  std::vector<PyObject*> ents(size_t(n), nullptr);
+  std::vector<int32_t> slots(size_t(n), -1);
+  auto release = [&] {
+    for (PyObject* e : ents) Py_XDECREF(e);
+    Py_DECREF(seq);
+  };
+  bool serial = false;
+  for (Py_ssize_t i = 0; i < n && !serial; ++i) {
+    PyObject* s = PySequence_Fast_GET_ITEM(seq, i);
+    PyObject* so = PyObject_GetAttr(s, s_size_bytes);
+    if (!so) {
+      release();
+      return nullptr;
+    }
+    int overflow = 0;
+    const long long size = PyLong_AsLongLongAndOverflow(so, &overflow);
+    Py_DECREF(so);
+    if (size == -1 && PyErr_Occurred()) {
+      release();
+      return nullptr;
+    }
+    if (overflow || size < 0 || size >= limit) continue;  // row stays zero, sz = -1 below
+    const int32_t slot = route[size / group_width];
+    if (slot < 0 || slot >= S) {
+      serial = true;  // the serial walk raises the IndexError
+      break;
+    }
+    PyObject* e = entries_of(s);
+    if (!e) {
+      release();
+      return nullptr;
+    }
+    ents[size_t(i)] = e;
+    slots[size_t(i)] = slot;
+    sz[i] = static_cast<int32_t>(size);
+  }
+  // 2. parallel dict walks (reads only; see above)
+  std::atomic<int> bad{0};
+  if (!serial) {
+    auto work = [&](int w) {
+      const Py_ssize_t lo = n * w / W, hi = n * (w + 1) / W;
+      for (Py_ssize_t i = lo; i < hi && !bad.load(std::memory_order_relaxed); ++i) {
+        PyObject* e = ents[size_t(i)];
+        if (!e) continue;
+        const int32_t* cols = slot_col.data() + size_t(slots[size_t(i)]) * uids;
+        int32_t* row = x + i * width;
+        Py_ssize_t pos = 0;
+        PyObject *k, *v;
+        while (PyDict_Next(e, &pos, &k, &v)) {
+          if (!PyUnicode_CheckExact(k) || !PyLong_CheckExact(v)) {
+            bad.store(1);
+            return;
+          }
+          const Py_hash_t h = KeyTable::cached_hash(k);
+          if (h == -1) {
+            bad.store(1);
+            return;
+          }
+          const int32_t id = tab.find(k, h);
+          if (id < 0) continue;
+          const int32_t j = cols[id];
+          if (j < 0) continue;
+          int overflow = 0;
+          const long long c = PyLong_AsLongLongAndOverflow(v, &overflow);
+          if (overflow || c < 0 || c > 2147483647LL) {
+            bad.store(1);
+            return;
+          }
+          row[j] = static_cast<int32_t>(c);
+        }
+      }
+    };
+    std::vector<std::thread> th;
+    th.reserve(size_t(W - 1));
+    for (int w = 1; w < W; ++w) th.emplace_back(work, w);
+    work(0);
+    for (auto& t : th) t.join();
+  }
+  // rows outside [0, limit) (their ents entry is null) get size -1
+  for (Py_ssize_t i = 0; i < n; ++i)
+    if (!ents[size_t(i)] && !serial) sz[i] = -1;
+  release();
+  if (serial || bad.load()) return gather_into_serial(self, args);
+  Py_RETURN_NONE;
+}
+
 // gather_into(samples, route: int32 buffer [G], colmaps: list[dict], width, limit,
 //             out: int32 [N, width], sizes_out: int32 [N])
 // Row i gets the counts of its routed model's features (FeatureSet order);
 // sizes outside [0, limit) become -1 and leave the row zero.
-PyObject* gather_into(PyObject*, PyObject* args) {
+PyObject* gather_into_serial(PyObject*, PyObject* args) {
   PyObject *samples, *route_o, *colmaps, *out, *sizes_o;
   Py_ssize_t width, group_width, limit;
   if (!PyArg_ParseTuple(args, "OOO!nnnOO", &samples, &route_o, &PyList_Type, &colmaps, &width,
@@ -427,6 +633,8 @@ PyMethodDef kMethods[] = {
      "densify_into(samples, columns, out, width): counts of `columns` per sample."},
     {"gather_into", gather_into, METH_VARARGS,
      "gather_into(samples, route, colmaps, width, group_width, limit, out, sizes_out)."},
+    {"gather_into_serial", gather_into_serial, METH_VARARGS,
+     "gather_into on the calling thread only (the reference walk for tests)."},
     {"meta_into", meta_into, METH_VARARGS,
      "meta_into(samples, limit, MALWARE, BENIGN, sizes_out, labels_out)."},
     {"discover_into", discover_into, METH_VARARGS,

@@ -124,3 +124,36 @@ def test_dense_vocab_matches_sorted_union(n_ops):
         for op, c in s.histogram.entries.items():
             want[i, col[op]] = c
     assert np.array_equal(x, want)
+
+
+@pytest.mark.parametrize("case", ["plain", "nonstr_key", "big_count", "bad_route", "copied_keys"])
+def test_parallel_gather_matches_serial(case):
+    """gather_into (threaded dict walk for >= 8192 samples) == the serial walk,
+    and every unusual input falls back to the serial path with its errors."""
+    rng = np.random.default_rng(7)
+    s = _samples(rng, 20_000)
+    route = np.array([0, 1, 1, 0, 1, 0], np.int32)
+    colmaps = [{"op1": 0, "op2": 1, "op3": 2, "op17": 3}, {"op29": 0, "op1": 2, "op5": 1}]
+    if case == "copied_keys":      # equal but not identical str keys in the column maps
+        colmaps = [{("op" + str(int(k[2:])))[:]: v for k, v in cm.items()} for cm in colmaps]
+    if case == "nonstr_key":
+        s[12345].histogram.entries[7] = 3
+    if case == "big_count":
+        s[15000] = SampleRecord("big", Label.MALWARE, 100,
+                                OpcodeHistogram.from_counts({"op1": 2**40}))
+    if case == "bad_route":
+        route = np.array([0, 1, 5, 0, 1, 0], np.int32)
+    outs = []
+    for fn in (_adapt.gather_into, _adapt.gather_into_serial):
+        x = np.zeros((len(s), 4), np.int32)
+        size = np.empty(len(s), np.int32)
+        try:
+            fn(s, route, colmaps, 4, 10000, 60000, x, size)
+            outs.append((x, size))
+        except Exception as e:  # noqa: BLE001
+            outs.append(type(e))
+    if case in ("big_count", "bad_route"):
+        assert outs[0] == outs[1] and isinstance(outs[0], type)
+    else:
+        assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
+        assert outs[0][0].any()
