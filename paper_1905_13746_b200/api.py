@@ -69,6 +69,10 @@ def _dense_vocab(samples: Sequence[SampleRecord]):
     vocabulary score_opcodes ranges over, features.py:71) and that vocabulary:
     one C-API walk of the histograms discovers the opcodes (first-seen columns)
     while densifying; the columns are then put in mnemonic order."""
+    fast = _adapt.vocab_dense(samples)          # threaded walk (None: serial rules apply)
+    if fast is not None:
+        ops, buf = fast
+        return np.frombuffer(buf, dtype=np.int32).reshape(len(samples), max(len(ops), 1)), ops
     width = 512
     while True:
         columns: dict[str, int] = {}

@@ -162,6 +162,20 @@ struct KeyTable {
       if (same(slot_key[i], k)) return slot_id[i];
     }
   }
+  // insert with growth (worker-local tables): keys get ids 0, 1, ... in
+  // first-seen order, recorded in `order`
+  std::vector<PyObject*> order;
+  int32_t add(PyObject* k) {
+    if (2 * (order.size() + 1) > slot_key.size()) {
+      std::vector<PyObject*> old = order;
+      reserve(2 * old.size() + 8);
+      order.clear();
+      for (PyObject* q : old) add(q);
+    }
+    const int32_t id = insert(k, static_cast<int32_t>(order.size()));
+    if (id == static_cast<int32_t>(order.size())) order.push_back(k);
+    return id;
+  }
   // worker-safe (reads only); -1 = not present
   int32_t find(PyObject* k, Py_hash_t h) const {
     for (size_t i = size_t(h) & mask;; i = (i + 1) & mask) {
@@ -313,6 +327,130 @@ PyObject* gather_into(PyObject* self, PyObject* args) {
   release();
   if (serial || bad.load()) return gather_into_serial(self, args);
   Py_RETURN_NONE;
+}
+
+// vocab_dense(samples) -> (ops, bytearray) | None: _dense_vocab in one call --
+// the sorted union of the histograms' opcodes and the [N, max(V, 1)] int32
+// counts in that column order, built by host threads (same read-only rules
+// as gather_into: the GIL stays held, the serial phase takes the references).
+//   A. threads collect the distinct keys of their rows;
+//   B. serial: union, sorted by code point (Python's str order);
+//   C. threads zero their rows and write each count at its sorted column.
+// None = an input outside the fast path's rules (non-str keys, non-int or
+// out-of-range counts, fewer than 8192 samples): the caller uses the serial
+// discover_into walk, which raises the serial errors.
+PyObject* vocab_dense(PyObject*, PyObject* args) {
+  PyObject* samples;
+  if (!PyArg_ParseTuple(args, "O", &samples)) return nullptr;
+  const unsigned hw = std::thread::hardware_concurrency();
+  const int W = static_cast<int>(std::min(hw ? hw : 1u, 32u));
+  PyObject* seq = PySequence_Fast(samples, "samples must be a sequence");
+  if (!seq) return nullptr;
+  const Py_ssize_t n = PySequence_Fast_GET_SIZE(seq);
+  if (W < 2 || n < 8192) {
+    Py_DECREF(seq);
+    Py_RETURN_NONE;
+  }
+  std::vector<PyObject*> ents(size_t(n), nullptr);
+  auto release = [&] {
+    for (PyObject* e : ents) Py_XDECREF(e);
+    Py_DECREF(seq);
+  };
+  for (Py_ssize_t i = 0; i < n; ++i) {
+    PyObject* e = entries_of(PySequence_Fast_GET_ITEM(seq, i));
+    if (!e) {
+      release();
+      return nullptr;
+    }
+    ents[size_t(i)] = e;
+  }
+  auto run = [&](auto&& fn) {
+    std::vector<std::thread> th;
+    th.reserve(size_t(W - 1));
+    for (int w = 1; w < W; ++w) th.emplace_back(fn, w);
+    fn(0);
+    for (auto& t : th) t.join();
+  };
+  // A. distinct keys per thread
+  std::atomic<int> bad{0};
+  std::vector<KeyTable> local(static_cast<size_t>(W));
+  run([&](int w) {
+    KeyTable& t = local[size_t(w)];
+    t.reserve(64);
+    const Py_ssize_t lo = n * w / W, hi = n * (w + 1) / W;
+    for (Py_ssize_t i = lo; i < hi; ++i) {
+      Py_ssize_t pos = 0;
+      PyObject *k, *v;
+      while (PyDict_Next(ents[size_t(i)], &pos, &k, &v)) {
+        if (!PyUnicode_CheckExact(k) || !PyLong_CheckExact(v) || KeyTable::cached_hash(k) == -1) {
+          bad.store(1);
+          return;
+        }
+        t.add(k);
+      }
+    }
+  });
+  if (bad.load()) {
+    release();
+    Py_RETURN_NONE;
+  }
+  // B. union, code-point order
+  KeyTable all;
+  all.reserve(64);
+  for (const KeyTable& t : local)
+    for (PyObject* k : t.order) all.add(k);
+  std::vector<PyObject*> ops = all.order;
+  std::sort(ops.begin(), ops.end(),
+            [](PyObject* a, PyObject* b) { return PyUnicode_Compare(a, b) < 0; });
+  KeyTable col;  // key -> sorted column
+  col.reserve(ops.size() + 1);
+  for (size_t j = 0; j < ops.size(); ++j) col.insert(ops[j], static_cast<int32_t>(j));
+  const Py_ssize_t V = std::max<Py_ssize_t>(static_cast<Py_ssize_t>(ops.size()), 1);
+  PyObject* buf = PyByteArray_FromStringAndSize(nullptr, n * V * 4);
+  if (!buf) {
+    release();
+    return nullptr;
+  }
+  int32_t* x = reinterpret_cast<int32_t*>(PyByteArray_AS_STRING(buf));
+  // C. rows
+  run([&](int w) {
+    const Py_ssize_t lo = n * w / W, hi = n * (w + 1) / W;
+    memset(x + lo * V, 0, size_t(hi - lo) * V * 4);
+    for (Py_ssize_t i = lo; i < hi; ++i) {
+      Py_ssize_t pos = 0;
+      PyObject *k, *v;
+      int32_t* row = x + i * V;
+      while (PyDict_Next(ents[size_t(i)], &pos, &k, &v)) {
+        int overflow = 0;
+        const long long c = PyLong_AsLongLongAndOverflow(v, &overflow);
+        if (overflow || c < 0 || c > 2147483647LL) {
+          bad.store(1);
+          return;
+        }
+        row[col.find(k, KeyTable::cached_hash(k))] = static_cast<int32_t>(c);
+      }
+    }
+  });
+  if (bad.load()) {
+    Py_DECREF(buf);
+    release();
+    Py_RETURN_NONE;
+  }
+  PyObject* names = PyList_New(static_cast<Py_ssize_t>(ops.size()));
+  if (!names) {
+    Py_DECREF(buf);
+    release();
+    return nullptr;
+  }
+  for (size_t j = 0; j < ops.size(); ++j) {
+    Py_INCREF(ops[j]);
+    PyList_SET_ITEM(names, static_cast<Py_ssize_t>(j), ops[j]);
+  }
+  release();
+  PyObject* r = PyTuple_Pack(2, names, buf);
+  Py_DECREF(names);
+  Py_DECREF(buf);
+  return r;
 }
 
 // gather_into(samples, route: int32 buffer [G], colmaps: list[dict], width, limit,
@@ -633,6 +771,8 @@ PyMethodDef kMethods[] = {
      "densify_into(samples, columns, out, width): counts of `columns` per sample."},
     {"gather_into", gather_into, METH_VARARGS,
      "gather_into(samples, route, colmaps, width, group_width, limit, out, sizes_out)."},
+    {"vocab_dense", vocab_dense, METH_VARARGS,
+     "vocab_dense(samples) -> (sorted opcodes, int32 bytearray [N, max(V, 1)]) or None."},
     {"gather_into_serial", gather_into_serial, METH_VARARGS,
      "gather_into on the calling thread only (the reference walk for tests)."},
     {"meta_into", meta_into, METH_VARARGS,

@@ -157,3 +157,31 @@ def test_parallel_gather_matches_serial(case):
     else:
         assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
         assert outs[0][0].any()
+
+
+@pytest.mark.parametrize("case", ["plain", "nonstr_key", "big_count", "unicode"])
+def test_vocab_dense_matches_serial(case, monkeypatch):
+    """The threaded vocabulary walk (vocab_dense) == the serial discover_into +
+    permute path: same sorted opcodes, same matrix; unusual inputs -> None and
+    the serial path (with its errors)."""
+    from paper_1905_13746_b200 import api
+    rng = np.random.default_rng(3)
+    s = _samples(rng, 12_000)
+    if case == "unicode":
+        s[77] = SampleRecord("u", Label.MALWARE, 5, OpcodeHistogram.from_counts(
+            {"mové": 4, "\U0001f600op": 2, "op1": 1}))
+    if case == "nonstr_key":
+        s[9000].histogram.entries[7] = 3
+    if case == "big_count":
+        s[11000] = SampleRecord("big", Label.MALWARE, 100,
+                                OpcodeHistogram.from_counts({"op1": 2**40}))
+    fast = _adapt.vocab_dense(s)
+    if case in ("nonstr_key", "big_count"):
+        assert fast is None
+        return
+    assert fast is not None
+    x_fast, v_fast = api._dense_vocab(s)
+    monkeypatch.setattr(api._adapt, "vocab_dense", lambda samples: None)
+    x_ser, v_ser = api._dense_vocab(s)
+    assert v_fast == v_ser == sorted(v_ser)
+    assert np.array_equal(x_fast, x_ser)
