@@ -21,7 +21,11 @@ from .model import Label, OpcodeHistogram, SampleRecord
 
 _L = N.lib
 _p, _i32, _i64, _sz = C.c_void_p, C.c_int32, C.c_int64, C.c_size_t
-_L.gnb_corpus_parse.argtypes = [C.c_char_p, _sz, _i32, _i32, C.POINTER(C.c_void_p)]
+_L.gnb_corpus_parse.argtypes = [C.c_void_p, _sz, _i32, _i32, C.POINTER(C.c_void_p)]
+# a str's UTF-8 bytes without a copy (for ASCII text CPython's own buffer)
+_utf8 = C.pythonapi.PyUnicode_AsUTF8AndSize
+_utf8.restype = C.c_void_p
+_utf8.argtypes = [C.py_object, C.POINTER(C.c_ssize_t)]
 _L.gnb_corpus_parse.restype = C.c_int
 _L.gnb_corpus_free.argtypes = [_p]
 _L.gnb_corpus_free.restype = None
@@ -139,12 +143,17 @@ def read_corpus(source, *, allow_unlabeled: bool = False, threads: int = 0) -> D
         with open(source, "rb") as fh:     # a path (text is JSONL: '{' or several lines)
             data = fh.read()
     elif isinstance(source, str):
-        data = source.encode()
+        data = source                  # kept alive across the call
     else:
         data = bytes(source)
+    if isinstance(data, str):
+        n = C.c_ssize_t()
+        addr = _utf8(data, C.byref(n))   # raises UnicodeEncodeError on lone surrogates
+        ptr, size = addr, n.value
+    else:
+        ptr, size = data, len(data)
     h = C.c_void_p()
-    rc = _L.gnb_corpus_parse(data, len(data), 1 if allow_unlabeled else 0, threads,
-                             C.byref(h))
+    rc = _L.gnb_corpus_parse(ptr, size, 1 if allow_unlabeled else 0, threads, C.byref(h))
     if rc != N.GNB_OK:
         line, msg = _i64(), C.c_char_p()
         kind = _L.gnb_corpus_error(h, C.byref(line), C.byref(msg))

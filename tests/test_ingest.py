@@ -69,6 +69,12 @@ def test_large_parallel_parse_matches_single_thread():
     with pytest.raises(IntegrityError) as ei:
         ingest.read_corpus("\n".join(lines), threads=8)
     assert "at line 12346" in str(ei.value)
+    lines[19000] = lines[18990]  # a second duplicate (same shard); the first in order wins
+    lines[300] = lines[19500]    # and one whose twin comes later: the later line is reported
+    for t in (1, 3, 8):
+        with pytest.raises(IntegrityError) as ei:
+            ingest.read_corpus("\n".join(lines), threads=t)
+        assert "at line 12346" in str(ei.value)
 
 
 def test_prediction_writer_byte_identical():
