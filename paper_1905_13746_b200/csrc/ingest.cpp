@@ -353,10 +353,34 @@ struct Shard {
   bool err_has_id = false;
 };
 
-inline uint64_t fnv1a(const char* s, size_t n) {
-  uint64_t h = 1469598103934665603ull;
-  for (size_t i = 0; i < n; ++i) h = (h ^ static_cast<unsigned char>(s[i])) * 1099511628211ull;
-  return h;
+// Hash of a lower-cased mnemonic, a word at a time: 8-byte little-endian
+// words, the last one zero-padded.  The fast path computes the same value
+// while it lower-cases (SWAR, below); everything else calls key_hash.
+inline uint64_t mix_word(uint64_t h, uint64_t w) {
+  h = (h ^ w) * 0x9E3779B97F4A7C15ull;
+  return h ^ (h >> 29);
+}
+inline uint64_t key_hash(const char* s, size_t n) {
+  uint64_t h = n * 0xC2B2AE3D27D4EB4Full;
+  size_t i = 0;
+  for (; i + 8 <= n; i += 8) {
+    uint64_t w;
+    memcpy(&w, s + i, 8);
+    h = mix_word(h, w);
+  }
+  if (i < n) {
+    uint64_t w = 0;
+    memcpy(&w, s + i, n - i);
+    h = mix_word(h, w);
+  }
+  return h ^ (h >> 32);
+}
+// 'A'..'Z' -> 'a'..'z' in each byte of w; every other byte (incl. >= 0x80) kept
+inline uint64_t lower8(uint64_t w) {
+  const uint64_t hi = 0x8080808080808080ull;
+  const uint64_t a = (w & ~hi) + 0x3F3F3F3F3F3F3F3Full;  // low 7 bits >= 'A'
+  const uint64_t z = (w & ~hi) + 0x2525252525252525ull;  // low 7 bits >  'Z'
+  return w | ((a & ~z & ~w & hi) >> 2);
 }
 
 // vid of the (already lower-cased) mnemonic [s, s+n) with FNV-1a hash h,
@@ -391,7 +415,7 @@ int32_t vocab_id(Shard& sh, const char* s, size_t n, uint64_t h) {
   return vid;
 }
 
-int32_t vocab_id(Shard& sh, const char* s, size_t n) { return vocab_id(sh, s, n, fnv1a(s, n)); }
+int32_t vocab_id(Shard& sh, const char* s, size_t n) { return vocab_id(sh, s, n, key_hash(s, n)); }
 
 std::string lower_ascii(const std::string& s) {
   std::string o = s;
@@ -522,19 +546,34 @@ bool fast_line(const char* a, const char* b, bool allow_unlabeled, Shard& sh, Ro
           // rare, so the full parser takes it
           if (v == 0) return false;
           {
-            // lower-case + hash in one pass (stack buffer for usual mnemonics)
-            char kb[64];
+            // lower-case + hash in one pass, 8 bytes at a time when the
+            // line holds whole words past the key (stack buffer for usual
+            // mnemonics)
+            alignas(8) char kb[64];
             char* key = kb;
-            if (n > sizeof(kb)) {
-              fs.key.resize(n);
-              key = fs.key.data();
-            }
-            uint64_t h = 1469598103934665603ull;
-            for (size_t i = 0; i < n; ++i) {
-              char c = s[i];
-              if (c >= 'A' && c <= 'Z') c = static_cast<char>(c - 'A' + 'a');
-              key[i] = c;
-              h = (h ^ static_cast<unsigned char>(c)) * 1099511628211ull;
+            uint64_t h;
+            if (n <= sizeof(kb) && s + ((n + 7) & ~size_t(7)) <= b) {
+              h = n * 0xC2B2AE3D27D4EB4Full;
+              for (size_t i = 0; i < n; i += 8) {
+                uint64_t w;
+                memcpy(&w, s + i, 8);
+                if (n - i < 8) w &= (uint64_t(1) << (8 * (n - i))) - 1;
+                w = lower8(w);
+                memcpy(kb + i, &w, 8);
+                h = mix_word(h, w);
+              }
+              h ^= h >> 32;
+            } else {
+              if (n > sizeof(kb)) {
+                fs.key.resize(n);
+                key = fs.key.data();
+              }
+              for (size_t i = 0; i < n; ++i) {
+                char c = s[i];
+                if (c >= 'A' && c <= 'Z') c = static_cast<char>(c - 'A' + 'a');
+                key[i] = c;
+              }
+              h = key_hash(key, n);
             }
             const int32_t vid = vocab_id(sh, key, n, h);
             if (sh.mark[vid] == row_tag) {
