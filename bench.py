@@ -52,6 +52,8 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-object-api", action="store_true")
+    ap.add_argument("--object-rows", type=int, default=100_000)
     ap.add_argument("--no-logpost", action="store_true")
     ap.add_argument("--fit-rows", type=int, default=1_000_000_000)
     ap.add_argument("--ref-rows", type=int, default=2_000_000,
@@ -423,6 +425,11 @@ def run_ours(args, world, rank, local):
         cpu = cpu_baseline_from(xg, size, fin, F, width, args.cpu_seconds, host_dtype,
                                 label=label, logpost=logpost)
 
+    # ---- the reference-shaped object API (SampleRecord in, TimedRun out), rank 0, N=1
+    obj = None
+    if rank == 0 and world == 1 and not args.no_object_api:
+        obj = object_api_leg(args.object_rows, V, local)
+
     return {
         "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": round(ms_per_step, 4),
@@ -437,6 +444,7 @@ def run_ours(args, world, rank, local):
                    "l2": "inputs (%.1f GB/GPU) >> 126 MB L2; no flush needed" % (n * 4 * F / 1e9),
                    "parallelism": f"dp{world} (row shards, no predict collective)"},
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "narrow_storage": narrow,
+        "object_api": obj,
         "gpu_launches": args.steps * world, "clocks": clk,
         "accuracy_vs_generator_labels": round(acc, 4),
         "mean_launch_ms": round(mean_launch_ms, 4),
@@ -532,6 +540,48 @@ def run_reference(args, world, rank):
                 "d2h_bytes_per_step": 0},
         "reference_python": ref_py,
     }
+
+
+def object_api_leg(n, V, device):
+    """The drop-in a reference user calls: train_bundle + classify_parallel on n
+    SampleRecords of the synthetic law (1 size group, V opcodes, k = V), wall
+    time of each call (ADAPT walk + device + TimedRun objects) and the device
+    share (TimedRun.elapsed_ns, the reference's own classification clock).
+    Compare with `reference_python` in the --impl reference line."""
+    import numpy as np
+    import paper_1905_13746_b200 as gnb
+    rng = np.random.default_rng(0)
+    vocab = [f"op{i:03d}" for i in range(V)]
+    label = np.arange(n) % 2
+    size = rng.integers(0, 5120, size=n)
+    w = np.where(np.arange(V)[None, :] < V // 2, 1.0, 0.2)
+    p = np.where(label[:, None] == 1, w, w[:, ::-1])
+    x = rng.poisson((64 + size // 64)[:, None] * (p / p.sum(1, keepdims=True)))
+    samples = []
+    for i in range(n):
+        nz = np.nonzero(x[i])[0]
+        samples.append(gnb.SampleRecord(
+            f"s{i}", gnb.Label.MALWARE if label[i] else gnb.Label.BENIGN, int(size[i]),
+            gnb.OpcodeHistogram.from_counts({vocab[j]: int(x[i, j]) for j in nz})))
+    grouped, _ = gnb.partition_by_group(samples, gnb.GroupingConfig())
+    gnb.train_bundle(grouped, V, created_at="bench", device=device)        # warm
+    t = time.perf_counter()
+    bundle = gnb.train_bundle(grouped, V, created_at="bench", device=device)
+    fit_s = time.perf_counter() - t
+    wl = gnb.Workload(tuple(samples), lanes=os.cpu_count() or 1)
+    gnb.classify_parallel(bundle, wl, device=device)                      # warm
+    t = time.perf_counter()
+    run = gnb.classify_parallel(bundle, wl, warmup=False, device=device)
+    cls_s = time.perf_counter() - t
+    acc = float(np.mean([(p.label == gnb.Label.MALWARE) == bool(label[i])
+                         for i, p in enumerate(run.predictions)]))
+    return {"api": "paper_1905_13746_b200.train_bundle / classify_parallel (reference "
+                   "signatures, SampleRecord in, TimedRun out)",
+            "samples": n, "features": V, "k": V,
+            "train_bundle_samples_per_s": round(n / fit_s, 1),
+            "classify_parallel_wall_samples_per_s": round(n / cls_s, 1),
+            "classify_parallel_elapsed_samples_per_s": round(n / (run.elapsed_ns / 1e9), 1),
+            "accuracy": round(acc, 4)}
 
 
 def reference_python_leg(n, V):

@@ -36,10 +36,13 @@ def test_reference_arm_contract():
 @pytest.mark.timeout(600)
 def test_gpu_arm_contract():
     d = _run(["--rows", "2000000", "--steps", "5", "--warmup", "3", "--e2e-rows", "1000000",
-              "--e2e-steps", "1", "--cpu-seconds", "1"], 550)
+              "--e2e-steps", "1", "--cpu-seconds", "1", "--object-rows", "20000"], 550)
     assert BASE_KEYS <= set(d)
     assert {"roofline", "cpu_baseline", "gpu_launches", "clocks"} <= set(d)
     r = d["roofline"]
     assert r["bound"] == "hbm" and r["unit"] == "GB/s" and 0 < r["frac"] < 1.5
     assert d["gpu_launches"] == 5 and d["e2e"]["matches_device_labels"] is True
     assert d["accuracy_vs_generator_labels"] > 0.9
+    o = d["object_api"]
+    assert o["samples"] == 20000 and o["accuracy"] > 0.9
+    assert o["classify_parallel_elapsed_samples_per_s"] > 0
