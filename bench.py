@@ -481,7 +481,7 @@ def cpu_baseline_from(xg, size, fin, F, width, seconds, host_dtype="int32", labe
            "sample": f"{sample} rows of this workload (even stride over all {n} rows), "
                      f"{done // sample} passes in {dt:.1f}s",
            "impl": "oracle/gnb_oracle.c (exact mul-then-add, pthreads)",
-           "x_host_dtype": host_dtype}
+           "x_host_dtype": host_dtype, "cpu_model": cpu_model(), "os_cpu_count": os.cpu_count()}
     if label is not None:
         want_lab, want_lp = out
         res["device_labels_equal"] = bool(np.array_equal(label[idx].cpu().numpy(), want_lab))
@@ -535,11 +535,24 @@ def run_reference(args, world, rank):
                    "x_host_dtype": host_dtype},
         "cpu_baseline": {"value": round(value, 1), "unit": UNIT, "cores": threads,
                          "kind": "port", "sample": f"{sample} rows per step",
-                         "impl": "oracle/gnb_oracle.c"},
+                         "impl": "oracle/gnb_oracle.c", "cpu_model": cpu_model(),
+                         "os_cpu_count": os.cpu_count()},
         "e2e": {"value": round(value, 1), "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
         "reference_python": ref_py,
     }
+
+
+def cpu_model() -> str:
+    """The host CPU's model name (lscpu's "Model name"), from /proc/cpuinfo."""
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 def object_api_leg(n, V, device):
