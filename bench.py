@@ -418,6 +418,9 @@ def run_ours(args, world, rank, local):
             e2e["int32_host_rows"] = {k: v for k, v in e2e_run("int32").items()
                                       if k in ("value", "h2d_bytes_per_step")}
         del sh, lh, ph
+        # the e2e roofline: host->device bytes per second of this run against a
+        # plain pinned 1 GiB torch copy on the same link (the PCIe ceiling)
+        e2e["pcie"] = pcie_roofline(e2e, dev)
 
     # ---- CPU baseline: C oracle on the box's host cores (rank 0, N=1 only)
     cpu = None
@@ -541,6 +544,27 @@ def run_reference(args, world, rank):
                 "d2h_bytes_per_step": 0},
         "reference_python": ref_py,
     }
+
+
+def pcie_roofline(e2e, dev):
+    """Achieved H2D GB/s of the e2e leg vs a pinned 1 GiB host->device copy."""
+    import torch
+    h = torch.empty(1 << 30, dtype=torch.uint8, pin_memory=True)
+    d = torch.empty(1 << 30, dtype=torch.uint8, device=dev)
+    d.copy_(h, non_blocking=True)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(3):
+        d.copy_(h, non_blocking=True)
+    b.record()
+    b.synchronize()
+    peak = 3 * (1 << 30) / (a.elapsed_time(b) / 1e3) / 1e9
+    rows_per_s = e2e["value"] / max(int(os.environ.get("WORLD_SIZE", "1")), 1)
+    achieved = rows_per_s * e2e["h2d_bytes_per_step"] / e2e["rows_per_step_per_gpu"] / 1e9
+    del h, d
+    return {"bound": "pcie_h2d", "achieved_gbs": round(achieved, 1),
+            "copy_gbs": round(peak, 1), "frac": round(achieved / peak, 3)}
 
 
 def cpu_model() -> str:
