@@ -67,7 +67,7 @@ bool put_count(int32_t* row, Py_ssize_t j, PyObject* v) {
 }
 
 // densify_into(samples, columns: dict[str, int], out: int32 buffer [N, width], width)
-PyObject* densify_into(PyObject*, PyObject* args) {
+PyObject* densify_into_serial(PyObject*, PyObject* args) {
   PyObject *samples, *columns, *out;
   Py_ssize_t width;
   if (!PyArg_ParseTuple(args, "OO!On", &samples, &PyDict_Type, &columns, &out, &width))
@@ -186,6 +186,133 @@ struct KeyTable {
   }
 };
 
+// Threads walk rows' entries dicts (null = skip) and write each count at
+// slot_col[slots[i]][id(key)]; false when any entry is outside the read-only
+// rules (the caller then redoes the call serially).
+bool walk_rows(const std::vector<PyObject*>& ents, const std::vector<int32_t>& slots,
+               const KeyTable& tab, const std::vector<int32_t>& slot_col, int32_t uids,
+               int32_t* x, Py_ssize_t width, int W) {
+  const Py_ssize_t n = static_cast<Py_ssize_t>(ents.size());
+  std::atomic<int> bad{0};
+  auto work = [&](int w) {
+    const Py_ssize_t lo = n * w / W, hi = n * (w + 1) / W;
+    for (Py_ssize_t i = lo; i < hi && !bad.load(std::memory_order_relaxed); ++i) {
+      PyObject* e = ents[size_t(i)];
+      if (!e) continue;
+      const int32_t* cols = slot_col.data() + size_t(slots[size_t(i)]) * uids;
+      int32_t* row = x + i * width;
+      Py_ssize_t pos = 0;
+      PyObject *k, *v;
+      while (PyDict_Next(e, &pos, &k, &v)) {
+        if (!PyUnicode_CheckExact(k) || !PyLong_CheckExact(v)) {
+          bad.store(1);
+          return;
+        }
+        const Py_hash_t h = KeyTable::cached_hash(k);
+        if (h == -1) {
+          bad.store(1);
+          return;
+        }
+        const int32_t id = tab.find(k, h);
+        if (id < 0) continue;
+        const int32_t j = cols[id];
+        if (j < 0) continue;
+        int overflow = 0;
+        const long long c = PyLong_AsLongLongAndOverflow(v, &overflow);
+        if (overflow || c < 0 || c > 2147483647LL) {
+          bad.store(1);
+          return;
+        }
+        row[j] = static_cast<int32_t>(c);
+      }
+    }
+  };
+  std::vector<std::thread> th;
+  th.reserve(size_t(W - 1));
+  for (int w = 1; w < W; ++w) th.emplace_back(work, w);
+  work(0);
+  for (auto& t : th) t.join();
+  return bad.load() == 0;
+}
+
+// Column map (exact str keys -> int columns in [0, width)) as a key table
+// plus uid -> column; false if the map is outside those rules.
+bool column_table(PyObject* columns, Py_ssize_t width, KeyTable& tab, std::vector<int32_t>& col,
+                  int32_t& uids) {
+  tab.reserve(size_t(PyDict_GET_SIZE(columns)) + 1);
+  uids = 0;
+  std::vector<int32_t> tmp;
+  Py_ssize_t pos = 0;
+  PyObject *k, *v;
+  while (PyDict_Next(columns, &pos, &k, &v)) {
+    if (!PyUnicode_CheckExact(k) || !PyLong_CheckExact(v) || PyObject_Hash(k) == -1) {
+      PyErr_Clear();
+      return false;
+    }
+    const Py_ssize_t j = PyLong_AsSsize_t(v);
+    if (j < 0 || j >= width) {
+      PyErr_Clear();
+      return false;
+    }
+    const int32_t id = tab.insert(k, uids);
+    if (id == uids) {
+      ++uids;
+      tmp.push_back(static_cast<int32_t>(j));
+    } else {
+      tmp[size_t(id)] = static_cast<int32_t>(j);
+    }
+  }
+  col = std::move(tmp);
+  if (col.empty()) col.push_back(-1);
+  return true;
+}
+
+// densify_into for >= 8192 samples: every row, one column map, threaded walk
+// (same rules as gather_into); anything unusual -> the serial densify walk.
+PyObject* densify_into_serial(PyObject*, PyObject* args);
+PyObject* densify_into(PyObject* self, PyObject* args) {
+  PyObject *samples, *columns, *out;
+  Py_ssize_t width;
+  if (!PyArg_ParseTuple(args, "OO!On", &samples, &PyDict_Type, &columns, &out, &width))
+    return nullptr;
+  const unsigned hw = std::thread::hardware_concurrency();
+  const int W = static_cast<int>(std::min(hw ? hw : 1u, 32u));
+  const Py_ssize_t n_hint = PyObject_Length(samples);
+  if (n_hint < 0) PyErr_Clear();
+  KeyTable tab;
+  std::vector<int32_t> col;
+  int32_t uids = 0;
+  if (W < 2 || n_hint < 8192 || !column_table(columns, width, tab, col, uids))
+    return densify_into_serial(self, args);
+  PyObject* seq = PySequence_Fast(samples, "samples must be a sequence");
+  if (!seq) return nullptr;
+  const Py_ssize_t n = PySequence_Fast_GET_SIZE(seq);
+  Buf b;
+  if (!b.get(out, 4, n * width)) {
+    Py_DECREF(seq);
+    return nullptr;
+  }
+  std::vector<PyObject*> ents(size_t(n), nullptr);
+  std::vector<int32_t> slots(size_t(n), 0);
+  auto release = [&] {
+    for (PyObject* e : ents) Py_XDECREF(e);
+    Py_DECREF(seq);
+  };
+  for (Py_ssize_t i = 0; i < n; ++i) {
+    PyObject* e = entries_of(PySequence_Fast_GET_ITEM(seq, i));
+    if (!e) {
+      release();
+      return nullptr;
+    }
+    ents[size_t(i)] = e;
+  }
+  const bool ok = walk_rows(ents, slots, tab, col, uids, static_cast<int32_t*>(b.view.buf),
+                            width, W);
+  release();
+  if (!ok) return densify_into_serial(self, args);
+  Py_RETURN_NONE;
+}
+
 PyObject* gather_into(PyObject* self, PyObject* args) {
   PyObject *samples, *route_o, *colmaps, *out, *sizes_o;
   Py_ssize_t width, group_width, limit;
@@ -280,52 +407,12 @@ PyObject* gather_into(PyObject* self, PyObject* args) {
     sz[i] = static_cast<int32_t>(size);
   }
   // 2. parallel dict walks (reads only; see above)
-  std::atomic<int> bad{0};
-  if (!serial) {
-    auto work = [&](int w) {
-      const Py_ssize_t lo = n * w / W, hi = n * (w + 1) / W;
-      for (Py_ssize_t i = lo; i < hi && !bad.load(std::memory_order_relaxed); ++i) {
-        PyObject* e = ents[size_t(i)];
-        if (!e) continue;
-        const int32_t* cols = slot_col.data() + size_t(slots[size_t(i)]) * uids;
-        int32_t* row = x + i * width;
-        Py_ssize_t pos = 0;
-        PyObject *k, *v;
-        while (PyDict_Next(e, &pos, &k, &v)) {
-          if (!PyUnicode_CheckExact(k) || !PyLong_CheckExact(v)) {
-            bad.store(1);
-            return;
-          }
-          const Py_hash_t h = KeyTable::cached_hash(k);
-          if (h == -1) {
-            bad.store(1);
-            return;
-          }
-          const int32_t id = tab.find(k, h);
-          if (id < 0) continue;
-          const int32_t j = cols[id];
-          if (j < 0) continue;
-          int overflow = 0;
-          const long long c = PyLong_AsLongLongAndOverflow(v, &overflow);
-          if (overflow || c < 0 || c > 2147483647LL) {
-            bad.store(1);
-            return;
-          }
-          row[j] = static_cast<int32_t>(c);
-        }
-      }
-    };
-    std::vector<std::thread> th;
-    th.reserve(size_t(W - 1));
-    for (int w = 1; w < W; ++w) th.emplace_back(work, w);
-    work(0);
-    for (auto& t : th) t.join();
-  }
+  const bool bad = !serial && !walk_rows(ents, slots, tab, slot_col, uids, x, width, W);
   // rows outside [0, limit) (their ents entry is null) get size -1
   for (Py_ssize_t i = 0; i < n; ++i)
     if (!ents[size_t(i)] && !serial) sz[i] = -1;
   release();
-  if (serial || bad.load()) return gather_into_serial(self, args);
+  if (serial || bad) return gather_into_serial(self, args);
   Py_RETURN_NONE;
 }
 
@@ -773,6 +860,8 @@ PyMethodDef kMethods[] = {
      "gather_into(samples, route, colmaps, width, group_width, limit, out, sizes_out)."},
     {"vocab_dense", vocab_dense, METH_VARARGS,
      "vocab_dense(samples) -> (sorted opcodes, int32 bytearray [N, max(V, 1)]) or None."},
+    {"densify_into_serial", densify_into_serial, METH_VARARGS,
+     "densify_into on the calling thread only (the reference walk for tests)."},
     {"gather_into_serial", gather_into_serial, METH_VARARGS,
      "gather_into on the calling thread only (the reference walk for tests)."},
     {"meta_into", meta_into, METH_VARARGS,

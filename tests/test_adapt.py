@@ -185,3 +185,30 @@ def test_vocab_dense_matches_serial(case, monkeypatch):
     x_ser, v_ser = api._dense_vocab(s)
     assert v_fast == v_ser == sorted(v_ser)
     assert np.array_equal(x_fast, x_ser)
+
+
+@pytest.mark.parametrize("case", ["plain", "nonstr_key", "big_count", "empty_map"])
+def test_parallel_densify_matches_serial(case):
+    """densify_into (threaded for >= 8192 samples) == the serial walk; unusual
+    inputs take the serial path and raise its errors."""
+    rng = np.random.default_rng(11)
+    s = _samples(rng, 10_000)
+    cols = {} if case == "empty_map" else {f"op{i}": (i * 7) % 15 for i in range(0, 30, 2)}
+    if case == "nonstr_key":
+        s[5000].histogram.entries[3] = 9
+    if case == "big_count":
+        s[9000] = SampleRecord("big", Label.MALWARE, 100,
+                               OpcodeHistogram.from_counts({"op2": 2**40}))
+    outs = []
+    for fn in (_adapt.densify_into, _adapt.densify_into_serial):
+        x = np.zeros((len(s), 15), np.int32)
+        try:
+            fn(s, cols, x, 15)
+            outs.append(x)
+        except Exception as e:  # noqa: BLE001
+            outs.append(type(e))
+    if case == "big_count":
+        assert outs[0] == outs[1] and isinstance(outs[0], type)
+    else:
+        assert np.array_equal(outs[0], outs[1])
+        assert outs[0].any() == (case != "empty_map")
