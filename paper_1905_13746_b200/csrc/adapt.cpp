@@ -666,8 +666,11 @@ PyObject* predictions(PyObject*, PyObject* args) {
   } else {
     // no cyclic-GC passes while allocating ~2 containers per row (they cost
     // more than the construction itself); the previous state is restored
+    // Label is an Enum: its __hash__ is Python code (~250 ns a call), so the
+    // two class keys are hashed once here, not twice per Prediction
+    const Py_hash_t h_malware = PyObject_Hash(malware), h_benign = PyObject_Hash(benign);
     const int gc_was_on = PyGC_Disable();
-    out = PyList_New(n);
+    out = (h_malware == -1 || h_benign == -1) ? nullptr : PyList_New(n);
     const int32_t* lab = static_cast<const int32_t*>(bl.buf);
     const double* lp = static_cast<const double*>(bp.buf);
     const int32_t* eff = static_cast<const int32_t*>(be.buf);
@@ -682,8 +685,9 @@ PyObject* predictions(PyObject*, PyObject* args) {
       PyObject* fm = PyFloat_FromDouble(lp[2 * i + 1]);
       PyObject* fb = PyFloat_FromDouble(lp[2 * i]);
       PyObject* g = PyLong_FromLong(eff[i]);
-      bool ok = obj && d && fm && fb && g && PyDict_SetItem(d, malware, fm) == 0 &&
-                PyDict_SetItem(d, benign, fb) == 0 &&
+      bool ok = obj && d && fm && fb && g &&
+                _PyDict_SetItem_KnownHash(d, malware, fm, h_malware) == 0 &&
+                _PyDict_SetItem_KnownHash(d, benign, fb, h_benign) == 0 &&
                 PyObject_GenericSetAttr(obj, s_f_label, PyTuple_GET_ITEM(classes, lab[i])) == 0 &&
                 PyObject_GenericSetAttr(obj, s_f_logpost, d) == 0 &&
                 PyObject_GenericSetAttr(obj, s_f_group, g) == 0;
