@@ -358,7 +358,8 @@ def run_ours(args, world, rank, local):
 
     # ---- end to end through the C ABI with host (pinned) buffers
     e2e = None
-    host_dtype = "uint8" if int(xg.max()) < 256 else ("uint16" if int(xg.max()) < 65536 else "int32")
+    xmax = _max_count(xg)
+    host_dtype = "uint8" if xmax < 256 else ("uint16" if xmax < 65536 else "int32")
     if not args.no_e2e:
         # rows per rank: the e2e number is a throughput; keep the job's pinned
         # host memory bounded as ranks are added (all ranks share one host)
@@ -409,7 +410,7 @@ def run_ours(args, world, rank, local):
                     "matches_device_labels": ok}
 
         # counts < 16 (the synthetic law's ~0.5 mean per cell): two per byte
-        e2e_dtype = "uint4" if int(xg[:m].max()) < 16 else host_dtype
+        e2e_dtype = "uint4" if _max_count(xg[:m]) < 16 else host_dtype
         e2e = e2e_run(e2e_dtype)
         if e2e_dtype != host_dtype and world == 1:
             e2e[f"{host_dtype}_host_rows"] = {k: v for k, v in e2e_run(host_dtype).items()
@@ -619,6 +620,12 @@ def object_api_leg(n, V, device):
             "classify_parallel_wall_samples_per_s": round(n / cls_s, 1),
             "classify_parallel_elapsed_samples_per_s": round(n / (run.elapsed_ns / 1e9), 1),
             "accuracy": round(acc, 4)}
+
+
+def _max_count(t):
+    """Largest count of a device row block (torch has no max kernel for uint16)."""
+    import torch
+    return int((t.to(torch.int32) if t.dtype == torch.uint16 else t).max())
 
 
 def reference_python_leg(n, V):

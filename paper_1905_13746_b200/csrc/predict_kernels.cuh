@@ -71,8 +71,15 @@ __device__ __forceinline__ double converted(const uint4& v, int e) {
   if constexpr (sz == 4) {
     return __uint2double_rn(w);
   } else {
+    // cvt from a .u8/.u16 source of the shifted word: ptxas folds the shift
+    // into the I2F byte/half-word selector (I2F.F64.U8 Rx.B1..B3, .U16 Rx.H1),
+    // where `(w >> s) & mask` cost a SHF + LOP3 per element before the I2F
     constexpr int bits = 8 * sz;
-    return __uint2double_rn((w >> ((e * bits) & 31)) & ((1u << bits) - 1u));
+    const uint32_t s = w >> ((e * bits) & 31);
+    double d;
+    if constexpr (sz == 1) asm("cvt.rn.f64.u8 %0, %1;" : "=d"(d) : "r"(s));
+    else asm("cvt.rn.f64.u16 %0, %1;" : "=d"(d) : "r"(s));
+    return d;
   }
 }
 
