@@ -64,10 +64,18 @@ struct Elem<int32_t> {
 // is exact (counts < 2^32) and runs on the conversion unit (I2F.F64; for
 // uint8/uint16 with a byte/half-word source select), so the product below is
 // ONE DMUL rounding, exactly the reference's `n * ll` (a Python float multiply).
-template <typename T>
+// FMA mode on uint8 rows (XU-bound): odd elements are converted on the FP64
+// pipe instead, as (2^52 | x) - 2^52 (exact: one PRMT builds the low word, one
+// DADD), so I2F and the DFMA chain share the load.
+template <typename T, bool FMA = false>
 __device__ __forceinline__ double converted(const uint4& v, int e) {
   constexpr int sz = static_cast<int>(sizeof(T));
   const uint32_t w = (e * sz) < 4 ? v.x : (e * sz) < 8 ? v.y : (e * sz) < 12 ? v.z : v.w;
+  if constexpr (FMA && sz == 1) {
+    if (e & 1)  // half: 3 of 4 measured slower (13.3 vs 13.7 G/s)
+      return __dadd_rn(__hiloint2double(0x43300000, static_cast<int>(__byte_perm(w, 0, 0x4440 + (e & 3)))),
+                       -4503599627370496.0);
+  }
   if constexpr (sz == 4) {
     return __uint2double_rn(w);
   } else {
@@ -103,7 +111,7 @@ __device__ __forceinline__ void score_quad(double (&acc)[CP], const uint4 v, con
                                            int feat0) {
 #pragma unroll
   for (int e = 0; e < Elem<T>::kPerQuad; ++e) {
-    const double xd = converted<T>(v, e);
+    const double xd = converted<T, FMA>(v, e);
 #pragma unroll
     for (int c = 0; c < CP; ++c)
       acc[c] = madd<FMA>(acc[c], xd, tab.get((feat0 + e) * CP + c));
@@ -225,7 +233,7 @@ __device__ __forceinline__ void score_chunk_uniform(double (&acc)[R][CP], const 
       }
 #pragma unroll
       for (int i = 0; i < R; ++i) {
-        const double xd = converted<T>(v[i], e);
+        const double xd = converted<T, FMA>(v[i], e);
 #pragma unroll
         for (int c = 0; c < CP; ++c) acc[i][c] = madd<FMA>(acc[i][c], xd, t[c]);
       }
@@ -506,7 +514,7 @@ __device__ __forceinline__ void rowbox_score_smem(double (&acc)[CP], const uint8
     if (Elem<T>::kSigned) neg |= v.x | v.y | v.z | v.w;
 #pragma unroll
     for (int e = 0; e < EQ; ++e) {
-      const double xd = converted<T>(v, e);
+      const double xd = converted<T, FMA>(v, e);
 #pragma unroll
       for (int c = 0; c < CP; c += 2) {  // broadcast LDS.128 per 2 classes
         const double2 t2 = *reinterpret_cast<const double2*>(tab + (EQ * q + e) * CP + c);
@@ -686,7 +694,7 @@ __global__ void __launch_bounds__(5 * 32, MINB)
               if (Elem<T>::kSigned) neg |= v[q].x | v[q].y | v[q].z | v[q].w;
 #pragma unroll
               for (int e = 0; e < EQ; ++e) {
-                const double xd = converted<T>(v[q], e);
+                const double xd = converted<T, FMA>(v[q], e);
 #pragma unroll
                 for (int c = 0; c < CP; c += 2) {
                   const double2 t2 =
