@@ -94,6 +94,32 @@ def peaks():
         return 6650.0, "fallback"
 
 
+def live_copy_gbs():
+    """This box's device copy bandwidth, measured the way MEASURED_PEAKS.json's
+    hbm_gbs is (b.copy_(a) over 1 Gi bf16 elements, read + write bytes, best of
+    10, CUDA events): reported beside `peak` so a frac above 1 (a box faster than
+    the pod's figure) can be read against the same box."""
+    import torch
+    try:
+        a = torch.empty(1 << 30, dtype=torch.bfloat16, device="cuda")
+        b = torch.empty_like(a)
+        b.copy_(a)
+        best = None
+        for _ in range(10):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            b.copy_(a)
+            e1.record()
+            e1.synchronize()
+            ms = e0.elapsed_time(e1)
+            best = ms if best is None else min(best, ms)
+        del a, b
+        torch.cuda.empty_cache()
+        return 2 * (1 << 30) * 2 / (best / 1e3) / 1e9
+    except Exception:
+        return None
+
+
 def ncu_traffic():
     """Per-sample DRAM bytes of K-PRED from the committed ncu --set full capture."""
     try:
@@ -355,6 +381,10 @@ def run_ours(args, world, rank, local):
                 "peak_spec": SPEC_HBM_GBS, "frac_spec": round(achieved / SPEC_HBM_GBS, 4)}
     if ncu:
         roofline["traffic_source"] = ncu.get("source")
+    live = live_copy_gbs()
+    if live:
+        roofline["live_copy_gbs"] = round(live, 1)
+        roofline["frac_live_copy"] = round(achieved / live, 4)
 
     # ---- end to end through the C ABI with host (pinned) buffers
     e2e = None
