@@ -1,6 +1,6 @@
 """K-PRED on uint8 rows (cfg4 shape, 16M rows): one warm launch, then one more
 for ncu (`-k regex:predict_tma -s 1 -c 1`).  Prints the plain timing of 10
-launches when run without ncu.  gpurun -- python tools/u8_probe.py [--fma]"""
+launches when run without ncu.  gpurun -- python tools/u8_probe.py [--fma] [--u16]"""
 import os
 import sys
 import time
@@ -20,7 +20,8 @@ fin = dense.fin_train(st.sums.cpu().numpy(), st.counts.cpu().numpy(), k=V, alpha
 F = int(fin.n_features[0])
 dense.generate(n, F, divergence=0.8, seed=0, col_map=fin.features[0, :F].copy(),
                out=(x[:, :F], size, lab), device=dev)
-xg = x[:, :F].to(torch.uint8)
+xdt = torch.uint16 if "--u16" in sys.argv else torch.uint8
+xg = x[:, :F].to(xdt)
 del x
 t = dense.DeviceTables.build(fin.log_prior[:1], fin.log_lik[:1, :, :F], np.zeros(1, np.int32),
                              group_size_bytes=width, max_size_bytes=width, device=dev)
@@ -37,5 +38,5 @@ for _ in range(10):
 b.record()
 b.synchronize()
 ms = a.elapsed_time(b) / 10
-print(f"uint8 {mode}: {ms:.3f} ms/launch, {n / ms / 1e6:.2f} G samples/s, "
-      f"{n * (F + 24) / ms / 1e6:.0f} GB/s")
+print(f"{str(xdt)[6:]} {mode}: {ms:.3f} ms/launch, {n / ms / 1e6:.2f} G samples/s, "
+      f"{n * (F * xg.element_size() + 24) / ms / 1e6:.0f} GB/s")
