@@ -17,7 +17,7 @@ ADAPT := $(PKG)/_adapt$(PYEXT)
 all: $(PKG)/libgnb.so $(ADAPT) oracle
 
 $(ADAPT): $(PKG)/csrc/adapt.cpp
-	g++ -O3 -std=c++17 -fPIC -shared -I$(PYINC) -o $@ $<
+	g++ -O3 -std=c++17 -ffp-contract=off -fPIC -shared -I$(PYINC) -o $@ $<
 
 # one object per translation unit so `make -j` compiles the K-PRED instances in parallel
 $(OBJDIR)/%.o: $(PKG)/csrc/%.cu $(HDR)

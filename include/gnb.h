@@ -163,6 +163,15 @@ int gnb_gather_features(const int32_t* x_vocab, int64_t n_rows, int32_t n_vocab,
                         const int32_t* n_features, int32_t n_slots, int32_t max_features,
                         int32_t* x_out, int64_t ldo, uintptr_t stream);
 
+/* gnb_gather_features for x_vocab stored as x_type (GNB_X_I32/U16/U8); x_out
+ * has the same element type (narrow rows stay narrow for gnb_predict_typed). */
+int gnb_gather_features_typed(const void* x_vocab, int32_t x_type, int64_t n_rows,
+                              int32_t n_vocab, int64_t ldx, const int32_t* size_bytes,
+                              int32_t group_size_bytes, int32_t max_size_bytes,
+                              const int32_t* route, const int32_t* features,
+                              const int32_t* n_features, int32_t n_slots, int32_t max_features,
+                              void* x_out, int64_t ldo, uintptr_t stream);
+
 /* gnb_predict_host for host rows stored as x_type (GNB_X_I32/U16/U8/U4), ldx
  * in elements (features): narrow storage moves 2x/4x/8x fewer bytes over PCIe. */
 int gnb_predict_host_typed(const void* x, int32_t x_type, int64_t n_rows, int32_t n_features,
@@ -171,6 +180,18 @@ int gnb_predict_host_typed(const void* x, int32_t x_type, int64_t n_rows, int32_
                            int32_t n_classes, const double* log_prior, const double* log_lik,
                            int32_t* label_out, double* logpost_out, int32_t device,
                            int64_t* elapsed_ns);
+
+/* Several GPUs in one call: rows cut into ceil(n / n_devices) contiguous
+ * shards, one per device (the reference's lane chunking, engine.py:264-268),
+ * each streamed through that device by its own host thread exactly as
+ * gnb_predict_host_typed does; no exchange (tables replicated, rows
+ * independent).  elapsed_ns = the slowest device's pipeline time. */
+int gnb_predict_host_sharded(const void* x, int32_t x_type, int64_t n_rows, int32_t n_features,
+                             int64_t ldx, const int32_t* size_bytes, int32_t group_size_bytes,
+                             int32_t max_size_bytes, const int32_t* route, int32_t n_slots,
+                             int32_t n_classes, const double* log_prior, const double* log_lik,
+                             int32_t* label_out, double* logpost_out, int32_t n_devices,
+                             const int32_t* devices, int64_t* elapsed_ns);
 
 /* ------------------------------------------------------------------ fit
  * Replaces: the sample x histogram count loops of features.class_frequency
@@ -206,6 +227,16 @@ int gnb_fit_stats_host(const int32_t* x, int64_t n_rows, int32_t n_cols, int64_t
                        int32_t group_size_bytes, int32_t max_size_bytes, int32_t n_classes,
                        double* sums, double* sumsq, double* counts,
                        unsigned long long* status, int32_t device);
+
+/* gnb_fit_stats_host over several GPUs: contiguous row shards, K-FIT on each
+ * device, then the one exchange -- the integer-valued statistics summed
+ * (exact in any order, so identical to one device). */
+int gnb_fit_stats_host_sharded(const int32_t* x, int64_t n_rows, int32_t n_cols, int64_t ldx,
+                               const int32_t* size_bytes, const int32_t* labels,
+                               int32_t group_size_bytes, int32_t max_size_bytes,
+                               int32_t n_classes, double* sums, double* sumsq, double* counts,
+                               unsigned long long* status, int32_t n_devices,
+                               const int32_t* devices);
 
 /* ------------------------------------------------------------------ finalize (host)
  * Replaces: features.score_opcodes + select_top_k (features.py:59-86) and the

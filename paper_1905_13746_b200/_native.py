@@ -65,8 +65,14 @@ _SIGS = {
                           _i32, _p], C.c_int),
     "gnb_gather_features": ([_p, _i64, _i32, _i64, _p, _i32, _i32, _p, _p, _p, _i32, _i32, _p,
                              _i64, _up], C.c_int),
+    "gnb_gather_features_typed": ([_p, _i32, _i64, _i32, _i64, _p, _i32, _i32, _p, _p, _p,
+                                   _i32, _i32, _p, _i64, _up], C.c_int),
     "gnb_predict_host_typed": ([_p, _i32, _i64, _i32, _i64, _p, _i32, _i32, _p, _i32, _i32, _p,
                                 _p, _p, _p, _i32, _p], C.c_int),
+    "gnb_predict_host_sharded": ([_p, _i32, _i64, _i32, _i64, _p, _i32, _i32, _p, _i32, _i32,
+                                  _p, _p, _p, _p, _i32, _p, _p], C.c_int),
+    "gnb_fit_stats_host_sharded": ([_p, _i64, _i32, _i64, _p, _p, _i32, _i32, _i32, _p, _p, _p,
+                                    _p, _i32, _p], C.c_int),
     "gnb_fit_stats": ([_p, _i64, _i32, _i64, _p, _p, _i32, _i32, _i32, _p, _p, _p, _p, _i32, _up],
                       C.c_int),
     "gnb_fit_stats_typed": ([_p, _i32, _i64, _i32, _i64, _p, _p, _i32, _i32, _i32, _p, _p, _p,

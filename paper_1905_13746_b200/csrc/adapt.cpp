@@ -404,7 +404,7 @@ PyObject* gather_into(PyObject* self, PyObject* args) {
     }
     ents[size_t(i)] = e;
     slots[size_t(i)] = slot;
-    sz[i] = static_cast<int32_t>(size);
+    sz[i] = static_cast<int32_t>(size / group_width);  // size group id (any size range)
   }
   // 2. parallel dict walks (reads only; see above)
   const bool bad = !serial && !walk_rows(ents, slots, tab, slot_col, uids, x, width, W);
@@ -543,7 +543,9 @@ PyObject* vocab_dense(PyObject*, PyObject* args) {
 // gather_into(samples, route: int32 buffer [G], colmaps: list[dict], width, limit,
 //             out: int32 [N, width], sizes_out: int32 [N])
 // Row i gets the counts of its routed model's features (FeatureSet order);
-// sizes outside [0, limit) become -1 and leave the row zero.
+// sizes_out[i] = its size group (size // group_width), or -1 (row left zero)
+// for sizes outside [0, limit): callers score with width 1 / limit G, so
+// size ranges beyond int32 route exactly.
 PyObject* gather_into_serial(PyObject*, PyObject* args) {
   PyObject *samples, *route_o, *colmaps, *out, *sizes_o;
   Py_ssize_t width, group_width, limit;
@@ -581,7 +583,7 @@ PyObject* gather_into_serial(PyObject*, PyObject* args) {
       sz[i] = -1;
       continue;
     }
-    sz[i] = static_cast<int32_t>(size);
+    sz[i] = static_cast<int32_t>(size / group_width);  // size group id (any size range)
     const int32_t slot = route[size / group_width];
     if (slot < 0 || slot >= S) {
       PyErr_SetString(PyExc_IndexError, "route entry out of range");
@@ -709,6 +711,257 @@ PyObject* predictions(PyObject*, PyObject* args) {
   PyBuffer_Release(&bp);
   PyBuffer_Release(&be);
   return out;
+}
+
+// ------------------------------------------------------------------ sequential scoring (Tc)
+// classifier.log_posterior (pkg/src/groupnb/classifier.py:132-148) over a
+// model's `_packed` rows, exactly: score_c = log_prior[c]; for (op, ll_m,
+// ll_b) in feature order: n = entries.get(op); if n is not None:
+// score_m += n * ll_m; score_b += n * ll_b.  For an int count CPython computes
+// `n * ll` as float(n) (correctly rounded; OverflowError past the double
+// range) times ll, one rounding, then one rounding for the add -- the doubles
+// below do the same (built without FMA contraction).  Anything else (a float
+// count, a non-float parameter) switches to the generic number protocol, i.e.
+// literally the reference's expressions.
+PyObject* s_packed = nullptr;
+PyObject* s_log_prior = nullptr;
+PyObject* s_group = nullptr;
+
+struct Score {
+  PyObject* m = nullptr;  // new references
+  PyObject* b = nullptr;
+};
+
+bool score_packed_impl(PyObject* packed, PyObject* prior_m, PyObject* prior_b, PyObject* entries,
+                       Score* out) {
+  if (!PyTuple_Check(packed) || !PyDict_Check(entries)) {
+    PyErr_SetString(PyExc_TypeError, "_packed must be a tuple and entries a dict");
+    return false;
+  }
+  const Py_ssize_t F = PyTuple_GET_SIZE(packed);
+  bool fast = PyFloat_CheckExact(prior_m) && PyFloat_CheckExact(prior_b);
+  double dm = fast ? PyFloat_AS_DOUBLE(prior_m) : 0.0, db = fast ? PyFloat_AS_DOUBLE(prior_b) : 0.0;
+  PyObject* om = nullptr;  // generic accumulators (owned) once !fast
+  PyObject* ob = nullptr;
+  if (!fast) {
+    Py_INCREF(prior_m);
+    Py_INCREF(prior_b);
+    om = prior_m;
+    ob = prior_b;
+  }
+  for (Py_ssize_t j = 0; j < F; ++j) {
+    PyObject* row = PyTuple_GET_ITEM(packed, j);
+    if (!PyTuple_Check(row) || PyTuple_GET_SIZE(row) != 3) {
+      PyErr_SetString(PyExc_TypeError, "_packed rows must be (op, ll_m, ll_b)");
+      Py_XDECREF(om);
+      Py_XDECREF(ob);
+      return false;
+    }
+    PyObject* n = PyDict_GetItemWithError(entries, PyTuple_GET_ITEM(row, 0));
+    if (!n) {
+      if (PyErr_Occurred()) {
+        Py_XDECREF(om);
+        Py_XDECREF(ob);
+        return false;
+      }
+      continue;
+    }
+    PyObject* lm = PyTuple_GET_ITEM(row, 1);
+    PyObject* lb = PyTuple_GET_ITEM(row, 2);
+    if (fast && PyLong_CheckExact(n) && PyFloat_CheckExact(lm) && PyFloat_CheckExact(lb)) {
+      const double x = PyLong_AsDouble(n);
+      if (x == -1.0 && PyErr_Occurred()) return false;
+      const double pm = x * PyFloat_AS_DOUBLE(lm);
+      const double pb = x * PyFloat_AS_DOUBLE(lb);
+      dm = dm + pm;
+      db = db + pb;
+      continue;
+    }
+    if (fast) {  // switch to objects from here on
+      fast = false;
+      om = PyFloat_FromDouble(dm);
+      ob = PyFloat_FromDouble(db);
+      if (!om || !ob) {
+        Py_XDECREF(om);
+        Py_XDECREF(ob);
+        return false;
+      }
+    }
+    PyObject* tm = PyNumber_Multiply(n, lm);
+    PyObject* nm = tm ? PyNumber_Add(om, tm) : nullptr;
+    Py_XDECREF(tm);
+    PyObject* tb = nm ? PyNumber_Multiply(n, lb) : nullptr;
+    PyObject* nb = tb ? PyNumber_Add(ob, tb) : nullptr;
+    Py_XDECREF(tb);
+    Py_DECREF(om);
+    Py_DECREF(ob);
+    om = nm;
+    ob = nb;
+    if (!om || !ob) {
+      Py_XDECREF(om);
+      Py_XDECREF(ob);
+      return false;
+    }
+  }
+  if (fast) {
+    out->m = PyFloat_FromDouble(dm);
+    out->b = PyFloat_FromDouble(db);
+    if (!out->m || !out->b) {
+      Py_CLEAR(out->m);
+      Py_CLEAR(out->b);
+      return false;
+    }
+  } else {
+    out->m = om;
+    out->b = ob;
+  }
+  return true;
+}
+
+// score_packed(packed, prior_m, prior_b, entries) -> (score_m, score_b)
+PyObject* score_packed(PyObject*, PyObject* args) {
+  PyObject *packed, *pm, *pb, *entries;
+  if (!PyArg_ParseTuple(args, "OOOO", &packed, &pm, &pb, &entries)) return nullptr;
+  Score sc;
+  if (!score_packed_impl(packed, pm, pb, entries, &sc)) return nullptr;
+  return Py_BuildValue("(NN)", sc.m, sc.b);
+}
+
+struct ModelPrep {
+  PyObject* packed;  // borrowed from the model (kept alive by `models`)
+  PyObject* prior_m;
+  PyObject* prior_b;
+  PyObject* group;   // owned
+};
+
+// classify_slice(samples, route_table: tuple, models: dict, width, limit,
+//                Prediction, malware, benign) -> (predictions list, error indices list)
+// engine._classify_slice (pkg/src/groupnb/engine.py:187-206) on ONE thread --
+// the Tc side of the reference's speedup ratio, "never parallelized
+// internally" (engine.py:212-215): per sample the range check, the route
+// table lookup, the log_posterior above and `malware iff strictly higher`
+// (classifier.py:151-158); None + an error index outside [0, limit).
+PyObject* classify_slice(PyObject*, PyObject* args) {
+  PyObject *samples, *table, *models, *type_o, *malware, *benign;
+  Py_ssize_t width;
+  long long limit;
+  if (!PyArg_ParseTuple(args, "OO!O!nLO!OO", &samples, &PyTuple_Type, &table, &PyDict_Type,
+                        &models, &width, &limit, &PyType_Type, &type_o, &malware, &benign))
+    return nullptr;
+  if (width <= 0) {
+    PyErr_SetString(PyExc_ValueError, "width must be positive");
+    return nullptr;
+  }
+  PyObject* seq = PySequence_Fast(samples, "samples must be a sequence");
+  if (!seq) return nullptr;
+  const Py_ssize_t n = PySequence_Fast_GET_SIZE(seq);
+  PyTypeObject* tp = reinterpret_cast<PyTypeObject*>(type_o);
+  PyObject* out = PyList_New(n);
+  PyObject* errs = PyList_New(0);
+  PyObject* empty = PyTuple_New(0);
+  std::vector<std::pair<PyObject*, ModelPrep>> cache;  // model -> prepared rows (few models)
+  bool ok = out && errs && empty;
+  for (Py_ssize_t i = 0; ok && i < n; ++i) {
+    PyObject* s = PySequence_Fast_GET_ITEM(seq, i);
+    PyObject* so = PyObject_GetAttr(s, s_size_bytes);
+    if (!so) {
+      ok = false;
+      break;
+    }
+    if (!PyLong_Check(so)) {
+      Py_DECREF(so);
+      PyErr_SetString(PyExc_TypeError, "size_bytes must be an int");
+      ok = false;
+      break;
+    }
+    int overflow = 0;
+    const long long size = PyLong_AsLongLongAndOverflow(so, &overflow);
+    Py_DECREF(so);
+    if (size == -1 && PyErr_Occurred()) {
+      ok = false;
+      break;
+    }
+    if (overflow || size < 0 || size >= limit) {
+      Py_INCREF(Py_None);
+      PyList_SET_ITEM(out, i, Py_None);
+      PyObject* idx = PyLong_FromSsize_t(i);
+      ok = idx && PyList_Append(errs, idx) == 0;
+      Py_XDECREF(idx);
+      continue;
+    }
+    const long long g = size / width;
+    if (g >= PyTuple_GET_SIZE(table)) {
+      PyErr_SetString(PyExc_IndexError, "tuple index out of range");
+      ok = false;
+      break;
+    }
+    PyObject* model = PyDict_GetItemWithError(models, PyTuple_GET_ITEM(table, g));
+    if (!model) {
+      if (!PyErr_Occurred()) PyErr_SetObject(PyExc_KeyError, PyTuple_GET_ITEM(table, g));
+      ok = false;
+      break;
+    }
+    const ModelPrep* mp = nullptr;
+    for (auto& c : cache)
+      if (c.first == model) mp = &c.second;
+    if (!mp) {
+      ModelPrep np{};
+      PyObject* lp = PyObject_GetAttr(model, s_log_prior);
+      np.packed = PyObject_GetAttr(model, s_packed);
+      np.group = PyObject_GetAttr(model, s_group);
+      np.prior_m = lp ? PyObject_GetItem(lp, malware) : nullptr;
+      np.prior_b = np.prior_m ? PyObject_GetItem(lp, benign) : nullptr;
+      Py_XDECREF(lp);
+      if (!np.packed || !np.group || !np.prior_m || !np.prior_b) {
+        Py_XDECREF(np.packed);
+        Py_XDECREF(np.group);
+        Py_XDECREF(np.prior_m);
+        Py_XDECREF(np.prior_b);
+        ok = false;
+        break;
+      }
+      cache.emplace_back(model, np);
+      mp = &cache.back().second;
+    }
+    PyObject* e = entries_of(s);
+    if (!e) {
+      ok = false;
+      break;
+    }
+    Score sc;
+    ok = score_packed_impl(mp->packed, mp->prior_m, mp->prior_b, e, &sc);
+    Py_DECREF(e);
+    if (!ok) break;
+    const int gt = PyObject_RichCompareBool(sc.m, sc.b, Py_GT);
+    PyObject* obj = gt < 0 ? nullptr : tp->tp_new(tp, empty, nullptr);
+    PyObject* d = obj ? PyDict_New() : nullptr;
+    ok = d && PyDict_SetItem(d, malware, sc.m) == 0 && PyDict_SetItem(d, benign, sc.b) == 0 &&
+         PyObject_GenericSetAttr(obj, s_f_label, gt ? malware : benign) == 0 &&
+         PyObject_GenericSetAttr(obj, s_f_logpost, d) == 0 &&
+         PyObject_GenericSetAttr(obj, s_f_group, mp->group) == 0;
+    Py_XDECREF(d);
+    Py_DECREF(sc.m);
+    Py_DECREF(sc.b);
+    if (!ok) {
+      Py_XDECREF(obj);
+      break;
+    }
+    PyList_SET_ITEM(out, i, obj);
+  }
+  for (auto& c : cache) {
+    Py_DECREF(c.second.packed);
+    Py_DECREF(c.second.group);
+    Py_DECREF(c.second.prior_m);
+    Py_DECREF(c.second.prior_b);
+  }
+  Py_XDECREF(empty);
+  Py_DECREF(seq);
+  if (!ok) {
+    Py_XDECREF(out);
+    Py_XDECREF(errs);
+    return nullptr;
+  }
+  return Py_BuildValue("(NN)", out, errs);
 }
 
 // discover_into(samples, columns: dict (grown), ops: list (grown), out int32 [N, width], width)
@@ -861,7 +1114,7 @@ PyMethodDef kMethods[] = {
     {"densify_into", densify_into, METH_VARARGS,
      "densify_into(samples, columns, out, width): counts of `columns` per sample."},
     {"gather_into", gather_into, METH_VARARGS,
-     "gather_into(samples, route, colmaps, width, group_width, limit, out, sizes_out)."},
+     "gather_into(samples, route, colmaps, width, group_width, limit, out, group_ids_out)."},
     {"vocab_dense", vocab_dense, METH_VARARGS,
      "vocab_dense(samples) -> (sorted opcodes, int32 bytearray [N, max(V, 1)]) or None."},
     {"densify_into_serial", densify_into_serial, METH_VARARGS,
@@ -874,6 +1127,11 @@ PyMethodDef kMethods[] = {
      "discover_into(samples, columns, ops, out, width) -> bool (vocabulary fit in width)."},
     {"permute_columns", permute_columns, METH_VARARGS,
      "permute_columns(src, src_width, order, dst): dst[:, j] = src[:, order[j]]."},
+    {"score_packed", score_packed, METH_VARARGS,
+     "score_packed(model._packed, prior_m, prior_b, entries) -> (score_m, score_b)."},
+    {"classify_slice", classify_slice, METH_VARARGS,
+     "classify_slice(samples, route_table, models, width, limit, Prediction, malware, benign)"
+     " -> (predictions, error_indices): engine._classify_slice on one thread."},
     {"predictions", predictions, METH_VARARGS,
      "predictions(label, logpost, eff, Prediction, classes, MALWARE, BENIGN) -> list."},
     {nullptr, nullptr, 0, nullptr}};
@@ -891,5 +1149,8 @@ PyMODINIT_FUNC PyInit__adapt(void) {
   s_f_label = s_label;
   s_f_logpost = PyUnicode_InternFromString("log_posterior");
   s_f_group = PyUnicode_InternFromString("effective_group");
+  s_packed = PyUnicode_InternFromString("_packed");
+  s_log_prior = PyUnicode_InternFromString("log_prior");
+  s_group = PyUnicode_InternFromString("group");
   return PyModule_Create(&kModule);
 }

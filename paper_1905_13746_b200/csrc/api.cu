@@ -1,6 +1,7 @@
 // C ABI of libgnb.so (declared in include/gnb.h): argument checking, TMA
 // tensor-map encoding, the device entry points and the host-buffer pipelines.
 #include <algorithm>
+#include <array>
 #include <atomic>
 #include <chrono>
 #include <condition_variable>
@@ -518,11 +519,14 @@ int gnb_generate(int32_t* x, int64_t n_rows, int32_t n_cols, int64_t ldx, int32_
   return GNB_OK;
 }
 
-int gnb_gather_features(const int32_t* x_vocab, int64_t n_rows, int32_t n_vocab, int64_t ldx,
-                        const int32_t* size_bytes, int32_t group_size_bytes,
-                        int32_t max_size_bytes, const int32_t* route, const int32_t* features,
-                        const int32_t* n_features, int32_t n_slots, int32_t max_features,
-                        int32_t* x_out, int64_t ldo, uintptr_t stream) {
+int gnb_gather_features_typed(const void* x_vocab, int32_t x_type, int64_t n_rows,
+                              int32_t n_vocab, int64_t ldx, const int32_t* size_bytes,
+                              int32_t group_size_bytes, int32_t max_size_bytes,
+                              const int32_t* route, const int32_t* features,
+                              const int32_t* n_features, int32_t n_slots, int32_t max_features,
+                              void* x_out, int64_t ldo, uintptr_t stream) {
+  if (x_type != GNB_X_I32 && x_type != GNB_X_U16 && x_type != GNB_X_U8)
+    return fail(GNB_EINVAL, "gather_features: unknown x_type %d", x_type);
   if (n_rows < 0 || n_vocab < 1 || ldx < n_vocab || max_features < 1 || ldo < max_features ||
       n_slots < 1 || group_size_bytes <= 0 || max_size_bytes <= 0 ||
       max_size_bytes % group_size_bytes)
@@ -530,11 +534,21 @@ int gnb_gather_features(const int32_t* x_vocab, int64_t n_rows, int32_t n_vocab,
   if (n_rows > 0 && (!x_vocab || !size_bytes || !x_out))
     return fail(GNB_EINVAL, "gather_features: null pointer");
   if (!route || !features || !n_features) return fail(GNB_EINVAL, "gather_features: null table");
-  GNB_CUDA(gather_launch(x_vocab, n_rows, n_vocab, ldx, size_bytes, group_size_bytes,
+  GNB_CUDA(gather_launch(x_vocab, x_type, n_rows, n_vocab, ldx, size_bytes, group_size_bytes,
                          max_size_bytes, route, features, n_features, max_features, x_out, ldo,
                          reinterpret_cast<cudaStream_t>(stream)),
            "gather launch");
   return GNB_OK;
+}
+
+int gnb_gather_features(const int32_t* x_vocab, int64_t n_rows, int32_t n_vocab, int64_t ldx,
+                        const int32_t* size_bytes, int32_t group_size_bytes,
+                        int32_t max_size_bytes, const int32_t* route, const int32_t* features,
+                        const int32_t* n_features, int32_t n_slots, int32_t max_features,
+                        int32_t* x_out, int64_t ldo, uintptr_t stream) {
+  return gnb_gather_features_typed(x_vocab, GNB_X_I32, n_rows, n_vocab, ldx, size_bytes,
+                                   group_size_bytes, max_size_bytes, route, features, n_features,
+                                   n_slots, max_features, x_out, ldo, stream);
 }
 
 }  // extern "C"
@@ -978,6 +992,154 @@ int gnb_fit_stats_host(const int32_t* x, int64_t n_rows, int32_t n_cols, int64_t
   if (sumsq) GNB_CUDA(cudaMemcpy(sumsq, dQ, stat_b, cudaMemcpyDeviceToHost), "D2H");
   GNB_CUDA(cudaMemcpy(counts, dN, size_t(keys) * 8, cudaMemcpyDeviceToHost), "D2H");
   if (status) GNB_CUDA(cudaMemcpy(status, dst, 16, cudaMemcpyDeviceToHost), "D2H");
+  return GNB_OK;
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------------ several GPUs, one call
+// The reference's classify_parallel cuts the batch into ceil(N / lanes)
+// contiguous chunks, one per worker (engine.py:264-268); here one host thread
+// per device runs the single-device pipeline above on its contiguous shard.
+// Predict has no exchange (rows are independent, the tables are replicated);
+// the fit's one exchange is the sum of the integer-valued statistics, exact in
+// any order (here on the host, since the host API returns host arrays).
+namespace {
+
+struct ShardErr {
+  int rc = GNB_OK;
+  char msg[512] = "";
+};
+
+int64_t shard_lo(int64_t n, int D, int d) {
+  const int64_t chunk = n ? (n + D - 1) / D : 0;
+  return std::min<int64_t>(chunk * d, n);
+}
+
+int join_shards(std::vector<std::thread>& th, std::vector<ShardErr>& err) {
+  for (auto& t : th) t.join();
+  for (auto& e : err)
+    if (e.rc) return fail(e.rc, "%s", e.msg);
+  return GNB_OK;
+}
+
+int check_devices(int32_t n_devices, const int32_t* devices) {
+  if (n_devices < 1 || n_devices > 64 || !devices)
+    return fail(GNB_EINVAL, "sharded: need 1..64 devices");
+  int count = 0;
+  GNB_CUDA(cudaGetDeviceCount(&count), "cudaGetDeviceCount");
+  for (int d = 0; d < n_devices; ++d)
+    if (devices[d] < 0 || devices[d] >= count)
+      return fail(GNB_EINVAL, "sharded: device %d not present (%d visible)", devices[d], count);
+  return GNB_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int gnb_predict_host_sharded(const void* x, int32_t x_type, int64_t n_rows, int32_t n_features,
+                             int64_t ldx, const int32_t* size_bytes, int32_t group_size_bytes,
+                             int32_t max_size_bytes, const int32_t* route, int32_t n_slots,
+                             int32_t n_classes, const double* log_prior, const double* log_lik,
+                             int32_t* label_out, double* logpost_out, int32_t n_devices,
+                             const int32_t* devices, int64_t* elapsed_ns) {
+  int rc = check_devices(n_devices, devices);
+  if (rc) return rc;
+  if (x_type != GNB_X_I32 && x_type != GNB_X_U16 && x_type != GNB_X_U8 && x_type != GNB_X_U4)
+    return fail(GNB_EINVAL, "predict_host_sharded: unknown x_type %d", x_type);
+  if (x_type == GNB_X_U4 && (ldx & 1))
+    return fail(GNB_EINVAL, "predict_host_sharded: GNB_X_U4 rows need an even ldx (features)");
+  // bytes per row of the caller's storage (U4: two features per byte)
+  const int64_t row_b = x_type == GNB_X_U4 ? ldx / 2 : ldx * elem_bytes(x_type);
+  std::vector<ShardErr> err(static_cast<size_t>(n_devices));
+  std::vector<int64_t> ns(size_t(n_devices), 0);
+  std::vector<std::thread> th;
+  for (int d = 0; d < n_devices; ++d) {
+    const int64_t lo = shard_lo(n_rows, n_devices, d), hi = shard_lo(n_rows, n_devices, d + 1);
+    th.emplace_back([=, &err, &ns] {
+      if (hi <= lo) return;
+      const uint8_t* xb = static_cast<const uint8_t*>(x) + lo * row_b;
+      const int r = predict_host_impl(xb, x_type, hi - lo, n_features, ldx, size_bytes + lo,
+                                      group_size_bytes, max_size_bytes, route, n_slots, n_classes,
+                                      log_prior, log_lik, label_out + lo,
+                                      logpost_out ? logpost_out + lo * n_classes : nullptr,
+                                      devices[d], &ns[size_t(d)]);
+      if (r) {
+        err[size_t(d)].rc = r;
+        snprintf(err[size_t(d)].msg, sizeof(err[size_t(d)].msg), "device %d: %s", devices[d],
+                 gnb_last_error());
+      }
+    });
+  }
+  if ((rc = join_shards(th, err))) return rc;
+  // the slowest device's pipeline time (each excludes its own buffer setup)
+  if (elapsed_ns) *elapsed_ns = *std::max_element(ns.begin(), ns.end());
+  return GNB_OK;
+}
+
+int gnb_fit_stats_host_sharded(const int32_t* x, int64_t n_rows, int32_t n_cols, int64_t ldx,
+                               const int32_t* size_bytes, const int32_t* labels,
+                               int32_t group_size_bytes, int32_t max_size_bytes,
+                               int32_t n_classes, double* sums, double* sumsq, double* counts,
+                               unsigned long long* status, int32_t n_devices,
+                               const int32_t* devices) {
+  int rc = check_devices(n_devices, devices);
+  if (rc) return rc;
+  if (n_rows < 0 || n_cols < 1 || ldx < n_cols)
+    return fail(GNB_EINVAL, "fit_stats_host_sharded: need n_rows>=0, n_cols>=1, ldx>=n_cols");
+  if (group_size_bytes <= 0 || max_size_bytes <= 0 || max_size_bytes % group_size_bytes)
+    return fail(GNB_EINVAL,
+                "fit_stats_host_sharded: need 0 < group_size_bytes dividing max_size_bytes");
+  if (!sums || !counts) return fail(GNB_EINVAL, "fit_stats_host_sharded: null output");
+  const int64_t keys = int64_t(max_size_bytes / group_size_bytes) * n_classes;
+  const size_t stat = size_t(keys) * n_cols;
+  std::vector<std::vector<double>> S(static_cast<size_t>(n_devices)), Q(static_cast<size_t>(n_devices)),
+      N(static_cast<size_t>(n_devices));
+  std::vector<std::array<unsigned long long, 2>> st(static_cast<size_t>(n_devices));
+  std::vector<ShardErr> err(static_cast<size_t>(n_devices));
+  std::vector<std::thread> th;
+  for (int d = 0; d < n_devices; ++d) {
+    const int64_t lo = shard_lo(n_rows, n_devices, d), hi = shard_lo(n_rows, n_devices, d + 1);
+    S[size_t(d)].assign(stat, 0.0);
+    if (sumsq) Q[size_t(d)].assign(stat, 0.0);
+    N[size_t(d)].assign(size_t(keys), 0.0);
+    st[size_t(d)] = {0ull, 0ull};
+    th.emplace_back([=, &S, &Q, &N, &st, &err] {
+      const int r = gnb_fit_stats_host(x + lo * ldx, hi - lo, n_cols, ldx, size_bytes + lo,
+                                       labels + lo, group_size_bytes, max_size_bytes, n_classes,
+                                       S[size_t(d)].data(), sumsq ? Q[size_t(d)].data() : nullptr,
+                                       N[size_t(d)].data(), st[size_t(d)].data(), devices[d]);
+      if (r) {
+        err[size_t(d)].rc = r;
+        snprintf(err[size_t(d)].msg, sizeof(err[size_t(d)].msg), "device %d: %s", devices[d],
+                 gnb_last_error());
+      }
+    });
+  }
+  if ((rc = join_shards(th, err))) return rc;
+  // the exchange: integer-valued doubles < 2^53 add exactly in any order
+  for (size_t i = 0; i < stat; ++i) {
+    double a = 0.0, q = 0.0;
+    for (int d = 0; d < n_devices; ++d) {
+      a += S[size_t(d)][i];
+      if (sumsq) q += Q[size_t(d)][i];
+    }
+    sums[i] = a;
+    if (sumsq) sumsq[i] = q;
+  }
+  for (size_t i = 0; i < size_t(keys); ++i) {
+    double a = 0.0;
+    for (int d = 0; d < n_devices; ++d) a += N[size_t(d)][i];
+    counts[i] = a;
+  }
+  if (status) {
+    status[0] = status[1] = 0;
+    for (int d = 0; d < n_devices; ++d) {
+      status[0] += st[size_t(d)][0];
+      status[1] += st[size_t(d)][1];
+    }
+  }
   return GNB_OK;
 }
 

@@ -38,11 +38,19 @@ extern "C" int gnb_fin_tables(const double* sums_g, const double* counts_g, int3
   if (n_tot == 0) return GNB_EINVAL;
   for (int c = 0; c < n_classes; ++c)
     log_prior[c] = std::log(static_cast<double>(as_count(counts_g[c])) / static_cast<double>(n_tot));
+  // total_c sums each DISTINCT feature once: the reference's per-class count
+  // dict is keyed by opcode (classifier.py:91-93, 116), while |F| counts a
+  // repeated opcode every time (n_features = len(features.opcodes), :112).
+  std::vector<char> seen(static_cast<size_t>(n_cols), 0);
+  for (int j = 0; j < n_features; ++j)
+    if (features[j] < 0 || features[j] >= n_cols) return GNB_EINVAL;
   for (int c = 0; c < n_classes; ++c) {
     const double* S = sums_g + static_cast<int64_t>(c) * n_cols;
     uint64_t total_c = 0;
+    std::fill(seen.begin(), seen.end(), 0);
     for (int j = 0; j < n_features; ++j) {
-      if (features[j] < 0 || features[j] >= n_cols) return GNB_EINVAL;
+      if (seen[static_cast<size_t>(features[j])]) continue;
+      seen[static_cast<size_t>(features[j])] = 1;
       total_c += as_count(S[features[j]]);
     }
     const double denom = static_cast<double>(total_c) + alpha * static_cast<double>(n_features);

@@ -12,41 +12,68 @@
 
 namespace gnb {
 
+// One warp per row (grid-stride over rows): lane j writes output columns j,
+// j+32, ... (coalesced stores); the reads are the row's routed feature
+// columns, gathered from a row that is one contiguous V-element span (L1/L2
+// sectors shared by the warp).  T: the caller's storage (int32 / uint16 /
+// uint8) in and out -- narrow rows stay narrow for K-PRED.
+template <typename T>
 __global__ void __launch_bounds__(256)
-    gather_kernel(const int32_t* __restrict__ x, int64_t n_rows, int32_t V, int64_t ldx,
+    gather_kernel(const T* __restrict__ x, int64_t n_rows, int32_t V, int64_t ldx,
                   const int32_t* __restrict__ size, int32_t width, int32_t limit,
                   const int32_t* __restrict__ route, const int32_t* __restrict__ features,
-                  const int32_t* __restrict__ n_features, int32_t F, int32_t* __restrict__ out,
+                  const int32_t* __restrict__ n_features, int32_t F, T* __restrict__ out,
                   int64_t ldo) {
-  const int64_t total = n_rows * F;
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t r = i / F;
-    const int j = static_cast<int>(i - r * F);
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+  for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x >> 5) + (threadIdx.x >> 5);
+       r < n_rows; r += warps) {
     const int sz = __ldg(size + r);
-    int v = 0;
-    if (sz >= 0 && sz < limit) {
-      const int s = __ldg(route + sz / width);
-      if (j < __ldg(n_features + s)) {
-        const int col = __ldg(features + static_cast<int64_t>(s) * F + j);
-        if (col >= 0 && col < V) v = __ldg(x + r * ldx + col);
+    const int s = (sz >= 0 && sz < limit) ? __ldg(route + sz / width) : -1;
+    const int nf = s >= 0 ? __ldg(n_features + s) : 0;
+    const T* row = x + r * ldx;
+    const int32_t* fs = features + static_cast<int64_t>(s < 0 ? 0 : s) * F;
+    for (int j = lane; j < F; j += 32) {
+      T v = 0;
+      if (j < nf) {
+        const int col = __ldg(fs + j);
+        if (col >= 0 && col < V) v = row[col];
       }
+      out[r * ldo + j] = v;
     }
-    out[r * ldo + j] = v;
   }
 }
 
-cudaError_t gather_launch(const int32_t* x, int64_t n_rows, int32_t V, int64_t ldx,
+template <typename T>
+static cudaError_t gather_launch_t(const void* x, int64_t n_rows, int32_t V, int64_t ldx,
+                                   const int32_t* size, int32_t width, int32_t limit,
+                                   const int32_t* route, const int32_t* features,
+                                   const int32_t* n_features, int32_t F, void* out, int64_t ldo,
+                                   cudaStream_t stream) {
+  const int64_t b = (n_rows + 7) / 8;  // 8 rows (warps) per block
+  gather_kernel<T><<<static_cast<int>(b < 148 * 16 ? b : 148 * 16), 256, 0, stream>>>(
+      static_cast<const T*>(x), n_rows, V, ldx, size, width, limit, route, features, n_features,
+      F, static_cast<T*>(out), ldo);
+  return cudaGetLastError();
+}
+
+cudaError_t gather_launch(const void* x, int x_type, int64_t n_rows, int32_t V, int64_t ldx,
                           const int32_t* size, int32_t width, int32_t limit,
                           const int32_t* route, const int32_t* features,
-                          const int32_t* n_features, int32_t F, int32_t* out, int64_t ldo,
+                          const int32_t* n_features, int32_t F, void* out, int64_t ldo,
                           cudaStream_t stream) {
-  const int64_t total = n_rows * F;
-  if (total == 0) return cudaSuccess;
-  const int64_t b = (total + 255) / 256;
-  gather_kernel<<<static_cast<int>(b < 148 * 32 ? b : 148 * 32), 256, 0, stream>>>(
-      x, n_rows, V, ldx, size, width, limit, route, features, n_features, F, out, ldo);
-  return cudaGetLastError();
+  if (n_rows == 0 || F == 0) return cudaSuccess;
+  switch (x_type) {
+    case GNB_X_U8:
+      return gather_launch_t<uint8_t>(x, n_rows, V, ldx, size, width, limit, route, features,
+                                      n_features, F, out, ldo, stream);
+    case GNB_X_U16:
+      return gather_launch_t<uint16_t>(x, n_rows, V, ldx, size, width, limit, route, features,
+                                       n_features, F, out, ldo, stream);
+    default:
+      return gather_launch_t<int32_t>(x, n_rows, V, ldx, size, width, limit, route, features,
+                                      n_features, F, out, ldo, stream);
+  }
 }
 
 // UNPACK-U4: one thread per 8 packed bytes (16 counts) -> one 16-B store.

@@ -101,10 +101,10 @@ struct GenParams {
 };
 cudaError_t generate_launch(const GenParams& p, cudaStream_t stream);
 
-cudaError_t gather_launch(const int32_t* x, int64_t n_rows, int32_t V, int64_t ldx,
+cudaError_t gather_launch(const void* x, int x_type, int64_t n_rows, int32_t V, int64_t ldx,
                           const int32_t* size, int32_t width, int32_t limit,
                           const int32_t* route, const int32_t* features,
-                          const int32_t* n_features, int32_t F, int32_t* out, int64_t ldo,
+                          const int32_t* n_features, int32_t F, void* out, int64_t ldo,
                           cudaStream_t stream);
 
 // Nibble-packed rows (GNB_X_U4, `packed_pitch` bytes per row, a multiple of 8)

@@ -92,6 +92,21 @@ __device__ __forceinline__ double converted(const uint4& v, int e) {
 }
 
 // ------------------------------------------------------------------ inner loops
+// Negative-count flag (int32 rows only).  The last 16-B quad of a row may run
+// past feature F into the row's pitch padding, which callers need not
+// initialise (and the 1-D bulk row-box copy moves raw): only the quad's first
+// (F - 4*(nq-1)) elements count towards the flag.
+struct QuadMask {
+  uint32_t y, z, w;
+};
+__device__ __forceinline__ QuadMask last_quad_mask(int nf) {
+  const int rem = nf - ((nf - 1) >> 2) * 4;  // valid int32 elements of the last quad, 1..4
+  return {rem > 1 ? ~0u : 0u, rem > 2 ? ~0u : 0u, rem > 3 ? ~0u : 0u};
+}
+__device__ __forceinline__ uint32_t quad_neg(const uint4& v, bool last, const QuadMask& m) {
+  return last ? (v.x | (v.y & m.y) | (v.z & m.z) | (v.w & m.w)) : (v.x | v.y | v.z | v.w);
+}
+
 struct GlobalTab {
   const double* p;
   __device__ __forceinline__ double get(int idx) const { return __ldg(p + idx); }
@@ -120,20 +135,21 @@ __device__ __forceinline__ void score_quad(double (&acc)[CP], const uint4 v, con
 
 template <int CP, typename T, typename Tab, bool FMA>
 __device__ __forceinline__ void score_chunk(double (&acc)[CP], const uint8_t* box, uint32_t row,
-                                            const Tab& tab, int nq, uint32_t& neg) {
+                                            const Tab& tab, int nq, uint32_t& neg,
+                                            const QuadMask& lm) {
   constexpr int EQ = Elem<T>::kPerQuad;
   if (nq == 8) {
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
       const uint4 v = *reinterpret_cast<const uint4*>(box + swz128(row, q));
-      if (Elem<T>::kSigned) neg |= v.x | v.y | v.z | v.w;
+      if (Elem<T>::kSigned) neg |= quad_neg(v, q == 7, lm);
       score_quad<CP, T, Tab, FMA>(acc, v, tab, EQ * q);
     }
   } else {
 #pragma unroll 1
     for (int q = 0; q < nq; ++q) {
       const uint4 v = *reinterpret_cast<const uint4*>(box + swz128(row, q));
-      if (Elem<T>::kSigned) neg |= v.x | v.y | v.z | v.w;
+      if (Elem<T>::kSigned) neg |= quad_neg(v, q == nq - 1, lm);
       score_quad<CP, T, Tab, FMA>(acc, v, tab, EQ * q);
     }
   }
@@ -213,14 +229,15 @@ __device__ __forceinline__ const double* chunk_table(const PredictParams& p, int
 template <int CP, typename T, int R, bool FMA>
 __device__ __forceinline__ void score_chunk_uniform(double (&acc)[R][CP], const uint8_t* box,
                                                     const uint32_t (&rows)[R], const double* tab,
-                                                    int nq, uint32_t (&neg)[R]) {
+                                                    int nq, uint32_t (&neg)[R],
+                                                    const QuadMask& lm) {
   constexpr int EQ = Elem<T>::kPerQuad;
   auto quad = [&](int q) {
     uint4 v[R];
 #pragma unroll
     for (int i = 0; i < R; ++i) {
       v[i] = *reinterpret_cast<const uint4*>(box + swz128(rows[i], q));
-      if (Elem<T>::kSigned) neg[i] |= v[i].x | v[i].y | v[i].z | v[i].w;
+      if (Elem<T>::kSigned) neg[i] |= quad_neg(v[i], q == nq - 1, lm);
     }
 #pragma unroll
     for (int e = 0; e < EQ; ++e) {
@@ -253,14 +270,14 @@ template <int CP, typename T, int R, bool FMA>
 __device__ __forceinline__ void score_chunk_mixed(const PredictParams& p, double (&acc)[R][CP],
                                                   const uint8_t* box, const uint32_t (&rows)[R],
                                                   const int (&slot)[R], int ch, int nq,
-                                                  uint32_t (&neg)[R]) {
+                                                  uint32_t (&neg)[R], const QuadMask& lm) {
 #pragma unroll
   for (int i = 0; i < R; ++i) {
     const GlobalTab tab{chunk_table<CP, T>(p, max(slot[i], 0), ch)};
     double a[CP];
 #pragma unroll
     for (int c = 0; c < CP; ++c) a[c] = acc[i][c];
-    score_chunk<CP, T, GlobalTab, FMA>(a, box, rows[i], tab, nq, neg[i]);
+    score_chunk<CP, T, GlobalTab, FMA>(a, box, rows[i], tab, nq, neg[i], lm);
 #pragma unroll
     for (int c = 0; c < CP; ++c) acc[i][c] = a[c];
   }
@@ -421,15 +438,16 @@ __global__ void __launch_bounds__((NW + 1) * 32)
           if (B > 1 && ch >= NCH) break;
           const int nf = min(CF, p.n_features - ch * CF);
           const int nq = (nf + EQ - 1) / EQ;
+          const QuadMask lm = last_quad_mask(nf);
           const uint8_t* box = smem + L::kX + stage * L::kXBytes + b * L::kBox;
           if (ts >= 0) {
             score_chunk_uniform<CP, T, R, FMA>(
                 acc, box, rows,
                 reinterpret_cast<const double*>(smem + L::kTab + stage * L::kTabBytes +
                                                 L::kPrior + b * L::kTabChunk),
-                nq, neg);
+                nq, neg, lm);
           } else {
-            score_chunk_mixed<CP, T, R, FMA>(p, acc, box, rows, slot, ch, nq, neg);
+            score_chunk_mixed<CP, T, R, FMA>(p, acc, box, rows, slot, ch, nq, neg, lm);
           }
         }
         __syncwarp();
@@ -506,12 +524,13 @@ __host__ __device__ inline int rowbox_tab_feats(int F, int EQ, int n_tab_blocks)
 // the nq quads of one row against one slot's smem table (prior excluded)
 template <int CP, typename T, bool FMA>
 __device__ __forceinline__ void rowbox_score_smem(double (&acc)[CP], const uint8_t* xrow,
-                                                  const double* tab, int nq, uint32_t& neg) {
+                                                  const double* tab, int nq, uint32_t& neg,
+                                                  const QuadMask& lm) {
   constexpr int EQ = Elem<T>::kPerQuad;
 #pragma unroll 2
   for (int q = 0; q < nq; ++q) {
     const uint4 v = *reinterpret_cast<const uint4*>(xrow + 16 * q);
-    if (Elem<T>::kSigned) neg |= v.x | v.y | v.z | v.w;
+    if (Elem<T>::kSigned) neg |= quad_neg(v, q == nq - 1, lm);
 #pragma unroll
     for (int e = 0; e < EQ; ++e) {
       const double xd = converted<T, FMA>(v, e);
@@ -660,6 +679,7 @@ __global__ void __launch_bounds__(5 * 32, MINB)
     // ---------------------------------------------------------- consumers
     const int row = lane + 32 * warp;
     const int nq = (p.n_features + EQ - 1) / EQ;
+    const QuadMask lm = last_quad_mask(p.n_features);
     const bool early = RQ > 0 && resident && nq <= RQ;
     const double* res = reinterpret_cast<const double*>(smem + L.res);
     int stage = 0;
@@ -691,7 +711,7 @@ __global__ void __launch_bounds__(5 * 32, MINB)
 #pragma unroll
           for (int q = 0; q < RQ; ++q) {
             if (q < nq) {
-              if (Elem<T>::kSigned) neg |= v[q].x | v[q].y | v[q].z | v[q].w;
+              if (Elem<T>::kSigned) neg |= quad_neg(v[q], q == nq - 1, lm);
 #pragma unroll
               for (int e = 0; e < EQ; ++e) {
                 const double xd = converted<T, FMA>(v[q], e);
@@ -712,7 +732,7 @@ __global__ void __launch_bounds__(5 * 32, MINB)
           const double* st = res + s * static_cast<int>(L.res_stride);
 #pragma unroll
           for (int c = 0; c < CP; ++c) acc[c] = st[c];
-          rowbox_score_smem<CP, T, FMA>(acc, xrow, st + CP, nq, neg);
+          rowbox_score_smem<CP, T, FMA>(acc, xrow, st + CP, nq, neg, lm);
         } else {
           const double* stab =
               reinterpret_cast<const double*>(smem + L.tab + stage * L.tab_bytes);
@@ -721,13 +741,13 @@ __global__ void __launch_bounds__(5 * 32, MINB)
 #pragma unroll
           for (int c = 0; c < CP; ++c) acc[c] = ts >= 0 ? stab[c] : __ldg(p.prior + s * CP + c);
           if (ts >= 0) {
-            rowbox_score_smem<CP, T, FMA>(acc, xrow, stab + CP, nq, neg);
+            rowbox_score_smem<CP, T, FMA>(acc, xrow, stab + CP, nq, neg, lm);
           } else {
             const GlobalTab tab{p.tab + s * slot_tab};
 #pragma unroll 1
             for (int q = 0; q < nq; ++q) {
               const uint4 v = *reinterpret_cast<const uint4*>(xrow + 16 * q);
-              if (Elem<T>::kSigned) neg |= v.x | v.y | v.z | v.w;
+              if (Elem<T>::kSigned) neg |= quad_neg(v, q == nq - 1, lm);
               score_quad<CP, T, GlobalTab, FMA>(acc, v, tab, EQ * q);
             }
           }

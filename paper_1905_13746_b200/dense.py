@@ -195,10 +195,11 @@ def pack_u4(x: torch.Tensor, out: torch.Tensor = None) -> torch.Tensor:
 
 def gather_features(x_vocab: torch.Tensor, size_bytes: torch.Tensor, tables: DeviceTables,
                     features, n_features, *, out=None, stream=None) -> torch.Tensor:
-    """[N, V] full-vocabulary counts -> [N, F] predict layout (routed FeatureSet order).
+    """[N, V] full-vocabulary counts -> [N, F] predict layout (routed FeatureSet order),
+    in x_vocab's storage (int32 / uint16 / uint8).
 
     features: [S, F] vocabulary column per (slot, feature); n_features: [S]."""
-    xp, n, V, ldx = _rows(x_vocab, "x_vocab")
+    xp, n, V, ldx = _rows(x_vocab, "x_vocab", dtypes=tuple(_X_TYPES))
     dev = x_vocab.device
     feats = torch.as_tensor(features, dtype=torch.int32).to(dev).contiguous()
     nf = torch.as_tensor(n_features, dtype=torch.int32).to(dev).contiguous()
@@ -206,15 +207,21 @@ def gather_features(x_vocab: torch.Tensor, size_bytes: torch.Tensor, tables: Dev
     if feats.shape != (tables.n_slots, F) or nf.shape != (tables.n_slots,):
         raise InvalidConfigError("features must be [n_slots, F] and n_features [n_slots]")
     if out is None:
-        ld = (F + 3) // 4 * 4
-        out = torch.empty((n, ld), dtype=torch.int32, device=dev)[:, :F]
-    op, _, Fo, ldo = _rows(out, "out")
+        eb = x_vocab.element_size()
+        ld = (F * eb + 15) // 16 * 16 // eb     # 16-B row pitch (TMA path of K-PRED)
+        full = torch.empty((n, ld), dtype=x_vocab.dtype, device=dev)
+        if ld > F:
+            full[:, F:].zero_()   # pitch padding: defined bytes for every consumer
+        out = full[:, :F]
+    if out.dtype != x_vocab.dtype:
+        raise InvalidConfigError("out must have x_vocab's dtype")
+    op, _, Fo, ldo = _rows(out, "out", dtypes=(x_vocab.dtype,))
     if Fo != F:
         raise InvalidConfigError("out must have F columns")
-    N.check(N.lib.gnb_gather_features(
-        xp, n, V, ldx, _vec(size_bytes, n, "size_bytes"), tables.group_size_bytes,
-        tables.max_size_bytes, tables.route.data_ptr(), feats.data_ptr(), nf.data_ptr(),
-        tables.n_slots, F, op, ldo, _stream(stream)), "gnb_gather_features")
+    N.check(N.lib.gnb_gather_features_typed(
+        xp, _X_TYPES[x_vocab.dtype], n, V, ldx, _vec(size_bytes, n, "size_bytes"),
+        tables.group_size_bytes, tables.max_size_bytes, tables.route.data_ptr(), feats.data_ptr(),
+        nf.data_ptr(), tables.n_slots, F, op, ldo, _stream(stream)), "gnb_gather_features_typed")
     return out
 
 
@@ -344,7 +351,10 @@ def generate(n_rows: int, n_cols: int, *, n_classes: int = 2, group_rows=None,
         ld = max(x.stride(0), x.shape[1])
     else:
         ld = ldx or (n_cols + 3) // 4 * 4
-        x = torch.empty((n_rows, ld), dtype=torch.int32, device=device)[:, :n_cols]
+        full = torch.empty((n_rows, ld), dtype=torch.int32, device=device)
+        if ld > n_cols:
+            full[:, n_cols:].zero_()   # pitch padding: defined bytes for every consumer
+        x = full[:, :n_cols]
         size = torch.empty(n_rows, dtype=torch.int32, device=device)
         lab = torch.empty(n_rows, dtype=torch.int32, device=device)
     cmap = None

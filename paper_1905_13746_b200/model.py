@@ -135,14 +135,19 @@ class GroupModel:
     log_likelihood: dict[Label, dict[str, float]]
     alpha: float
     train_counts: dict[Label, int]
+    # (opcode, ll_malware, ll_benign) rows in FeatureSet order: the summation
+    # order every scoring path follows (classifier.py:36-52)
+    _packed: tuple[tuple[str, float, float], ...] = field(init=False, repr=False, compare=False)
 
     def __post_init__(self):
-        for c in CLASSES:
-            row = self.log_likelihood.get(c, {})
-            missing = [op for op in self.features.opcodes if op not in row]
-            if missing:
-                raise IntegrityError(
-                    f"group {self.group}: log_likelihood missing feature {missing[0]!r}")
+        ll_m = self.log_likelihood.get(Label.MALWARE, {})
+        ll_b = self.log_likelihood.get(Label.BENIGN, {})
+        packed = []
+        for op in self.features.opcodes:
+            if op not in ll_m or op not in ll_b:
+                raise IntegrityError(f"group {self.group}: log_likelihood missing feature {op!r}")
+            packed.append((op, ll_m[op], ll_b[op]))
+        object.__setattr__(self, "_packed", tuple(packed))
 
 
 @dataclass(frozen=True)

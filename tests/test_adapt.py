@@ -50,6 +50,7 @@ def test_gather_routes_per_sample():
         if not 0 <= r.size_bytes < 60000:
             assert size[i] == -1 and not x[i].any()
             continue
+        assert size[i] == r.size_bytes // 10000         # the size group id
         cm = colmaps[route[r.size_bytes // 10000]]
         want = np.zeros(3, np.int32)
         for op, n in r.histogram.entries.items():
@@ -83,7 +84,7 @@ def test_gather_walks_either_dict():
             want = np.zeros(width, np.int32)
             for op, j in maps[r.size_bytes // 30000].items():
                 want[j] = r.histogram.entries.get(op, 0)
-            assert sz[i] == r.size_bytes and np.array_equal(x[i], want)
+            assert sz[i] == r.size_bytes // 30000 and np.array_equal(x[i], want)
 
 
 def test_predictions_match_python_construction():

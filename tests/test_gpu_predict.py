@@ -22,13 +22,13 @@ def _tables(rng, S, C, F, group_count):
     return prior, ll, route
 
 
-def _run(x, size, prior, ll, route, width, limit, *, generic=False, ldx=None):
+def _run(x, size, prior, ll, route, width, limit, *, generic=False, ldx=None, pad=0):
     dev = torch.device("cuda")
     N, F = x.shape
     if ldx is None or ldx == F:
         xd = torch.from_numpy(np.ascontiguousarray(x, dtype=np.int32)).to(dev)
     else:
-        base = torch.zeros((N, ldx), dtype=torch.int32, device=dev)
+        base = torch.full((N, ldx), pad, dtype=torch.int32, device=dev)
         base[:, :F] = torch.from_numpy(x.astype(np.int32)).to(dev)
         xd = base[:, :F]
     t = dense.DeviceTables.build(prior, ll, route, group_size_bytes=width, max_size_bytes=limit)
@@ -103,6 +103,21 @@ def test_rowbox_paths(F, ldx, S, C):
     _check(x, size, prior, ll, route, width, width * G, ldx=ldx)
     perm = rng.permutation(N)
     _check(x[perm], size[perm], prior, ll, route, width, width * G, ldx=ldx)
+
+
+@pytest.mark.parametrize("F,ldx", [(13, 16), (50, 52), (50, 56), (101, 104), (33, 36),
+                                   (250, 252), (255, 260)])
+def test_uninitialised_pitch_padding(F, ldx):
+    """Pitch padding columns [F, ldx) full of 0xFFFFFFFF (leftover memory with the
+    sign bit set) are neither scored nor flagged as negative counts, on every
+    K-PRED path (1-D bulk row box, 2-D row box, 128-B boxes, mixed tiles)."""
+    rng = np.random.default_rng(F * 7 + ldx)
+    prior, ll, route = _tables(rng, 3, 2, F, 4)
+    N = 3 * 128 + 41
+    size = np.sort(rng.integers(0, 400, size=N))
+    x = rng.poisson(2.0, size=(N, F))
+    for order in (np.arange(N), rng.permutation(N)):
+        _check(x[order], size[order], prior, ll, route, 100, 400, ldx=ldx, pad=-1)
 
 
 def test_ragged_groups_sorted_and_shuffled():

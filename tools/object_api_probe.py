@@ -50,13 +50,13 @@ def main():
     wl = gnb.Workload(tuple(samples), lanes=8)
     gnb.classify_parallel(bundle, wl)                       # buffers, context
     t = time.perf_counter()
-    packed = api._PackedBundle(bundle)
+    packed = api._PackedBundle(bundle, api._ns.of(bundle))
     out["pack_s"] = round(time.perf_counter() - t, 4)
     t = time.perf_counter()
     xg, sz = api._gather(samples, packed, cfg)
     out["adapt_gather_s"] = round(time.perf_counter() - t, 4)
     t = time.perf_counter()
-    lab, lp, el = api._predict_host(xg, sz, packed, cfg, 0)
+    lab, lp, el = api._predict_host(xg, sz, packed, cfg.group_count, [0])
     out["device_call_s"] = round(time.perf_counter() - t, 4)
     out["device_elapsed_s"] = round(el / 1e9, 4)
     t = time.perf_counter()
