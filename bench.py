@@ -45,7 +45,12 @@ def parse():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--rows", type=int, default=DEFAULT_ROWS, help="samples per GPU (weak scaling)")
+    ap.add_argument("--rows", type=int, default=DEFAULT_ROWS,
+                    help="cfg4 samples: the job total (strong scaling, default) or per GPU "
+                         "(--scaling weak)")
+    ap.add_argument("--scaling", choices=("strong", "weak"), default="strong",
+                    help="strong = BASELINE cfg4 (100M samples sharded over the GPUs); "
+                         "weak = --rows per GPU")
     ap.add_argument("--features", type=int, default=DEFAULT_F)
     ap.add_argument("--e2e-rows", type=int, default=8_000_000)
     ap.add_argument("--e2e-steps", type=int, default=3)
@@ -197,10 +202,30 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------- distributed plumbing
+def relaunch_if_needed(args):
+    """`python bench.py --gpus N` (N > 1) outside torchrun: re-exec this command
+    under torch.distributed.run with one rank per GPU, so the driver's plain
+    invocation and its torchrun invocation measure the same thing."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    sys.stdout.flush()
+    os.execv(sys.executable, cmd)
+
+
 def dist_init(args):
     import torch
     import torch.distributed as dist
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1 and not dist.is_initialized():
@@ -249,11 +274,17 @@ def run_ours(args, world, rank, local):
     from paper_1905_13746_b200 import dense
     from paper_1905_13746_b200.sharding import allreduce_stats
 
+    from paper_1905_13746_b200.sharding import shard_bounds
+
     dev = torch.device("cuda", torch.cuda.current_device())
-    n, V = args.rows, args.features
+    V = args.features
     width = 5120
-    offset = rank * n                      # contiguous shard of the global index space
-    group_rows = [world * n]
+    # contiguous shard of the global index space (engine.py:264-268 chunking):
+    # strong scaling = BASELINE cfg4, 100M samples over all GPUs
+    total = args.rows if args.scaling == "strong" else args.rows * world
+    offset, hi = shard_bounds(total, world, rank)
+    n = hi - offset
+    group_rows = [total]
 
     # ---- data + model (outside the timed region)
     x, size, lab = dense.generate(n, V, group_rows=group_rows, divergence=0.8, seed=0,
@@ -316,7 +347,7 @@ def run_ours(args, world, rank, local):
     total_ms = barrier_max(total_ms, world, dev)
     mean_launch_ms = barrier_max(sum(launch_ms) / len(launch_ms), world, dev)
     ms_per_step = total_ms / args.steps
-    value = world * n * args.steps / (total_ms / 1e3)
+    value = total * args.steps / (total_ms / 1e3)     # every rank's rows / slowest rank
 
     # ---- the same rows stored as uint8 (lossless here): 4x fewer bytes per sample
     narrow = None
@@ -338,14 +369,14 @@ def run_ours(args, world, rank, local):
         x8 = xg.to(torch.uint8)
         ms8 = timed(x8, "exact")
         bps8 = F + 4 + (4 + (16 if logpost is not None else 0))
-        narrow = {"x_dtype": "uint8", "value": round(world * n / (ms8 / 1e3), 1),
+        narrow = {"x_dtype": "uint8", "value": round(total / (ms8 / 1e3), 1),
                   "ms_per_step": round(ms8, 4), "bytes_per_sample": f"F+24 = {bps8}",
                   "achieved_gbs": round(n * bps8 / (ms8 / 1e3) / 1e9, 1),
                   "note": "same rows, counts < 256: K-PRED is FP64/I2F-bound, not HBM-bound"}
         # GNB_MODE_FMA (one rounding per term; not bit-exact, ~1e-12 relative):
         # halves the FP64 work where K-PRED is compute-bound
         ms8f = timed(x8, "fma")
-        narrow["fma_mode"] = {"value": round(world * n / (ms8f / 1e3), 1),
+        narrow["fma_mode"] = {"value": round(total / (ms8f / 1e3), 1),
                               "ms_per_step": round(ms8f, 4)}
         del x8
 
@@ -467,12 +498,15 @@ def run_ours(args, world, rank, local):
     return {
         "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": round(ms_per_step, 4),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (reference synth law, GEN kernel, seed 0); model fitted on it",
-        "config": {"workload": "cfg4: predict 100M samples x 256 features per GPU, 2 classes, "
-                               "1 size group" if (n == DEFAULT_ROWS and V == DEFAULT_F)
-                   else f"predict {n} samples x {V} features per GPU, 2 classes",
-                   "rows_per_gpu": n, "features": F, "classes": 2, "x_dtype": args.x_dtype,
+        "config": {"workload": ("cfg4: predict 100M samples x 256 features sharded over the "
+                                "GPUs, 2 classes, 1 size group")
+                   if (total == DEFAULT_ROWS and V == DEFAULT_F and args.scaling == "strong")
+                   else f"predict {total} samples x {V} features ({args.scaling} scaling), "
+                        "2 classes",
+                   "rows_total": total, "rows_per_gpu": n, "features": F, "classes": 2,
+                   "x_dtype": args.x_dtype,
                    "outputs": "label int32 + log-posterior fp64 x2" if logpost is not None
                    else "label int32", "parity": "bit-exact vs reference (exact mode)",
                    "l2": "inputs (%.1f GB/GPU) >> 126 MB L2; no flush needed" % (n * 4 * F / 1e9),
@@ -561,7 +595,7 @@ def run_reference(args, world, rank):
         "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(dt / args.steps * 1e3, 3), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "impl": "reference",
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "impl": "reference",
         "data": "synthetic (reference synth law, numpy)",
         "config": {"workload": "cfg4: predict 100M samples x 256 features per GPU, 2 classes, "
                                "1 size group (CPU: bounded sample per step)",
@@ -753,6 +787,7 @@ def run_sweep(args, world, rank, local):
     """cfg2: F = 50/100/200/500/1000 at 1M samples, 2 classes, 1 B200."""
     import numpy as np
     import torch
+    from oracle import oracle as O
     from paper_1905_13746_b200 import dense
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
@@ -779,10 +814,18 @@ def run_sweep(args, world, rank, local):
             lambda: dense.predict(x[:, :nf], size, t, label_out=label, logpost_out=lp),
             args.steps, max(args.warmup, 3))
         bps = 4 * nf + 24
+        # parity spot check of this launch: the C oracle on a strided subsample
+        idx = torch.arange(0, n, 97, device=dev)
+        want, wlp = O.c_predict(x[:, :nf][idx].cpu().numpy(), size[idx].cpu().numpy(),
+                                np.zeros(1, np.int32), fin.log_prior[:1],
+                                fin.log_lik[:1, :, :nf], width=5120, limit=5120, threads=8)
+        exact = bool(np.array_equal(label[idx].cpu().numpy(), want) and
+                     lp[idx].cpu().numpy().tobytes() == wlp.tobytes())
         rows.append({"F": nf, "ldx": int(x.stride(0)), "ms": round(mean_ms, 4),
                      "samples_per_s": round(n / (mean_ms / 1e3), 1),
                      "achieved_gbs": round(n * bps / (mean_ms / 1e3) / 1e9, 1),
-                     "frac": round(n * bps / (mean_ms / 1e3) / 1e9 / peak, 4)})
+                     "frac": round(n * bps / (mean_ms / 1e3) / 1e9 / peak, 4),
+                     "bit_exact_subsample_vs_oracle": exact})
         del x, size, lab, label, lp
     return {"metric": METRIC, "workload": "cfg2: F sweep at 1M samples, 2 classes, L2 flushed "
             "before every launch", "flush": FLUSH_MODE, "pitch": args.pitch, "unit": UNIT, "peak_gbs": peak, "peak_source": kind,
@@ -864,6 +907,7 @@ def run_fit(args, world, rank, local):
     """cfg5: fit statistics (S, Q, n) over 1B samples x 128 features, 16 classes,
     rows sharded over the ranks, generated in 100M-row chunks (512 GB total does
     not fit one GPU), fit kernel timed per chunk, one NCCL all-reduce at the end."""
+    import numpy as np
     import torch
     from paper_1905_13746_b200 import dense
     from paper_1905_13746_b200.sharding import allreduce_stats, shard_bounds
@@ -896,6 +940,19 @@ def run_fit(args, world, rank, local):
         b.record(s)
         b.synchronize()
         ms += a.elapsed_time(b)
+    # parity spot check on this workload's data: the first 1M rows of the last
+    # chunk fitted again and compared with the C oracle's exact integer counts
+    from oracle import oracle as O
+    m = min(1_000_000, n)
+    chk = dense.fit_stats(xs[:m], size[:m], lab[:m], n_classes=C, group_size_bytes=5120,
+                          max_size_bytes=5120)
+    So, Qo, no, bado, ooro = O.c_fit_stats(x[:m].cpu().numpy(), size[:m].cpu().numpy(),
+                                           lab[:m].cpu().numpy(), C, 5120, 5120)
+    exact = bool(np.array_equal(chk.sums.cpu().numpy(), So.astype(np.float64)) and
+                 np.array_equal(chk.sumsq.cpu().numpy(), Qo.astype(np.float64)) and
+                 np.array_equal(chk.counts.cpu().numpy(), no.astype(np.float64)) and
+                 chk.status.cpu().tolist() == [bado, ooro])
+    del chk
     if world > 1:
         torch.distributed.barrier()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -918,7 +975,7 @@ def run_fit(args, world, rank, local):
             "achieved_gbs_per_gpu": round(rows_here * bps / (ms / 1e3) / 1e9, 1),
             "frac": round(rows_here * bps / (ms / 1e3) / 1e9 / peak, 4), "peak_gbs": peak,
             "bytes_per_sample": f"{xs.element_size()}V+8", "x_dtype": args.x_dtype,
-            "rows_counted": n_total,
+            "rows_counted": n_total, "bit_exact_chunk_vs_oracle": exact,
             "stats_bytes_allreduced": int(st.packed().numel() * 8)}
 
 
@@ -953,6 +1010,14 @@ def run_fin(args, world, rank, local):
         h, d = host(), device()
         same = all(np.array_equal(getattr(h, f), getattr(d, f))
                    for f in ("state", "n_features", "features", "log_prior", "log_lik"))
+        # the oracle (pinned to the reference) on the first trained group
+        from oracle import oracle as O
+        g0 = int(np.nonzero(h.state == 1)[0][0])
+        feats, _ = O.select_features(S[g0].astype(np.int64), k, g0)
+        tt = O.train_tables(S[g0].astype(np.int64), cnt[g0].astype(np.int64), feats, 1.0, g0)
+        F0 = int(d.n_features[g0])
+        oracle_ok = (feats.tolist() == d.features[g0, :F0].tolist() and
+                     tt.log_lik.tobytes() == np.ascontiguousarray(d.log_lik[g0, :, :F0]).tobytes())
         th, td = [], []
         for _ in range(max(args.steps, 5)):
             t0 = time.perf_counter()
@@ -962,7 +1027,8 @@ def run_fin(args, world, rank, local):
             device()
             td.append(time.perf_counter() - t0)
         rows.append({"groups": G, "vocab": V, "k": k, "host_ms": round(statistics.median(th) * 1e3, 3),
-                     "device_ms": round(statistics.median(td) * 1e3, 3), "identical": same})
+                     "device_ms": round(statistics.median(td) * 1e3, 3), "identical": same,
+                     "bit_exact_group_vs_oracle": oracle_ok})
         del st
     return {"metric": "FIN wall time per call (feature scoring + top-k + log tables, all groups)",
             "workload": "fin: G groups x V vocabulary statistics from K-FIT on synthetic rows",
@@ -973,6 +1039,7 @@ def main():
     global FLUSH_MODE
     args = parse()
     FLUSH_MODE = args.flush
+    relaunch_if_needed(args)
     world, rank, local = dist_init(args)
     if args.impl == "reference":
         out = run_reference(args, world, rank)

@@ -138,7 +138,9 @@ def train_tables(S_g, n_g, features, alpha: float, group: int) -> GroupTables:
     ll = np.empty((C, F))
     for c in range(C):
         counts = [int(S_g[c, v]) for v in features]
-        denom = sum(counts) + alpha * F
+        # total_c over DISTINCT features (the reference's count dict is keyed
+        # by opcode, classifier.py:91-93, 116); |F| counts repeats (:112)
+        denom = sum(int(S_g[c, v]) for v in dict.fromkeys(int(f) for f in features)) + alpha * F
         for j, cnt in enumerate(counts):
             ll[c, j] = math.log((cnt + alpha) / denom)
     return GroupTables(group, np.asarray(features), log_prior, ll,

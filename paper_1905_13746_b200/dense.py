@@ -276,6 +276,46 @@ def fit_stats(x: torch.Tensor, size_bytes: torch.Tensor, labels: torch.Tensor, *
     return out
 
 
+# ---------------------------------------------------------------- several GPUs, one process
+def fit_stats_sharded(xs, sizes, labels, *, n_classes: int, group_size_bytes: int,
+                      max_size_bytes: int, sumsq: bool = True, comms=None) -> list[FitStats]:
+    """K-FIT on every device's row shard (xs[d] / sizes[d] / labels[d] resident on
+    device d, launched back to back so the devices run concurrently), then the
+    fit's one exchange: the library's NCCL communicator all-reduces the packed
+    statistics in place over NVLink (gnb_fit_allreduce).  Returns one FitStats
+    per device, all equal to a single-device fit of the concatenated rows."""
+    from .sharding import Comms
+    if not (len(xs) == len(sizes) == len(labels)) or not xs:
+        raise InvalidConfigError("need one x / sizes / labels shard per device")
+    devs = [x.device.index for x in xs]
+    if len(set(devs)) != len(devs):
+        raise InvalidConfigError("one shard per device (devices must differ)")
+    out = []
+    for x, sz, lb in zip(xs, sizes, labels):
+        with torch.cuda.device(x.device):
+            out.append(fit_stats(x, sz, lb, n_classes=n_classes,
+                                 group_size_bytes=group_size_bytes,
+                                 max_size_bytes=max_size_bytes, sumsq=sumsq))
+    if len(out) > 1:
+        (comms or Comms.local_cached(devs)).allreduce(out)
+    return out
+
+
+def predict_sharded(xs, sizes, tables, **kw):
+    """K-PRED on every device's shard with that device's replica of the tables
+    (tables[d], DeviceTables.build(..., device=d)); no exchange.  Returns
+    [(label, logpost)] per device, launched back to back (concurrent)."""
+    if not (len(xs) == len(sizes) == len(tables)) or not xs:
+        raise InvalidConfigError("need one x / sizes / tables per device")
+    out = []
+    for x, sz, t in zip(xs, sizes, tables):
+        if t.route.device != x.device:
+            raise InvalidConfigError("tables[d] must live on shard d's device")
+        with torch.cuda.device(x.device):
+            out.append(predict(x, sz, t, **kw))
+    return out
+
+
 # ---------------------------------------------------------------- finalize (host C++)
 @dataclass
 class FinResult:

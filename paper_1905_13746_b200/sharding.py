@@ -36,6 +36,54 @@ def allreduce_stats(stats, group=None):
     return stats.unpack_(flat)
 
 
+# ---------------------------------------------------------------- one process per GPU
+def fit_distributed(x, size_bytes, labels, *, n_classes: int, group_size_bytes: int,
+                    max_size_bytes: int, sumsq: bool = True, group=None, fit=None):
+    """This rank's row shard -> K-FIT -> the fit's one exchange (SUM all-reduce
+    of the packed statistics).  Every rank returns the statistics of ALL rows,
+    identical to a single-device fit of the concatenated shards.
+    `fit` (default dense.fit_stats) produces the local statistics."""
+    if fit is None:
+        from .dense import fit_stats as fit
+    st = fit(x, size_bytes, labels, n_classes=n_classes, group_size_bytes=group_size_bytes,
+             max_size_bytes=max_size_bytes, sumsq=sumsq)
+    return allreduce_stats(st, group=group)
+
+
+def train_distributed(x, size_bytes, labels, *, k: int, alpha: float, group_size_bytes: int,
+                      max_size_bytes: int, min_per_class: int, group=None, fit=None):
+    """fit_distributed (2 classes) + the host finalize (scores, top-k, libm
+    logs): every rank gets the same FinResult, bit-identical for any world size
+    (train_bundle's dense form, engine.py:157-177)."""
+    from .dense import fin_train
+    st = fit_distributed(x, size_bytes, labels, n_classes=2, group_size_bytes=group_size_bytes,
+                         max_size_bytes=max_size_bytes, sumsq=False, group=group, fit=fit)
+    return fin_train(st.sums.cpu().numpy(), st.counts.cpu().numpy(), k=k, alpha=alpha,
+                     min_per_class=min_per_class)
+
+
+def gather_rows(local, group=None):
+    """Concatenate every rank's rows of `local` (a tensor) in rank order -- the
+    sharded predict's optional output collection (predict itself needs no
+    collective).  Shards may differ in length (ceil chunking)."""
+    import torch
+    import torch.distributed as dist
+    if not dist.is_available() or not dist.is_initialized() or dist.get_world_size(group) == 1:
+        return local
+    world = dist.get_world_size(group)
+    dev = local.device if dist.get_backend(group) == "nccl" else torch.device("cpu")
+    n = torch.tensor([local.shape[0]], dtype=torch.int64, device=dev)
+    ns = [torch.zeros_like(n) for _ in range(world)]
+    dist.all_gather(ns, n, group=group)
+    ns = [int(v.item()) for v in ns]
+    m = max(ns)
+    buf = torch.zeros((m,) + tuple(local.shape[1:]), dtype=local.dtype, device=dev)
+    buf[:local.shape[0]] = local.to(dev)
+    parts = [torch.empty_like(buf) for _ in range(world)]
+    dist.all_gather(parts, buf, group=group)
+    return torch.cat([p[:c] for p, c in zip(parts, ns)]).to(local.device)
+
+
 class Comms:
     """The library's own NCCL communicator (gnb_comms_* in include/gnb.h), for
     callers without torch.distributed: one process driving several GPUs
@@ -99,6 +147,18 @@ class Comms:
         for s, f in zip(stats_per_device, flats):
             s.unpack_(f)
         return stats_per_device
+
+    _local_cache: dict = {}
+
+    @classmethod
+    def local_cached(cls, devices) -> "Comms":
+        """Comms.local for a device tuple, created once per process (ncclCommInitAll
+        costs far more than the all-reduce it serves)."""
+        key = tuple(int(d) for d in devices)
+        c = cls._local_cache.get(key)
+        if c is None:
+            c = cls._local_cache[key] = cls.local(list(key))
+        return c
 
     def close(self) -> None:
         h, self._h = self._h, None

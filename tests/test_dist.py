@@ -1,6 +1,8 @@
-"""N>1 host logic on CPU with gloo, world_size 2: sharded fit stats + one all-reduce
-give the single-process statistics and the identical bundle; sharded predict
-concatenates to the single-process result."""
+"""N>1 host logic on CPU with gloo, world_size 2, through the repo's own sharded
+drivers (sharding.fit_distributed / train_distributed / gather_rows): sharded fit
+stats + one all-reduce + host FIN give the single-process statistics and the
+identical model; sharded predict outputs gather to the single-process result.
+Only the per-rank kernels are stood in by the CPU oracle (no GPU here)."""
 
 import os
 import socket
@@ -23,41 +25,37 @@ def _free_port():
     return port
 
 
-class _CpuStats:
-    """FitStats stand-in holding CPU tensors (the GPU fit is tested on the GPU)."""
-
-    def __init__(self, S, Q, n):
-        self.sums, self.sumsq, self.counts = (torch.from_numpy(a.astype(np.float64))
-                                              for a in (S, Q, n))
-
-    def packed(self):
-        return torch.cat([self.sums.reshape(-1), self.sumsq.reshape(-1), self.counts.reshape(-1)])
-
-    def unpack_(self, flat):
-        o = 0
-        for t in (self.sums, self.sumsq, self.counts):
-            t.copy_(flat[o:o + t.numel()].view_as(t))
-            o += t.numel()
-        return self
+def _cpu_fit(x, size, label, *, n_classes, group_size_bytes, max_size_bytes, sumsq=True):
+    """The local statistics producer on CPU (K-FIT needs a GPU): the oracle's
+    counts, in the repo's own FitStats container."""
+    from paper_1905_13746_b200.dense import FitStats
+    S, Q, n, bad, oor = O.fit_stats(x, size, label, n_classes, group_size_bytes, max_size_bytes)
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64))  # noqa: E731
+    return FitStats(t(S), t(Q) if sumsq else None, t(n), torch.tensor([bad, oor]))
 
 
 def _worker(rank, world, port, out):
+    from paper_1905_13746_b200.sharding import fit_distributed, gather_rows, train_distributed
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     x, size, label = O.synth_dense(5003, 40, seed=1, divergence=0.3)
     lo, hi = shard_bounds(len(size), world, rank)
-    S, Q, n, _, _ = O.fit_stats(x[lo:hi], size[lo:hi], label[lo:hi], 2, 5120, 5120)
-    st = allreduce_stats(_CpuStats(S, Q, n))
-    feats, _ = O.select_features(st.sums.numpy()[0].astype(np.int64), 30, 0)
-    t = O.train_tables(st.sums.numpy()[0].astype(np.int64), st.counts.numpy()[0].astype(np.int64),
-                       feats, 1.0, 0)
+    # the repo's sharded drivers: local stats -> the one all-reduce (-> host FIN)
+    st = fit_distributed(x[lo:hi], size[lo:hi], label[lo:hi], n_classes=2,
+                         group_size_bytes=5120, max_size_bytes=5120, fit=_cpu_fit)
+    fin = train_distributed(x[lo:hi], size[lo:hi], label[lo:hi], k=30, alpha=1.0,
+                            group_size_bytes=5120, max_size_bytes=5120, min_per_class=6,
+                            fit=_cpu_fit)
+    F = int(fin.n_features[0])
+    feats = fin.features[0, :F]
     lab, lp = O.predict_dense(x[lo:hi][:, feats], size[lo:hi], np.zeros(1, np.int32),
-                              t.log_prior[None], t.log_lik[None], width=5120, limit=5120)
-    gl = [None] * world
-    dist.all_gather_object(gl, (lab.tolist(), lp.tobytes()))
+                              fin.log_prior[:1], fin.log_lik[:1, :, :F], width=5120, limit=5120)
+    all_lab = gather_rows(torch.from_numpy(lab.astype(np.int32)))
+    all_lp = gather_rows(torch.from_numpy(np.ascontiguousarray(lp)))
     if rank == 0:
         out.put((st.sums.numpy().tobytes(), st.sumsq.numpy().tobytes(), st.counts.numpy().tobytes(),
-                 feats.tolist(), t.log_lik.tobytes(), gl))
+                 feats.tolist(), fin.log_lik[0, :, :F].tobytes(), all_lab.numpy().tolist(),
+                 all_lp.numpy().tobytes()))
     dist.destroy_process_group()
 
 
@@ -81,7 +79,7 @@ def test_gloo_world2_fit_allreduce_and_predict():
     for p in procs:
         p.join(60)
         assert p.exitcode == 0
-    S2, Q2, n2, feats2, ll2, parts = res
+    S2, Q2, n2, feats2, ll2, all_lab, all_lp = res
     x, size, label = O.synth_dense(5003, 40, seed=1, divergence=0.3)
     S, Q, n, _, _ = O.fit_stats(x, size, label, 2, 5120, 5120)
     assert S.astype(np.float64).tobytes() == S2
@@ -92,5 +90,5 @@ def test_gloo_world2_fit_allreduce_and_predict():
     assert feats.tolist() == feats2 and t.log_lik.tobytes() == ll2
     lab, lp = O.predict_dense(x[:, feats], size, np.zeros(1, np.int32), t.log_prior[None],
                               t.log_lik[None], width=5120, limit=5120)
-    assert sum((p[0] for p in parts), []) == lab.tolist()
-    assert b"".join(p[1] for p in parts) == lp.tobytes()
+    assert all_lab == lab.tolist()
+    assert all_lp == lp.tobytes()

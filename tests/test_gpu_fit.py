@@ -125,7 +125,8 @@ def test_narrow_storage_fit(dtype, hi, V, C):
 @pytest.mark.parametrize("V,G,k", [(1, 1, 1), (40, 3, 15), (256, 1, 100), (1000, 32, 200),
                                    (5000, 4, 300), (16384, 2, 64)])
 def test_device_fin_matches_host_fin(V, G, k):
-    """Device scoring + top-k (bitonic sort) == host FIN (itself pinned to the reference)."""
+    """Device scoring + top-k (bitonic sort) == host FIN == the oracle's
+    select_features / train_tables (pinned to the reference) at every V."""
     rng = np.random.default_rng(V + G)
     S = rng.integers(0, 50, size=(G, 2, V)) * (rng.random((G, 2, V)) < 0.7)
     half = V // 2
@@ -146,6 +147,21 @@ def test_device_fin_matches_host_fin(V, G, k):
         assert dev.features[g, :F].tolist() == host.features[g, :F].tolist()
     assert dev.log_prior.tobytes() == host.log_prior.tobytes()
     assert dev.log_lik.tobytes() == host.log_lik.tobytes()
+    # the oracle: (benign, malware) class order, exact integer sums
+    for g in range(G):
+        if host.state[g] == 0:
+            assert O.trainable(n[g:g + 1].astype(np.int64), 3) == []
+            continue
+        if host.state[g] < 0:
+            with pytest.raises(O.OracleError):
+                O.select_features(S[g].astype(np.int64), k, g)
+            continue
+        feats, _ = O.select_features(S[g].astype(np.int64), k, g)
+        F = int(host.n_features[g])
+        assert feats.tolist() == dev.features[g, :F].tolist()
+        t = O.train_tables(S[g].astype(np.int64), n[g].astype(np.int64), feats, 1.0, g)
+        assert t.log_prior.tobytes() == dev.log_prior[g].tobytes()
+        assert t.log_lik.tobytes() == np.ascontiguousarray(dev.log_lik[g, :, :F]).tobytes()
 
 
 def test_library_comms_allreduce_single_device():
