@@ -8,6 +8,8 @@
 //        tools/gather_probe.cu -o tools/gather_probe
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
+#include <cmath>
 #include <cstdint>
 #include <vector>
 #include <algorithm>
