@@ -5,7 +5,7 @@ NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -O3
 PKG := paper_1905_13746_b200
 CU := predict predict_i32_exact predict_i32_fma predict_u16_exact predict_u16_fma \
       predict_u8_exact predict_u8_fma fit gen gather sort fin_select api
-CXX_SRC := fin ingest comms
+CXX_SRC := fin ingest comms narrow
 OBJDIR := $(PKG)/csrc/build
 OBJ := $(CU:%=$(OBJDIR)/%.o) $(CXX_SRC:%=$(OBJDIR)/%.o)
 HDR := $(wildcard $(PKG)/csrc/*.h $(PKG)/csrc/*.cuh) include/gnb.h

@@ -664,43 +664,51 @@ int get_ctx(int device, HostCtx** out) {
     GNB_CUDA(cudaEventCreateWithFlags(&c->ev[i], cudaEventDisableTiming), "event create");
     GNB_CUDA(cudaEventCreateWithFlags(&c->copied[i], cudaEventDisableTiming), "event create");
   }
-  const unsigned hw = std::thread::hardware_concurrency();
-  c->pool = new Pool(static_cast<int>(hw > 0 ? std::min(hw, 64u) : 4u));
   g_ctx.push_back(c);
   *out = c;
   return GNB_OK;
 }
 
-// Narrow rows [0, n) of an int32 matrix into `dst` as uint8 (ld = dld) if every
-// count is < 256, else uint16 if < 65536; returns the x_type written, or
-// GNB_X_I32 when neither fits (negative or large counts): the caller then
-// ships the int32 rows unchanged.  Lossless by construction.
-template <typename U>
-bool narrow_rows(Pool& pool, const int32_t* src, int64_t n, int32_t F, int64_t ldx, U* dst,
-                 int64_t dld) {
+// Host-side narrowing of int32 rows (lossless, chosen per pipeline chunk):
+// the narrowest storage that holds every count of the chunk -- GNB_X_U4 (two
+// counts per byte, < 16), GNB_X_U8, GNB_X_U16 -- written into pinned staging
+// in one pass over the int32 rows per attempted width (each worker stops its
+// attempt at the first 16-row block that does not fit).  int32 rows cost
+// 1024 B/row of host DRAM reads either way (the C port's cost too); what the
+// narrowing buys is 2-8x fewer bytes over PCIe, so e2e on int32 host buffers
+// is bound by host memory bandwidth instead of the ~55 GB/s link.
+// Returns the x_type written, or GNB_X_I32 when no narrow width holds the
+// chunk (negative or >= 65536 counts): the caller then ships int32 rows.
+template <int BITS>
+bool narrow_chunk_at(Pool& pool, const int32_t* src, int64_t n, int32_t F, int64_t ldx,
+                     uint8_t* dst, int64_t dpitch) {
   std::atomic<uint32_t> bad{0};
   const int W = pool.size();
   pool.run([&](int w) {
     const int64_t lo = n * w / W, hi = n * (w + 1) / W;
-    uint32_t acc = 0;
-    for (int64_t r = lo; r < hi; ++r) {
-      const int32_t* s = src + r * ldx;
-      U* d = dst + r * dld;
-      for (int32_t j = 0; j < F; ++j) {
-        const uint32_t v = static_cast<uint32_t>(s[j]);
-        acc |= v;
-        d[j] = static_cast<U>(v);
+    for (int64_t r = lo; r < hi; r += 16) {
+      if (bad.load(std::memory_order_relaxed)) return;
+      if (!narrow_rows_block(BITS, src, F, ldx, dst, dpitch, r, std::min<int64_t>(r + 16, hi))) {
+        bad.store(1u, std::memory_order_relaxed);
+        return;
       }
-      if (acc >> (8 * sizeof(U))) break;
     }
-    if (acc >> (8 * sizeof(U))) bad.fetch_or(1u);
   });
   return bad.load() == 0;
 }
 
-bool narrowing_enabled() {
+int narrow_chunk(Pool& pool, const int32_t* src, int64_t n, int32_t F, int64_t ldx,
+                 uint8_t* dst, int64_t ld8, int64_t ld16) {
+  if (narrow_chunk_at<4>(pool, src, n, F, ldx, dst, ld8 / 2)) return GNB_X_U4;
+  if (narrow_chunk_at<8>(pool, src, n, F, ldx, dst, ld8)) return GNB_X_U8;
+  if (narrow_chunk_at<16>(pool, src, n, F, ldx, dst, ld16 * 2)) return GNB_X_U16;
+  return GNB_X_I32;
+}
+
+// GNB_HOST_NARROW=0 ships int32 host rows as they are (A/B); default on.
+bool narrowing_enabled() {  // read per call (once per host pipeline call)
   const char* e = getenv("GNB_HOST_NARROW");
-  return e != nullptr && atoi(e) != 0;
+  return e == nullptr || atoi(e) != 0;
 }
 
 // MiB of X crossing PCIe per pipeline chunk (GNB_HOST_CHUNK_MB, read once).
@@ -758,11 +766,9 @@ static int predict_host_impl(const void* xv, int x_type, int64_t n_rows, int32_t
   GNB_CUDA(cudaEventRecord(c->ev[0], s0), "event");
   for (int i = 1; i < kLanes; ++i) GNB_CUDA(cudaStreamWaitEvent(c->s[i], c->ev[0], 0), "wait");
 
-  // Rows cross PCIe in the caller's storage (int32 / uint16 / uint8).  For
-  // int32 input, GNB_HOST_NARROW=1 makes host threads narrow each chunk into
-  // pinned staging first (lossless; chunks that do not fit stay int32) -- a
-  // win only when host DRAM bandwidth well exceeds PCIe (off by default:
-  // measured slower on the B200 box, profiles/r01_tuning.md).
+  // Rows cross PCIe in the caller's storage (uint16 / uint8 / nibbles); int32
+  // input is narrowed per chunk by host threads into pinned staging first
+  // (narrow_chunk: lossless, chunks that fit no narrow width stay int32).
   const int64_t ld = (n_features + 3) / 4 * 4;  // device rows padded for TMA (int32)
   const int64_t ld8 = (n_features + 15) / 16 * 16, ld16 = (n_features + 7) / 8 * 8;
   // chunk rows from the bytes each row moves over PCIe; device rows as stored
@@ -772,10 +778,14 @@ static int predict_host_impl(const void* xv, int x_type, int64_t n_rows, int32_t
                         : x_type == GNB_X_U16 ? ld16 * 2 : ld * 4;
   const int64_t rows = std::min<int64_t>(chunk_rows_for(wire_b), std::max<int64_t>(n_rows, 1));
   const bool narrow = x_type == GNB_X_I32 && narrowing_enabled();
+  if (narrow && c->pool == nullptr) {
+    const unsigned hw = std::thread::hardware_concurrency();
+    c->pool = new Pool(static_cast<int>(hw > 0 ? std::min(hw, 64u) : 4u));
+  }
   for (int i = 0; i < kLanes; ++i) {
     GNB_CUDA(c->x[i].ensure(size_t(rows) * dev_b), "malloc");
     if (narrow) GNB_CUDA(c->stage[i].ensure(size_t(rows) * ld16 * 2), "cudaHostAlloc");
-    if (x_type == GNB_X_U4) GNB_CUDA(c->x4[i].ensure(size_t(rows) * ld8 / 2), "malloc");
+    if (x_type == GNB_X_U4 || narrow) GNB_CUDA(c->x4[i].ensure(size_t(rows) * ld8 / 2), "malloc");
     GNB_CUDA(c->size[i].ensure(size_t(rows) * 4), "malloc");
     GNB_CUDA(c->label[i].ensure(size_t(rows) * 4), "malloc");
     if (logpost_out) GNB_CUDA(c->logpost[i].ensure(size_t(rows) * n_classes * 8), "malloc");
@@ -819,22 +829,25 @@ static int predict_host_impl(const void* xv, int x_type, int64_t n_rows, int32_t
                  "H2D 2D");
     } else if (narrow) {
       GNB_CUDA(cudaEventSynchronize(c->copied[lane]), "event sync");  // staging free again
-      const int32_t* src = x + r0 * ldx;
-      if (narrow_rows(*c->pool, src, n, n_features, ldx,
-                      static_cast<uint8_t*>(c->stage[lane].p), ld8)) {
+      const int nt = narrow_chunk(*c->pool, x + r0 * ldx, n, n_features, ldx,
+                                  static_cast<uint8_t*>(c->stage[lane].p), ld8, ld16);
+      if (nt == GNB_X_U4) {  // nibbles over PCIe, unpacked to uint8 rows on the device
+        GNB_CUDA(cudaMemcpyAsync(c->x4[lane].p, c->stage[lane].p, size_t(n) * (ld8 / 2),
+                                 cudaMemcpyHostToDevice, s),
+                 "H2D");
+        GNB_CUDA(unpack_u4_launch(static_cast<const uint8_t*>(c->x4[lane].p), n, ld8 / 2,
+                                  static_cast<uint8_t*>(dx), s),
+                 "unpack_u4");
         xt = GNB_X_U8;
         dld = ld8;
-      } else if (narrow_rows(*c->pool, src, n, n_features, ldx,
-                             static_cast<uint16_t*>(c->stage[lane].p), ld16)) {
-        xt = GNB_X_U16;
-        dld = ld16;
-      }
-      if (xt != GNB_X_I32) {
+      } else if (nt != GNB_X_I32) {
+        xt = nt;
+        dld = nt == GNB_X_U8 ? ld8 : ld16;
         GNB_CUDA(cudaMemcpyAsync(dx, c->stage[lane].p, size_t(n) * dld * elem_bytes(xt),
                                  cudaMemcpyHostToDevice, s),
                  "H2D");
-        GNB_CUDA(cudaEventRecord(c->copied[lane], s), "event");
       }
+      GNB_CUDA(cudaEventRecord(c->copied[lane], s), "event");
     }
     if (xt == GNB_X_I32) {
       if (ldx == ld) {

@@ -10,6 +10,11 @@
 
 namespace gnb {
 
+// Host narrowing of int32 rows [r0, r1) to BITS = 4 / 8 / 16 bits per count
+// (narrow.cpp); false when some count does not fit.
+bool narrow_rows_block(int bits, const int32_t* s, int32_t F, int64_t ldx, uint8_t* d,
+                       int64_t dpitch, int64_t r0, int64_t r1);
+
 // Records `msg` for gnb_last_error() (thread-local) and returns `code`.
 int set_error(int code, const char* msg);
 

@@ -264,21 +264,23 @@ def test_narrowest_roundtrip():
 
 
 @pytest.mark.parametrize("narrow", ["0", "1"])
-@pytest.mark.parametrize("hi,neg", [(256, False), (60000, False), (2**31 - 1, False), (100, True)])
-def test_host_entry_narrowing_paths(hi, neg, narrow, monkeypatch):
-    """gnb_predict_host (GNB_HOST_NARROW=1: chunks shipped as uint8 / uint16 / int32 by
-    content) gives identical results."""
+@pytest.mark.parametrize("hi,neg", [(16, False), (256, False), (60000, False), (2**31 - 1, False),
+                                    (100, True), (16, True)])
+@pytest.mark.parametrize("F", [45, 64])
+def test_host_entry_narrowing_paths(hi, neg, narrow, F, monkeypatch):
+    """gnb_predict_host (default GNB_HOST_NARROW=1: int32 chunks shipped as nibbles /
+    uint8 / uint16 / int32 by content) gives identical results."""
     import ctypes
     from paper_1905_13746_b200 import _native as N
     monkeypatch.setenv("GNB_HOST_NARROW", narrow)
     rng = np.random.default_rng(hi % 1000)
-    S, C, F, G = 2, 2, 45, 3
+    S, C, G = 2, 2, 3
     prior, ll, route = _tables(rng, S, C, F, G)
     n = 70_000
     x = rng.integers(0, hi, size=(n, F)).astype(np.int32)
     if neg:
         x[123, 7] = -5
-    ldx = 48                                  # padded host rows: exercises the pitch paths
+    ldx = F + 3                               # padded host rows: exercises the pitch paths
     xh = np.zeros((n, ldx), np.int32)
     xh[:, :F] = x
     size = rng.integers(-3, G * 100, size=n).astype(np.int32)
