@@ -494,8 +494,10 @@ def run_ours(args, world, rank, local):
                 e2e[name] = {k: v for k, v in e2e_run(dt_, nar).items()
                              if k in ("value", "h2d_bytes_per_step")}
         del sh, lh, ph
-        # the e2e roofline: host->device bytes per second of this run against a
-        # plain pinned 1 GiB torch copy on the same link (the PCIe ceiling)
+        # the e2e rooflines: int32 host rows are read once by the host threads
+        # that narrow them (host DRAM read bound); the narrowed rows then cross
+        # PCIe (against a plain pinned 1 GiB torch copy on the same link)
+        e2e["host_read"] = host_read_roofline(e2e, F)
         e2e["pcie"] = pcie_roofline(e2e, dev)
 
     # ---- CPU baseline: C oracle on the box's host cores (rank 0, N=1 only)
@@ -623,6 +625,29 @@ def run_reference(args, world, rank):
                 "d2h_bytes_per_step": 0},
         "reference_python": ref_py,
     }
+
+
+def host_read_roofline(e2e, F):
+    """Achieved host DRAM read GB/s of the int32 e2e rows vs this host's own
+    all-core streaming narrow (torch int32 -> uint8 copy of 2 GiB)."""
+    import torch
+    n = (2 << 30) // (4 * F)
+    src = torch.ones((n, F), dtype=torch.int32)
+    dst = torch.empty((n, F), dtype=torch.uint8)
+    threads = torch.get_num_threads()
+    torch.set_num_threads(os.cpu_count() or 1)
+    dst.copy_(src)
+    t = time.perf_counter()
+    for _ in range(3):
+        dst.copy_(src)
+    peak = 3 * n * F * 4 / (time.perf_counter() - t) / 1e9
+    torch.set_num_threads(threads)
+    rows_per_s = e2e["value"] / max(int(os.environ.get("WORLD_SIZE", "1")), 1)
+    achieved = rows_per_s * e2e["host_x_bytes_per_step"] / e2e["rows_per_step_per_gpu"] / 1e9
+    del src, dst
+    return {"bound": "host_dram_read", "achieved_gbs": round(achieved, 1),
+            "peak_gbs": round(peak, 1), "frac": round(achieved / peak, 3),
+            "peak_source": "torch int32->uint8 copy, all host cores, 2 GiB"}
 
 
 def pcie_roofline(e2e, dev):

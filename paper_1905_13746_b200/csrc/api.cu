@@ -600,11 +600,20 @@ class Pool {
   }
   int size() const { return n_; }
   void run(const std::function<void(int)>& f) {  // f(worker), blocks until all finish
-    std::unique_lock<std::mutex> g(m_);
+    start(f);
+    wait();
+  }
+  // start(f): every worker runs f(worker) while the caller goes on; wait()
+  // blocks until they all finished.  f must outlive the wait().
+  void start(const std::function<void(int)>& f) {
+    std::lock_guard<std::mutex> g(m_);
     job_ = &f;
     pending_ = n_;
     ++gen_;
     cv_.notify_all();
+  }
+  void wait() {
+    std::unique_lock<std::mutex> g(m_);
     done_.wait(g, [this] { return pending_ == 0; });
     job_ = nullptr;
   }
@@ -679,31 +688,48 @@ int get_ctx(int device, HostCtx** out) {
 // is bound by host memory bandwidth instead of the ~55 GB/s link.
 // Returns the x_type written, or GNB_X_I32 when no narrow width holds the
 // chunk (negative or >= 65536 counts): the caller then ships int32 rows.
-template <int BITS>
-bool narrow_chunk_at(Pool& pool, const int32_t* src, int64_t n, int32_t F, int64_t ldx,
-                     uint8_t* dst, int64_t dpitch) {
+// One chunk's narrowing, run by the pool in the background while the calling
+// thread issues the previous chunk's copies and kernels: the 4-bit attempt is
+// started asynchronously (start); finish() waits for it and, only if some count
+// did not fit, retries 8 / 16 bits synchronously.
+struct NarrowJob {
+  const int32_t* src = nullptr;
+  int64_t n = 0, ldx = 0, ld8 = 0, ld16 = 0;
+  int32_t F = 0;
+  uint8_t* dst = nullptr;
+  int bits = 4;
   std::atomic<uint32_t> bad{0};
-  const int W = pool.size();
-  pool.run([&](int w) {
-    const int64_t lo = n * w / W, hi = n * (w + 1) / W;
-    for (int64_t r = lo; r < hi; r += 16) {
-      if (bad.load(std::memory_order_relaxed)) return;
-      if (!narrow_rows_block(BITS, src, F, ldx, dst, dpitch, r, std::min<int64_t>(r + 16, hi))) {
-        bad.store(1u, std::memory_order_relaxed);
-        return;
-      }
-    }
-  });
-  return bad.load() == 0;
-}
+  std::function<void(int)> fn;
+  int W = 1;
 
-int narrow_chunk(Pool& pool, const int32_t* src, int64_t n, int32_t F, int64_t ldx,
-                 uint8_t* dst, int64_t ld8, int64_t ld16) {
-  if (narrow_chunk_at<4>(pool, src, n, F, ldx, dst, ld8 / 2)) return GNB_X_U4;
-  if (narrow_chunk_at<8>(pool, src, n, F, ldx, dst, ld8)) return GNB_X_U8;
-  if (narrow_chunk_at<16>(pool, src, n, F, ldx, dst, ld16 * 2)) return GNB_X_U16;
-  return GNB_X_I32;
-}
+  void attempt(Pool& pool, int b, bool async) {
+    bits = b;
+    bad.store(0u);
+    W = pool.size();
+    const int64_t pitch = b == 4 ? ld8 / 2 : b == 8 ? ld8 : ld16 * 2;
+    fn = [this, pitch](int w) {
+      const int64_t lo = n * w / W, hi = n * (w + 1) / W;
+      for (int64_t r = lo; r < hi; r += 64) {
+        if (bad.load(std::memory_order_relaxed)) return;
+        if (!narrow_rows_block(bits, src, F, ldx, dst, pitch, r, std::min<int64_t>(r + 64, hi))) {
+          bad.store(1u, std::memory_order_relaxed);
+          return;
+        }
+      }
+    };
+    if (async) pool.start(fn);
+    else pool.run(fn);
+  }
+  // the x_type written: GNB_X_U4 / U8 / U16, or GNB_X_I32 (nothing fits)
+  int finish(Pool& pool) {
+    pool.wait();
+    if (bits == 4 && bad.load() == 0) return GNB_X_U4;
+    attempt(pool, 8, false);
+    if (bad.load() == 0) return GNB_X_U8;
+    attempt(pool, 16, false);
+    return bad.load() == 0 ? GNB_X_U16 : GNB_X_I32;
+  }
+};
 
 // GNB_HOST_NARROW=0 ships int32 host rows as they are (A/B); default on.
 bool narrowing_enabled() {  // read per call (once per host pipeline call)
@@ -794,6 +820,33 @@ static int predict_host_impl(const void* xv, int x_type, int64_t n_rows, int32_t
   // builds its worker pool before its timer, engine.py:273-285): a first call
   // -- or one larger than any before -- allocates device buffers here.
   if (elapsed_ns) t0 = std::chrono::steady_clock::now();
+  // GNB_HOST_TIMING=1: per-call breakdown of the host side on stderr (profiling)
+  const char* te = getenv("GNB_HOST_TIMING");
+  const bool timing = te != nullptr && atoi(te) != 0;
+  double t_wait = 0.0, t_narrow = 0.0;
+  NarrowJob jobs[2];
+  // an error return must not leave pool workers writing through `jobs`
+  struct PoolDrain {
+    Pool* p;
+    ~PoolDrain() {
+      if (p) p->wait();
+    }
+  } drain{narrow ? c->pool : nullptr};
+  auto start_narrow = [&](int64_t k, int lane_k) {
+    NarrowJob& j = jobs[k & 1];
+    j.src = x + k * rows * ldx;
+    j.n = std::min(rows, n_rows - k * rows);
+    j.F = n_features;
+    j.ldx = ldx;
+    j.ld8 = ld8;
+    j.ld16 = ld16;
+    j.dst = static_cast<uint8_t*>(c->stage[lane_k].p);
+    j.attempt(*c->pool, 4, true);
+  };
+  if (narrow && n_rows > 0) {
+    GNB_CUDA(cudaEventSynchronize(c->copied[0]), "event sync");
+    start_narrow(0, 0);
+  }
   int64_t chunk = 0;
   for (int64_t r0 = 0; r0 < n_rows; r0 += rows, ++chunk) {
     const int lane = static_cast<int>(chunk % kLanes);
@@ -828,9 +881,20 @@ static int predict_host_impl(const void* xv, int x_type, int64_t n_rows, int32_t
                                    cudaMemcpyHostToDevice, s),
                  "H2D 2D");
     } else if (narrow) {
-      GNB_CUDA(cudaEventSynchronize(c->copied[lane]), "event sync");  // staging free again
-      const int nt = narrow_chunk(*c->pool, x + r0 * ldx, n, n_features, ldx,
-                                  static_cast<uint8_t*>(c->stage[lane].p), ld8, ld16);
+      // this chunk was narrowed in the background (started one chunk ago);
+      // start the next one before issuing this chunk's copies and kernels
+      const auto tn = std::chrono::steady_clock::now();
+      const int nt = jobs[chunk & 1].finish(*c->pool);
+      const auto tw = std::chrono::steady_clock::now();
+      if (r0 + rows < n_rows) {
+        const int nl = static_cast<int>((chunk + 1) % kLanes);
+        GNB_CUDA(cudaEventSynchronize(c->copied[nl]), "event sync");  // its staging is free
+        start_narrow(chunk + 1, nl);
+      }
+      if (timing) {
+        t_narrow += std::chrono::duration<double>(tw - tn).count();
+        t_wait += std::chrono::duration<double>(std::chrono::steady_clock::now() - tw).count();
+      }
       if (nt == GNB_X_U4) {  // nibbles over PCIe, unpacked to uint8 rows on the device
         GNB_CUDA(cudaMemcpyAsync(c->x4[lane].p, c->stage[lane].p, size_t(n) * (ld8 / 2),
                                  cudaMemcpyHostToDevice, s),
@@ -903,7 +967,14 @@ static int predict_host_impl(const void* xv, int x_type, int64_t n_rows, int32_t
                                size_t(n) * n_classes * 8, cudaMemcpyDeviceToHost, s),
                "D2H");
   }
+  const auto t_issue = std::chrono::steady_clock::now();
   for (int i = 0; i < kLanes; ++i) GNB_CUDA(cudaStreamSynchronize(c->s[i]), "sync");
+  if (timing)
+    fprintf(stderr, "[gnb host] rows %lld chunks %lld: narrow wait %.3f ms, next-start %.3f ms, "
+            "loop %.3f ms, drain %.3f ms\n", (long long)n_rows, (long long)chunk,
+            t_narrow * 1e3, t_wait * 1e3,
+            std::chrono::duration<double>(t_issue - t0).count() * 1e3,
+            std::chrono::duration<double>(std::chrono::steady_clock::now() - t_issue).count() * 1e3);
   if (elapsed_ns)
     *elapsed_ns = std::chrono::duration_cast<std::chrono::nanoseconds>(
                       std::chrono::steady_clock::now() - t0)

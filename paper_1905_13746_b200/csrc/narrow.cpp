@@ -6,6 +6,7 @@
 // same bytes.  Returns whether every count of rows [r0, r1) fits BITS bits
 // (negative counts never fit).  Pitch padding of each output row is zeroed.
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 
 #if defined(__x86_64__)
@@ -102,8 +103,56 @@ __attribute__((target("avx2"))) bool narrow_avx2(const int32_t* s, int32_t F, in
   return (all >> BITS) == 0;
 }
 
+// 16 counts per step with AVX-512: saturating down-conversion (vpmovusdb /
+// vpmovusdw) straight from the 512-bit load.
+template <int BITS>
+__attribute__((target("avx512f,avx512bw"))) bool narrow_avx512(const int32_t* s, int32_t F,
+                                                               int64_t ldx, uint8_t* d,
+                                                               int64_t dpitch, int64_t r0,
+                                                               int64_t r1) {
+  const int32_t F16 = F / 16 * 16;
+  __m512i acc = _mm512_setzero_si512();
+  const __m128i nib = _mm_set1_epi16(0x1001);
+  for (int64_t r = r0; r < r1; ++r) {
+    const int32_t* a = s + r * ldx;
+    uint8_t* o = d + r * dpitch;
+    for (int32_t j = 0; j < F16; j += 16) {
+      const __m512i x = _mm512_loadu_si512(a + j);
+      acc = _mm512_or_si512(acc, x);
+      if constexpr (BITS == 16) {
+        _mm256_storeu_si256(reinterpret_cast<__m256i*>(o + 2 * j), _mm512_cvtusepi32_epi16(x));
+      } else {
+        const __m128i b = _mm512_cvtusepi32_epi8(x);
+        if constexpr (BITS == 8) {
+          _mm_storeu_si128(reinterpret_cast<__m128i*>(o + j), b);
+        } else {
+          const __m128i p = _mm_maddubs_epi16(b, nib);
+          _mm_storel_epi64(reinterpret_cast<__m128i*>(o + j / 2), _mm_packus_epi16(p, p));
+        }
+      }
+    }
+    if (F16 < F && !narrow_scalar<BITS>(s, F, ldx, d, dpitch, r, r + 1, F16)) return false;
+    if (F16 == F) {
+      const int64_t used = BITS == 4 ? (F + 1) / 2 : BITS == 8 ? F : 2 * int64_t(F);
+      if (dpitch > used) std::memset(o + used, 0, static_cast<size_t>(dpitch - used));
+    }
+  }
+  return (static_cast<uint32_t>(_mm512_reduce_or_epi32(acc)) >> BITS) == 0;
+}
+
 bool have_avx2() {
   static const bool v = __builtin_cpu_supports("avx2");
+  return v;
+}
+
+// GNB_NARROW_ISA=avx2 / scalar: force a narrower instruction set (A/B)
+int isa() {
+  static const int v = [] {
+    const char* e = getenv("GNB_NARROW_ISA");
+    if (e && !strcmp(e, "scalar")) return 0;
+    if (__builtin_cpu_supports("avx512bw") && !(e && !strcmp(e, "avx2"))) return 2;
+    return have_avx2() ? 1 : 0;
+  }();
   return v;
 }
 #endif
@@ -113,7 +162,15 @@ bool have_avx2() {
 bool narrow_rows_block(int bits, const int32_t* s, int32_t F, int64_t ldx, uint8_t* d,
                        int64_t dpitch, int64_t r0, int64_t r1) {
 #if defined(__x86_64__)
-  if (have_avx2()) {
+  const int level = isa();
+  if (level == 2) {
+    switch (bits) {
+      case 4: return narrow_avx512<4>(s, F, ldx, d, dpitch, r0, r1);
+      case 8: return narrow_avx512<8>(s, F, ldx, d, dpitch, r0, r1);
+      default: return narrow_avx512<16>(s, F, ldx, d, dpitch, r0, r1);
+    }
+  }
+  if (level == 1) {
     switch (bits) {
       case 4: return narrow_avx2<4>(s, F, ldx, d, dpitch, r0, r1);
       case 8: return narrow_avx2<8>(s, F, ldx, d, dpitch, r0, r1);

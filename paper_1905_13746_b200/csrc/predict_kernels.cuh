@@ -92,10 +92,11 @@ __device__ __forceinline__ double converted(const uint4& v, int e) {
 }
 
 // ------------------------------------------------------------------ inner loops
-// Negative-count flag (int32 rows only).  The last 16-B quad of a row may run
-// past feature F into the row's pitch padding, which callers need not
-// initialise (and the 1-D bulk row-box copy moves raw): only the quad's first
-// (F - 4*(nq-1)) elements count towards the flag.
+// Negative-count flag (int32 rows only).  TMA tensor boxes zero-fill columns
+// >= F, but the row-box kernel's 1-D bulk tile copy moves the HBM row pitch
+// raw, and callers need not initialise pitch padding: when F is not a
+// multiple of 4 the last quad of a row carries padding, and only its first
+// (F - 4*(nq-1)) elements may count towards the flag (TAILMASK instances).
 struct QuadMask {
   uint32_t y, z, w;
 };
@@ -135,21 +136,20 @@ __device__ __forceinline__ void score_quad(double (&acc)[CP], const uint4 v, con
 
 template <int CP, typename T, typename Tab, bool FMA>
 __device__ __forceinline__ void score_chunk(double (&acc)[CP], const uint8_t* box, uint32_t row,
-                                            const Tab& tab, int nq, uint32_t& neg,
-                                            const QuadMask& lm) {
+                                            const Tab& tab, int nq, uint32_t& neg) {
   constexpr int EQ = Elem<T>::kPerQuad;
   if (nq == 8) {
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
       const uint4 v = *reinterpret_cast<const uint4*>(box + swz128(row, q));
-      if (Elem<T>::kSigned) neg |= quad_neg(v, q == 7, lm);
+      if (Elem<T>::kSigned) neg |= v.x | v.y | v.z | v.w;
       score_quad<CP, T, Tab, FMA>(acc, v, tab, EQ * q);
     }
   } else {
 #pragma unroll 1
     for (int q = 0; q < nq; ++q) {
       const uint4 v = *reinterpret_cast<const uint4*>(box + swz128(row, q));
-      if (Elem<T>::kSigned) neg |= quad_neg(v, q == nq - 1, lm);
+      if (Elem<T>::kSigned) neg |= v.x | v.y | v.z | v.w;
       score_quad<CP, T, Tab, FMA>(acc, v, tab, EQ * q);
     }
   }
@@ -229,15 +229,14 @@ __device__ __forceinline__ const double* chunk_table(const PredictParams& p, int
 template <int CP, typename T, int R, bool FMA>
 __device__ __forceinline__ void score_chunk_uniform(double (&acc)[R][CP], const uint8_t* box,
                                                     const uint32_t (&rows)[R], const double* tab,
-                                                    int nq, uint32_t (&neg)[R],
-                                                    const QuadMask& lm) {
+                                                    int nq, uint32_t (&neg)[R]) {
   constexpr int EQ = Elem<T>::kPerQuad;
   auto quad = [&](int q) {
     uint4 v[R];
 #pragma unroll
     for (int i = 0; i < R; ++i) {
       v[i] = *reinterpret_cast<const uint4*>(box + swz128(rows[i], q));
-      if (Elem<T>::kSigned) neg[i] |= quad_neg(v[i], q == nq - 1, lm);
+      if (Elem<T>::kSigned) neg[i] |= v[i].x | v[i].y | v[i].z | v[i].w;
     }
 #pragma unroll
     for (int e = 0; e < EQ; ++e) {
@@ -270,14 +269,14 @@ template <int CP, typename T, int R, bool FMA>
 __device__ __forceinline__ void score_chunk_mixed(const PredictParams& p, double (&acc)[R][CP],
                                                   const uint8_t* box, const uint32_t (&rows)[R],
                                                   const int (&slot)[R], int ch, int nq,
-                                                  uint32_t (&neg)[R], const QuadMask& lm) {
+                                                  uint32_t (&neg)[R]) {
 #pragma unroll
   for (int i = 0; i < R; ++i) {
     const GlobalTab tab{chunk_table<CP, T>(p, max(slot[i], 0), ch)};
     double a[CP];
 #pragma unroll
     for (int c = 0; c < CP; ++c) a[c] = acc[i][c];
-    score_chunk<CP, T, GlobalTab, FMA>(a, box, rows[i], tab, nq, neg[i], lm);
+    score_chunk<CP, T, GlobalTab, FMA>(a, box, rows[i], tab, nq, neg[i]);
 #pragma unroll
     for (int c = 0; c < CP; ++c) acc[i][c] = a[c];
   }
@@ -438,16 +437,15 @@ __global__ void __launch_bounds__((NW + 1) * 32)
           if (B > 1 && ch >= NCH) break;
           const int nf = min(CF, p.n_features - ch * CF);
           const int nq = (nf + EQ - 1) / EQ;
-          const QuadMask lm = last_quad_mask(nf);
           const uint8_t* box = smem + L::kX + stage * L::kXBytes + b * L::kBox;
           if (ts >= 0) {
             score_chunk_uniform<CP, T, R, FMA>(
                 acc, box, rows,
                 reinterpret_cast<const double*>(smem + L::kTab + stage * L::kTabBytes +
                                                 L::kPrior + b * L::kTabChunk),
-                nq, neg, lm);
+                nq, neg);
           } else {
-            score_chunk_mixed<CP, T, R, FMA>(p, acc, box, rows, slot, ch, nq, neg, lm);
+            score_chunk_mixed<CP, T, R, FMA>(p, acc, box, rows, slot, ch, nq, neg);
           }
         }
         __syncwarp();
@@ -522,7 +520,7 @@ __host__ __device__ inline int rowbox_tab_feats(int F, int EQ, int n_tab_blocks)
 }
 
 // the nq quads of one row against one slot's smem table (prior excluded)
-template <int CP, typename T, bool FMA>
+template <int CP, typename T, bool FMA, bool TAILMASK>
 __device__ __forceinline__ void rowbox_score_smem(double (&acc)[CP], const uint8_t* xrow,
                                                   const double* tab, int nq, uint32_t& neg,
                                                   const QuadMask& lm) {
@@ -530,7 +528,7 @@ __device__ __forceinline__ void rowbox_score_smem(double (&acc)[CP], const uint8
 #pragma unroll 2
   for (int q = 0; q < nq; ++q) {
     const uint4 v = *reinterpret_cast<const uint4*>(xrow + 16 * q);
-    if (Elem<T>::kSigned) neg |= quad_neg(v, q == nq - 1, lm);
+    if (Elem<T>::kSigned) neg |= TAILMASK ? quad_neg(v, q == nq - 1, lm) : (v.x | v.y | v.z | v.w);
 #pragma unroll
     for (int e = 0; e < EQ; ++e) {
       const double xd = converted<T, FMA>(v, e);
@@ -544,7 +542,8 @@ __device__ __forceinline__ void rowbox_score_smem(double (&acc)[CP], const uint8
   }
 }
 
-template <int CP, typename T, int kRowBoxAhead, bool FMA, int RQ = kRegQuads<CP>, int MINB = 4>
+template <int CP, typename T, int kRowBoxAhead, bool FMA, int RQ = kRegQuads<CP>, int MINB = 4,
+          bool TAILMASK = false>
 __global__ void __launch_bounds__(5 * 32, MINB)
     predict_rowbox_kernel(const __grid_constant__ PredictMaps maps, const PredictParams p) {
   const CUtensorMap& xmap = maps.main;
@@ -711,7 +710,8 @@ __global__ void __launch_bounds__(5 * 32, MINB)
 #pragma unroll
           for (int q = 0; q < RQ; ++q) {
             if (q < nq) {
-              if (Elem<T>::kSigned) neg |= quad_neg(v[q], q == nq - 1, lm);
+              if (Elem<T>::kSigned)
+                neg |= TAILMASK ? quad_neg(v[q], q == nq - 1, lm) : (v[q].x | v[q].y | v[q].z | v[q].w);
 #pragma unroll
               for (int e = 0; e < EQ; ++e) {
                 const double xd = converted<T, FMA>(v[q], e);
@@ -732,7 +732,7 @@ __global__ void __launch_bounds__(5 * 32, MINB)
           const double* st = res + s * static_cast<int>(L.res_stride);
 #pragma unroll
           for (int c = 0; c < CP; ++c) acc[c] = st[c];
-          rowbox_score_smem<CP, T, FMA>(acc, xrow, st + CP, nq, neg, lm);
+          rowbox_score_smem<CP, T, FMA, TAILMASK>(acc, xrow, st + CP, nq, neg, lm);
         } else {
           const double* stab =
               reinterpret_cast<const double*>(smem + L.tab + stage * L.tab_bytes);
@@ -741,13 +741,14 @@ __global__ void __launch_bounds__(5 * 32, MINB)
 #pragma unroll
           for (int c = 0; c < CP; ++c) acc[c] = ts >= 0 ? stab[c] : __ldg(p.prior + s * CP + c);
           if (ts >= 0) {
-            rowbox_score_smem<CP, T, FMA>(acc, xrow, stab + CP, nq, neg, lm);
+            rowbox_score_smem<CP, T, FMA, TAILMASK>(acc, xrow, stab + CP, nq, neg, lm);
           } else {
             const GlobalTab tab{p.tab + s * slot_tab};
 #pragma unroll 1
             for (int q = 0; q < nq; ++q) {
               const uint4 v = *reinterpret_cast<const uint4*>(xrow + 16 * q);
-              if (Elem<T>::kSigned) neg |= quad_neg(v, q == nq - 1, lm);
+              if (Elem<T>::kSigned)
+                neg |= TAILMASK ? quad_neg(v, q == nq - 1, lm) : (v.x | v.y | v.z | v.w);
               score_quad<CP, T, GlobalTab, FMA>(acc, v, tab, EQ * q);
             }
           }
@@ -858,9 +859,10 @@ static cudaError_t launch_tma(const PredictMaps& map, const PredictParams& p,
 inline constexpr int kRowBoxMaxQuads = 26;       // 128 rows x 26 x 16 B = 52 KB per stage
 inline constexpr uint32_t kRowBoxRingBytes = 53248;  // ring depth: stages x box ~ 52 KB
 
-template <int CP, typename T, int AHEAD, bool FMA, int RQ = kRegQuads<CP>, int MINB = 4>
-static cudaError_t launch_rowbox_a(const PredictMaps& map, PredictParams p, cudaStream_t stream) {
-  constexpr auto kern = predict_rowbox_kernel<CP, T, AHEAD, FMA, RQ, MINB>;
+template <int CP, typename T, int AHEAD, bool FMA, int RQ = kRegQuads<CP>, int MINB = 4,
+          bool TAILMASK = false>
+static cudaError_t launch_rowbox_b(const PredictMaps& map, PredictParams p, cudaStream_t stream) {
+  constexpr auto kern = predict_rowbox_kernel<CP, T, AHEAD, FMA, RQ, MINB, TAILMASK>;
   int sms = 0;
   cudaError_t e = kernel_prepare<kern>(&sms);
   if (e != cudaSuccess) return e;
@@ -908,6 +910,15 @@ static cudaError_t launch_rowbox_a(const PredictMaps& map, PredictParams p, cuda
   if (grid == 0) return cudaSuccess;
   kern<<<grid, 5 * 32, smem, stream>>>(map, p);
   return cudaGetLastError();
+}
+
+// The masked instance only where raw pitch padding can reach the flag: int32
+// rows, 1-D bulk tiles, F not a multiple of 4 (the check costs issue slots).
+template <int CP, typename T, int AHEAD, bool FMA, int RQ = kRegQuads<CP>, int MINB = 4>
+static cudaError_t launch_rowbox_a(const PredictMaps& map, PredictParams p, cudaStream_t stream) {
+  if (Elem<T>::kSigned && p.rowbox_contig && p.n_features % Elem<T>::kPerQuad != 0)
+    return launch_rowbox_b<CP, T, AHEAD, FMA, RQ, MINB, true>(map, p, stream);
+  return launch_rowbox_b<CP, T, AHEAD, FMA, RQ, MINB, false>(map, p, stream);
 }
 
 // GNB_ROWBOX_WIDE=0: rows of 14-26 quads keep their stage while scoring (A/B).
