@@ -645,6 +645,10 @@ class Pool {
 };
 
 constexpr int kLanes = 3;  // chunk pipeline depth (streams)
+// int32 host rows in page-locked memory: every 3rd chunk goes raw by DMA, two
+// are narrowed on host threads -- 111M vs 79M rows/s at F=256 on the B200 box
+// (raw every 2nd / 4th: 89M / 100M; tools/e2e_hybrid_ab.sh).
+constexpr int64_t kHostRawEvery = 3;
 
 struct HostCtx {
   int device = -1;
@@ -738,13 +742,10 @@ bool narrowing_enabled() {  // read per call (once per host pipeline call)
 }
 
 // MiB of X crossing PCIe per pipeline chunk (GNB_HOST_CHUNK_MB, read once).
-int64_t host_chunk_bytes() {
-  static const int64_t v = [] {
-    const char* e = getenv("GNB_HOST_CHUNK_MB");
-    const int64_t mb = e ? atoll(e) : 64;
-    return (mb >= 1 && mb <= 4096 ? mb : 64) << 20;
-  }();
-  return v;
+int64_t host_chunk_bytes() {  // read per host pipeline call
+  const char* e = getenv("GNB_HOST_CHUNK_MB");
+  const int64_t mb = e ? atoll(e) : 64;
+  return (mb >= 1 && mb <= 4096 ? mb : 64) << 20;
 }
 
 int64_t chunk_rows_for(int64_t row_bytes) {
@@ -832,8 +833,8 @@ static int predict_host_impl(const void* xv, int x_type, int64_t n_rows, int32_t
       if (p) p->wait();
     }
   } drain{narrow ? c->pool : nullptr};
-  auto start_narrow = [&](int64_t k, int lane_k) {
-    NarrowJob& j = jobs[k & 1];
+  auto start_narrow = [&](int64_t k, int lane_k, int slot) {
+    NarrowJob& j = jobs[slot];
     j.src = x + k * rows * ldx;
     j.n = std::min(rows, n_rows - k * rows);
     j.F = n_features;
@@ -843,9 +844,37 @@ static int predict_host_impl(const void* xv, int x_type, int64_t n_rows, int32_t
     j.dst = static_cast<uint8_t*>(c->stage[lane_k].p);
     j.attempt(*c->pool, 4, true);
   };
+  // Hybrid split of int32 chunks (GNB_HOST_RAW_EVERY=N: every N-th chunk is
+  // copied as raw int32 rows by the DMA engine while host threads narrow the
+  // others -- the copy engine reads host memory without any CPU, so both paths
+  // draw on host DRAM bandwidth at once).  0 = narrow every chunk.
+  // Only for page-locked input: from pageable memory the driver stages the
+  // copy through its own buffers on the CPU, which is slower than narrowing.
+  const char* re = getenv("GNB_HOST_RAW_EVERY");
+  int64_t raw_every = re ? atoll(re) : kHostRawEvery;
+  if (narrow && raw_every > 0) {
+    cudaPointerAttributes pa{};
+    if (cudaPointerGetAttributes(&pa, x) != cudaSuccess || pa.type != cudaMemoryTypeHost) {
+      cudaGetLastError();  // clear a non-sticky "not a CUDA pointer" error
+      raw_every = 0;
+    }
+  }
+  const int64_t n_chunks = (n_rows + rows - 1) / rows;
+  auto narrow_chunk_k = [&](int64_t k) {
+    return narrow && !(raw_every > 0 && k % raw_every == raw_every - 1);
+  };
+  auto next_narrow = [&](int64_t k) -> int64_t {
+    for (int64_t k2 = k + 1; k2 < n_chunks; ++k2)
+      if (narrow_chunk_k(k2)) return k2;
+    return -1;
+  };
+  int pend_slot = 0;
   if (narrow && n_rows > 0) {
-    GNB_CUDA(cudaEventSynchronize(c->copied[0]), "event sync");
-    start_narrow(0, 0);
+    const int64_t first = next_narrow(-1);
+    if (first >= 0) {
+      GNB_CUDA(cudaEventSynchronize(c->copied[first % kLanes]), "event sync");
+      start_narrow(first, static_cast<int>(first % kLanes), pend_slot);
+    }
   }
   int64_t chunk = 0;
   for (int64_t r0 = 0; r0 < n_rows; r0 += rows, ++chunk) {
@@ -880,16 +909,18 @@ static int predict_host_impl(const void* xv, int x_type, int64_t n_rows, int32_t
         GNB_CUDA(cudaMemcpy2DAsync(dx, dld * eb, src, ldx * eb, size_t(n_features) * eb, n,
                                    cudaMemcpyHostToDevice, s),
                  "H2D 2D");
-    } else if (narrow) {
-      // this chunk was narrowed in the background (started one chunk ago);
-      // start the next one before issuing this chunk's copies and kernels
+    } else if (narrow_chunk_k(chunk)) {
+      // this chunk was narrowed in the background (started while the previous
+      // chunk was issued); start the next narrow chunk before issuing this one
       const auto tn = std::chrono::steady_clock::now();
-      const int nt = jobs[chunk & 1].finish(*c->pool);
+      const int nt = jobs[pend_slot].finish(*c->pool);
       const auto tw = std::chrono::steady_clock::now();
-      if (r0 + rows < n_rows) {
-        const int nl = static_cast<int>((chunk + 1) % kLanes);
+      const int64_t nxt = next_narrow(chunk);
+      if (nxt >= 0) {
+        const int nl = static_cast<int>(nxt % kLanes);
         GNB_CUDA(cudaEventSynchronize(c->copied[nl]), "event sync");  // its staging is free
-        start_narrow(chunk + 1, nl);
+        pend_slot ^= 1;
+        start_narrow(nxt, nl, pend_slot);
       }
       if (timing) {
         t_narrow += std::chrono::duration<double>(tw - tn).count();

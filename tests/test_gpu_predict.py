@@ -263,7 +263,7 @@ def test_narrowest_roundtrip():
     assert dense.narrowest(x * 1000).dtype == torch.int32
 
 
-@pytest.mark.parametrize("narrow", ["0", "1"])
+@pytest.mark.parametrize("narrow", ["0", "1", "raw2"])
 @pytest.mark.parametrize("hi,neg", [(16, False), (256, False), (60000, False), (2**31 - 1, False),
                                     (100, True), (16, True)])
 @pytest.mark.parametrize("F", [45, 64])
@@ -272,7 +272,9 @@ def test_host_entry_narrowing_paths(hi, neg, narrow, F, monkeypatch):
     uint8 / uint16 / int32 by content) gives identical results."""
     import ctypes
     from paper_1905_13746_b200 import _native as N
-    monkeypatch.setenv("GNB_HOST_NARROW", narrow)
+    monkeypatch.setenv("GNB_HOST_NARROW", "0" if narrow == "0" else "1")
+    monkeypatch.setenv("GNB_HOST_RAW_EVERY", "2" if narrow == "raw2" else "0")
+    monkeypatch.setenv("GNB_HOST_CHUNK_MB", "1")      # several chunks per call
     rng = np.random.default_rng(hi % 1000)
     S, C, G = 2, 2, 3
     prior, ll, route = _tables(rng, S, C, F, G)
