@@ -67,6 +67,20 @@ class DenseCorpus:
         self.max_count = _L.gnb_corpus_max_count(handle)
         self.nnz = _L.gnb_corpus_nnz(handle)
         self._ids = None
+        self._merge = None
+        # The C++ parser lower-cases ASCII only; the reference lower-cases with
+        # str.lower() (corpus.py:51), which also folds non-ASCII letters and so
+        # can merge mnemonics the parser kept apart.  Fold those here: columns
+        # whose Python-lowered keys coincide are summed (like from_counts does).
+        if not all(v.isascii() for v in self.vocab):
+            lowered = [v.lower() for v in self.vocab]
+            if lowered != self.vocab:
+                new_vocab = sorted(set(lowered))
+                col = {v: j for j, v in enumerate(new_vocab)}
+                self._merge = np.array([col[v] for v in lowered], dtype=np.int64)
+                mult = int(np.bincount(self._merge).max())
+                self.vocab = new_vocab
+                self.max_count = self.max_count * mult     # bound on merged counts
 
     def __len__(self) -> int:
         return len(self.size)
@@ -97,6 +111,17 @@ class DenseCorpus:
         V = max(len(self.vocab), 1)
         if out is None:
             out = np.empty((hi - lo, V), dtype=dtype)
+        if self._merge is not None:   # fold case-variant columns (see __init__)
+            raw = np.empty((hi - lo, max(len(self._merge), 1)), dtype=np.int32)
+            if _L.gnb_corpus_dense(self._h, N.X_I32, raw.ctypes.data, raw.shape[1], lo,
+                                   hi - lo, threads) != N.GNB_OK:
+                raise InvalidConfigError("gnb_corpus_dense failed")
+            merged = np.zeros((hi - lo, V), dtype=np.int64)
+            np.add.at(merged.T, self._merge, raw.T)
+            if merged.size and int(merged.max()) > np.iinfo(dtype).max:
+                raise InvalidConfigError(f"merged counts do not fit {dtype}")
+            out[:, :V] = merged
+            return out
         ldx = out.strides[0] // out.itemsize
         if _L.gnb_corpus_dense(self._h, _DTYPES[dtype], out.ctypes.data, ldx, lo, hi - lo,
                                threads) != N.GNB_OK:

@@ -95,3 +95,28 @@ def test_duplicate_and_case_keys_like_json_loads(ops, want):
     text = '{"id": "a", "label": "benign", "size_bytes": 1, "opcodes": %s}' % ops
     rec = ingest.parse_corpus(text)[0]
     assert rec.histogram.entries == want
+
+
+def test_non_ascii_mnemonics_fold_like_str_lower():
+    """Keys differing only in non-ASCII case merge as the reference's
+    str.lower() merges them (corpus.py:51), though the C++ parser folds ASCII
+    only: same vocabulary, same counts."""
+    import json
+    from refpkg import groupnb
+    from paper_1905_13746_b200 import ingest
+    gn = groupnb()
+    if gn is None:
+        pytest.skip("baseline/_ref not installed")
+    recs = [{"id": "a", "label": "malware", "size_bytes": 10,
+             "opcodes": {"MÖV": 2, "möv": 3, "Möv": 1, "ADD": 4, "add": 1, "ßhr": 2}},
+            {"id": "b", "label": "benign", "size_bytes": 20,
+             "opcodes": {"İnc": 5, "möv": 7, "ÉTÉ": 1, "été": 2}}]
+    text = "\n".join(json.dumps(r, ensure_ascii=False) for r in recs)
+    ref = gn.parse_corpus(text)
+    got = ingest.read_corpus(text)
+    want_vocab = sorted({op for s in ref for op in s.histogram.entries})
+    assert got.vocab == want_vocab
+    x = got.dense(np.int32)
+    for i, s in enumerate(ref):
+        row = {got.vocab[j]: int(x[i, j]) for j in np.nonzero(x[i])[0]}
+        assert row == s.histogram.entries
