@@ -916,6 +916,7 @@ def run_ragged(args, world, rank, local):
     import numpy as np
     import torch
     from oracle import oracle as O
+    from paper_1905_13746_b200 import _native as N_
     from paper_1905_13746_b200 import dense
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
@@ -955,8 +956,16 @@ def run_ragged(args, world, rank, local):
     bps = 4 * F + 24
     shuf = torch.randperm(N, device=dev)
     xs_, ss_ = xg[shuf].contiguous(), size[shuf].contiguous()
+    lab_g, lp_g = label.clone(), lp.clone()   # grouped-order outputs (oracle-checked above)
     mix_ms, _ = _timed_launches(
         lambda: dense.predict(xs_, ss_, t, label_out=label, logpost_out=lp), args.steps, 3)
+    hint_ms, _ = _timed_launches(
+        lambda: dense.predict(xs_, ss_, t, label_out=label, logpost_out=lp, order="mixed"),
+        args.steps, 3)
+    # shuffled outputs == grouped outputs at the same rows (bit for bit)
+    mix_ok = bool(torch.equal(label, lab_g[shuf]) and
+                  torch.equal(lp.view(torch.int64), lp_g[shuf].view(torch.int64)))
+    mixed_rows = int(N_.lib.gnb_predict_mixed_rows(F, N_.X_I32, 2, len(trained)))
     # same shuffled batch, device slot sort + gather4 K-PRED (both inside the timed launch)
     srt_ms, _ = _timed_launches(
         lambda: dense.predict(xs_, ss_, t, label_out=label, logpost_out=lp,
@@ -972,7 +981,16 @@ def run_ragged(args, world, rank, local):
             "trained_groups": len(trained), "bit_exact_subsample_vs_oracle": ok,
             "shuffled_rows": {"ms": round(mix_ms, 4),
                               "value": round(N / (mix_ms / 1e3), 1),
-                              "note": "rows in random group order: mixed tiles, L1 table path"},
+                              "frac": round(N * bps / (mix_ms / 1e3) / 1e9 / peak, 4),
+                              "bit_exact_vs_grouped_order": mix_ok,
+                              "kernel": ("predict_mixed_kernel (all slot tables resident in "
+                                         "smem, in-tile slot sort, no device sort)"
+                                         if mixed_rows else "predict_tma_kernel (L1 tables)"),
+                              "order_hint_mixed": {"ms": round(hint_ms, 4),
+                                                   "frac": round(N * bps / (hint_ms / 1e3) / 1e9 / peak, 4)},
+                              "note": "same rows in random order, one plain predict call "
+                                      "(order auto: a device count of the tiles that mix "
+                                      "models gates the kernel choice, timed)"},
             "shuffled_rows_slot_sorted": {
                 "ms": round(srt_ms, 4), "value": round(N / (srt_ms / 1e3), 1),
                 "frac": round(N * bps / (srt_ms / 1e3) / 1e9 / peak, 4),

@@ -61,6 +61,17 @@ enum { GNB_X_U4 = 3 };
 
 /* predict arithmetic (gnb_predict_mode) */
 enum { GNB_MODE_EXACT = 0, GNB_MODE_FMA = 1 };
+/* row-order hint, OR-ed into gnb_predict_mode's `mode` (ragged batches of >= 2
+ * slots whose tables fit in shared memory, gnb_predict_mixed_rows() > 0):
+ *   GNB_ORDER_AUTO     (0, every other entry point) a device pass over the sizes
+ *                      counts the 128-row tiles that mix models and gates the
+ *                      kernel on the device, no host sync: grouped batches
+ *                      take the 6-CTA kernel, interleaved ones the mixed-slot
+ *                      kernel;
+ *   GNB_ORDER_GROUPED  rows grouped by size group (GroupedCorpus order): no check;
+ *   GNB_ORDER_MIXED    rows in any order: mixed-slot kernel, no check.
+ * Results are identical for every hint. */
+enum { GNB_ORDER_AUTO = 0, GNB_ORDER_GROUPED = 0x10, GNB_ORDER_MIXED = 0x20 };
 
 int gnb_abi_version(void);
 const char* gnb_strerror(int code);
@@ -99,7 +110,17 @@ int gnb_predict_typed(const void* x, int32_t x_type, int64_t n_rows, int32_t n_f
                       int32_t n_classes, const void* packed, int32_t* label_out,
                       double* logpost_out, uintptr_t stream);
 
-/* Ragged batches in arbitrary row order.  gnb_slot_sort writes perm[n] = row
+/* Ragged batches in arbitrary row order (engine.py:198-202 routes every file
+ * by its own size).  When this returns > 0 for a batch's shape, gnb_predict /
+ * gnb_predict_typed / gnb_predict_mode already score rows of any slot order at
+ * streaming speed (mixed-slot kernel: every slot's table resident in shared
+ * memory, each tile's rows sorted by slot inside the CTA; the value is the tile
+ * height) and no slot sort is needed; 0 = the sort + permuted path below pays
+ * for shuffled batches (C > 2, or tables too large for shared memory). */
+int32_t gnb_predict_mixed_rows(int32_t n_features, int32_t x_type, int32_t n_classes,
+                               int32_t n_slots);
+
+/* gnb_slot_sort writes perm[n] = row
  * indices grouped by routed model slot (device counting sort over the sizes;
  * rows with size out of range last), using `workspace`
  * (gnb_slot_sort_workspace_bytes).  gnb_predict_permuted then scores tiles of

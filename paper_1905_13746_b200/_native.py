@@ -20,6 +20,7 @@ HEADER = os.path.join(os.path.dirname(_HERE), "include", "gnb.h")
 
 GNB_OK, GNB_EINVAL, GNB_ECUDA, GNB_EUNSUPPORTED, GNB_ENOMEM = 0, 1, 2, 3, 4
 GNB_MODE_EXACT, GNB_MODE_FMA = 0, 1
+GNB_ORDER_AUTO, GNB_ORDER_GROUPED, GNB_ORDER_MIXED = 0, 0x10, 0x20
 ROW_OUT_OF_RANGE = -1
 ROW_NEGATIVE_COUNT = -2
 MAX_CLASSES = 16
@@ -53,6 +54,7 @@ _SIGS = {
                     C.c_int),
     "gnb_predict_typed": ([_p, _i32, _i64, _i32, _i64, _p, _i32, _i32, _p, _i32, _i32, _p, _p,
                            _p, _up], C.c_int),
+    "gnb_predict_mixed_rows": ([_i32, _i32, _i32, _i32], _i32),
     "gnb_slot_sort_workspace_bytes": ([_i64, _i32], _sz),
     "gnb_slot_sort": ([_p, _i64, _i32, _i32, _p, _i32, _p, _p, _sz, _up], C.c_int),
     "gnb_predict_permuted": ([_p, _i32, _i64, _i32, _i64, _p, _i32, _i32, _p, _i32, _i32, _p, _p,

@@ -519,7 +519,7 @@ def classify_corpus(bundle, corpus, *, device=None, warmup: bool = True):
         xv = host.to(dev, non_blocking=True)[:, :V]
         sd = torch.from_numpy(gid).to(dev, non_blocking=True)
         xg = dense.gather_features(xv, sd, tables, feats, nfeat)
-        perm = dense.slot_sort(sd, tables) if len(packed.ids) > 1 else None
+        perm = dense.slot_sort(sd, tables) if dense.needs_slot_sort(xg.dtype, tables) else None
         lab, lp = dense.predict(xg, sd, tables, perm=perm)
         out = lab.cpu().numpy(), lp.cpu().numpy()
         return out, time.perf_counter_ns() - t0

@@ -11,6 +11,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <vector>
 
@@ -202,6 +203,27 @@ static bool rowbox_bulk() {
   return v != 0;
 }
 
+// The 4-byte tile-mix counter of GNB_ORDER_AUTO, one per (device, stream):
+// reuse on the same stream is stream-ordered (memset -> count -> gated
+// kernels), different streams never share one.  Allocated once, never freed.
+static int32_t* gate_counter(cudaStream_t stream) {
+  static std::mutex mu;
+  static std::map<std::pair<int, uintptr_t>, int32_t*> counters;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  std::lock_guard<std::mutex> lock(mu);
+  int32_t*& c = counters[{dev, reinterpret_cast<uintptr_t>(stream)}];
+  if (c == nullptr && cudaMalloc(reinterpret_cast<void**>(&c), sizeof(int32_t)) != cudaSuccess)
+    c = nullptr;
+  return c;
+}
+
+// True when predict_device will take the mixed-slot kernel (rows of any slot
+// order at full speed, tables resident): no device slot sort for ragged batches.
+static bool mixed_kernel(int32_t F, int x_type, int32_t C, int32_t S) {
+  return predict_rowbox_quads(F, x_type, C) == 0 && predict_mixed_rows(F, x_type, C, S) > 0;
+}
+
 static int predict_device(const void* x, int x_type, int64_t n_rows, int32_t F, int64_t ldx,
                           const int32_t* size, int32_t width, int32_t limit,
                           const int32_t* route, int32_t S, int32_t C, const void* packed,
@@ -230,22 +252,54 @@ static int predict_device(const void* x, int x_type, int64_t n_rows, int32_t F, 
     p.label = label + r0;
     p.logpost = logpost ? logpost + r0 * C : nullptr;
     p.perm = use_tma ? perm : nullptr;  // the L1 kernel walks rows in order
-    p.mode = mode;
+    p.mode = mode & 0xF;
+    const int order = mode & (GNB_ORDER_GROUPED | GNB_ORDER_MIXED);
     PredictMaps map;
     const PredictMaps* mp = nullptr;
     if (use_tma) {
       // row-box mode (short rows): whole rows per box, unswizzled; gather mode:
       // box height 1 (tile::gather4 loads 4 rows per instruction)
+      // mixed-slot mode (>= 2 slots whose tables fit in smem): box height = its tile
+      // (short rows keep the row-box kernel, which has resident tables too)
       const int wq = perm ? 0 : predict_rowbox_quads(F, x_type, C);
+      const int mr = perm || wq > 0 || order == GNB_ORDER_GROUPED
+                         ? 0
+                         : predict_mixed_rows(F, x_type, C, S);
+      if (mr > 0 && order == GNB_ORDER_AUTO) {
+        // Row order unknown: count the 128-row tiles that mix slots on the
+        // device and launch both kernels gated on that count (the one not
+        // chosen exits at once) -- no host round trip.
+        PredictMaps mmap, gmap;
+        if (!encode_map(&mmap.main, p.x, n, F, ldx, mr, true, x_type) ||
+            !encode_map(&gmap.main, p.x, n, F, ldx, predict_box_rows(C), true, x_type))
+          return fail(GNB_ECUDA, "predict: cuTensorMapEncodeTiled failed");
+        mmap.tail = mmap.main;
+        gmap.tail = gmap.main;
+        int32_t* cnt = gate_counter(stream);
+        if (cnt == nullptr) return fail(GNB_ENOMEM, "predict: gate counter allocation failed");
+        GNB_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t), stream), "memset");
+        GNB_CUDA(tile_mix_launch(p.size, n, width, limit, route, cnt, stream), "tile_mix");
+        PredictParams pm = p, pg = p;
+        pm.mixed_rows = mr;
+        pg.mixed_rows = 0;
+        pm.gate = pg.gate = cnt;
+        pm.gate_tiles = pg.gate_tiles = (n + kMixTileRows - 1) / kMixTileRows;
+        pm.gate_want = 1;
+        pg.gate_want = 0;
+        GNB_CUDA(predict_launch(&mmap, pm, stream, force_generic), "predict launch");
+        GNB_CUDA(predict_launch(&gmap, pg, stream, force_generic), "predict launch");
+        continue;
+      }
       bool ok = wq > 0 ? encode_map(&map.main, p.x, n, F, ldx, kRowBoxRows, false, x_type,
                                     wq * 16 / eb)
-                       : encode_map(&map.main, p.x, n, F, ldx, perm ? 1 : predict_box_rows(C),
-                                    true, x_type);
+                       : encode_map(&map.main, p.x, n, F, ldx,
+                                    perm ? 1 : mr > 0 ? mr : predict_box_rows(C), true, x_type);
       map.tail = map.main;
       if (ok && perm && gather_tail_promo() >= 0)
         ok = encode_map(&map.tail, p.x, n, F, ldx, 1, true, x_type, 0, gather_tail_promo());
       if (!ok) return fail(GNB_ECUDA, "predict: cuTensorMapEncodeTiled failed");
       p.rowbox_quads = wq;
+      p.mixed_rows = mr;
       p.rowbox_contig = wq > 0 && ldx * eb == int64_t(wq) * 16 && rowbox_bulk();
       mp = &map;
     }
@@ -344,6 +398,14 @@ int gnb_fin_train_device(const double* sums, const double* counts, int32_t n_gro
   return GNB_OK;
 }
 
+int32_t gnb_predict_mixed_rows(int32_t n_features, int32_t x_type, int32_t n_classes,
+                               int32_t n_slots) {
+  if (n_features < 1 || n_classes < 2 || n_classes > GNB_MAX_CLASSES || n_slots < 1) return 0;
+  if (x_type != GNB_X_I32 && x_type != GNB_X_U16 && x_type != GNB_X_U8) return 0;
+  if (!mixed_kernel(n_features, x_type, n_classes, n_slots)) return 0;
+  return predict_mixed_rows(n_features, x_type, n_classes, n_slots);
+}
+
 size_t gnb_slot_sort_workspace_bytes(int64_t n_rows, int32_t n_slots) {
   if (n_rows < 0 || n_slots < 1) return 0;
   return slot_sort_workspace(n_rows, n_slots);
@@ -389,7 +451,9 @@ int gnb_predict_mode(const void* x, int32_t x_type, int64_t n_rows, int32_t n_fe
                      int32_t* label_out, double* logpost_out, uintptr_t stream) {
   if (x_type != GNB_X_I32 && x_type != GNB_X_U16 && x_type != GNB_X_U8)
     return fail(GNB_EINVAL, "predict: unknown x_type %d", x_type);
-  if (mode != GNB_MODE_EXACT && mode != GNB_MODE_FMA)
+  const int arith = mode & 0xF, order = mode & ~0xF;
+  if ((arith != GNB_MODE_EXACT && arith != GNB_MODE_FMA) ||
+      (order != GNB_ORDER_AUTO && order != GNB_ORDER_GROUPED && order != GNB_ORDER_MIXED))
     return fail(GNB_EINVAL, "predict: unknown mode %d", mode);
   int rc = check_predict(static_cast<const int32_t*>(x), n_rows, n_features, ldx, size_bytes,
                          group_size_bytes, max_size_bytes, route, n_slots, n_classes, packed,
@@ -956,14 +1020,17 @@ static int predict_host_impl(const void* xv, int x_type, int64_t n_rows, int32_t
     GNB_CUDA(cudaMemcpyAsync(c->size[lane].p, size_bytes + r0, size_t(n) * 4,
                              cudaMemcpyHostToDevice, s),
              "H2D");
-    // Ragged batch not grouped by size group (more than 1 in 8 tiles would mix
-    // models): sort the chunk's rows by slot on the device, score via gather4.
+    // Ragged batch: the host sees the sizes, so it picks the kernel itself.
+    // Rows grouped by size group -> 6-CTA kernel (GNB_ORDER_GROUPED); more than
+    // 1 in 16 tiles mixing models -> the mixed-slot kernel (GNB_ORDER_MIXED),
+    // or, where its tables do not fit in smem, a device slot sort + gather4.
     const int32_t* perm = nullptr;
+    int order = GNB_ORDER_GROUPED;
     if (n_slots > 1) {
       int64_t mixed = 0, tiles = 0;
-      for (int64_t t0 = 0; t0 < n; t0 += 128, ++tiles) {
+      for (int64_t t0 = 0; t0 < n; t0 += kMixTileRows, ++tiles) {
         int first = -2;
-        for (int64_t r = t0; r < std::min<int64_t>(t0 + 128, n); ++r) {
+        for (int64_t r = t0; r < std::min<int64_t>(t0 + kMixTileRows, n); ++r) {
           const int32_t sz = size_bytes[r0 + r];
           if (sz < 0 || sz >= max_size_bytes) continue;
           const int sl = route[sz / group_size_bytes];
@@ -974,21 +1041,25 @@ static int predict_host_impl(const void* xv, int x_type, int64_t n_rows, int32_t
           }
         }
       }
-      if (mixed * 8 > tiles) {
-        GNB_CUDA(c->perm[lane].ensure(size_t(n) * 4), "malloc");
-        GNB_CUDA(c->sortws[lane].ensure(slot_sort_workspace(n, n_slots)), "malloc");
-        GNB_CUDA(slot_sort(static_cast<int32_t*>(c->size[lane].p), n, group_size_bytes,
-                           max_size_bytes, static_cast<int32_t*>(c->route.p), n_slots,
-                           static_cast<int32_t*>(c->perm[lane].p), c->sortws[lane].p, s),
-                 "slot_sort");
-        perm = static_cast<int32_t*>(c->perm[lane].p);
+      if (mixed * 16 > tiles) {
+        if (mixed_kernel(n_features, xt, n_classes, n_slots)) {
+          order = GNB_ORDER_MIXED;
+        } else {
+          GNB_CUDA(c->perm[lane].ensure(size_t(n) * 4), "malloc");
+          GNB_CUDA(c->sortws[lane].ensure(slot_sort_workspace(n, n_slots)), "malloc");
+          GNB_CUDA(slot_sort(static_cast<int32_t*>(c->size[lane].p), n, group_size_bytes,
+                             max_size_bytes, static_cast<int32_t*>(c->route.p), n_slots,
+                             static_cast<int32_t*>(c->perm[lane].p), c->sortws[lane].p, s),
+                   "slot_sort");
+          perm = static_cast<int32_t*>(c->perm[lane].p);
+        }
       }
     }
     rc = predict_device(dx, xt, n, n_features, dld, static_cast<int32_t*>(c->size[lane].p),
                         group_size_bytes, max_size_bytes, static_cast<int32_t*>(c->route.p),
                         n_slots, n_classes, c->packed.p, static_cast<int32_t*>(c->label[lane].p),
                         logpost_out ? static_cast<double*>(c->logpost[lane].p) : nullptr, s, 0,
-                        perm);
+                        perm, GNB_MODE_EXACT | order);
     if (rc) return rc;
     GNB_CUDA(cudaMemcpyAsync(label_out + r0, c->label[lane].p, size_t(n) * 4,
                              cudaMemcpyDeviceToHost, s),

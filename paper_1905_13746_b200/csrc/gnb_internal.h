@@ -44,6 +44,14 @@ struct PredictParams {
   int32_t rowbox_contig; // row box: HBM row pitch == smem row pitch -> 1-D bulk tile copy
   int32_t rowbox_resident; // row box: all slot tables resident in smem, set by predict_launch
   int32_t mode;          // GNB_MODE_EXACT (reference roundings) or GNB_MODE_FMA
+  int32_t mixed_rows;    // > 0: mixed-slot mode (resident tables, in-tile slot sort), tile rows
+  int32_t mixed_stages;  // mixed-slot ring depth, set by predict_launch
+  int32_t dep_zero;      // always 0: an opaque zero for data dependencies in SASS
+  // device-side kernel gate (GNB_ORDER_AUTO): *gate = number of 128-row tiles
+  // that mix slots; a gated kernel runs iff (*gate * 16 > gate_tiles) == gate_want
+  const int32_t* gate;
+  int64_t gate_tiles;
+  int32_t gate_want;
 };
 
 struct FitParams {
@@ -74,6 +82,14 @@ int predict_box_rows(int n_classes);  // TMA box height of the K-PRED variant
 // Row-box mode (short rows): quads per box row, 0 when the shape does not use it.
 // The box is then {quads * 16 / elem_bytes columns, kRowBoxRows rows}, no swizzle.
 int predict_rowbox_quads(int n_features, int x_type, int n_classes);
+// Mixed-slot mode (rows of many slots interleaved, every slot's table resident
+// in smem): tile rows (= TMA box height), 0 when the shape does not use it.
+// Batches in any row order then need no device slot sort.
+int predict_mixed_rows(int n_features, int x_type, int n_classes, int n_slots);
+// *count += number of 128-row tiles whose in-range rows route to more than one slot
+cudaError_t tile_mix_launch(const int32_t* size, int64_t n, int width, int limit,
+                            const int32_t* route, int32_t* count, cudaStream_t stream);
+constexpr int kMixTileRows = 128;
 constexpr int kRowBoxRows = 128;
 // K-PRED tensor maps: `main` for every chunk; `tail` for the last chunk of a
 // row in gather mode (encoded without L2 promotion, so a random row's last

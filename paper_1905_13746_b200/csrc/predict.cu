@@ -24,6 +24,8 @@
 //     once, coalesced.
 //
 // Kernels: predict_kernels.cuh.  This unit: table packing and the dispatch.
+#include <climits>
+
 #include "predict_kernels.cuh"
 
 namespace gnb {
@@ -92,6 +94,60 @@ int predict_rowbox_quads(int n_features, int x_type, int n_classes) {
   const int wq = nq | 1;
   if (wq > kRowBoxMaxQuads || wq * 16 / eb > 256) return 0;
   return wq;
+}
+
+// GNB_PRED_MIXED: 0 never, 1 (default) batches of >= 2 slots, 2 also one slot (A/B).
+int predict_mixed_rows(int n_features, int x_type, int n_classes, int n_slots) {
+  static const int mode = [] {  // read once (thread-safe static init)
+    const char* e = getenv("GNB_PRED_MIXED");
+    return e ? atoi(e) : 1;
+  }();
+  if (mode == 0 || class_pad(n_classes) != 2 || n_features < 1) return 0;
+  if (n_slots < (mode == 2 ? 1 : 2)) return 0;
+  const int eb = x_type == GNB_X_U8 ? 1 : x_type == GNB_X_U16 ? 2 : 4;
+  return mixed_stages_fit(n_features, eb, n_slots) > 0 ? kMixedNW * 32 : 0;
+}
+
+// One warp per 128-row tile (grid-strided): min/max routed slot of the tile's
+// in-range rows, one atomic per mixed tile.  Reads the 4-B sizes only.
+__global__ void __launch_bounds__(256) tile_mix_kernel(const int32_t* __restrict__ size,
+                                                       int64_t n, int width, int limit,
+                                                       const int32_t* __restrict__ route,
+                                                       int32_t* __restrict__ count) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+  const int64_t tiles = (n + kMixTileRows - 1) / kMixTileRows;
+  int mixed = 0;
+  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x >> 5) + (threadIdx.x >> 5);
+       t < tiles; t += warps) {
+    int lo = INT_MAX, hi = INT_MIN;
+#pragma unroll
+    for (int i = 0; i < kMixTileRows / 32; ++i) {
+      const int64_t r = t * kMixTileRows + lane + 32 * i;
+      if (r < n) {
+        const int sz = __ldg(size + r);
+        if (sz >= 0 && sz < limit) {
+          const int s = __ldg(route + sz / width);
+          lo = min(lo, s);
+          hi = max(hi, s);
+        }
+      }
+    }
+    lo = __reduce_min_sync(0xffffffffu, lo);
+    hi = __reduce_max_sync(0xffffffffu, hi);
+    mixed += lo < hi;
+  }
+  if (lane == 0 && mixed) atomicAdd(count, mixed);
+}
+
+cudaError_t tile_mix_launch(const int32_t* size, int64_t n, int width, int limit,
+                            const int32_t* route, int32_t* count, cudaStream_t stream) {
+  const int64_t tiles = (n + kMixTileRows - 1) / kMixTileRows;
+  const int64_t blocks64 = (tiles + 7) / 8;
+  const int blocks = static_cast<int>(blocks64 < 148 * 8 ? blocks64 : 148 * 8);
+  if (blocks == 0) return cudaSuccess;
+  tile_mix_kernel<<<blocks, 256, 0, stream>>>(size, n, width, limit, route, count);
+  return cudaGetLastError();
 }
 
 int predict_box_rows(int n_classes) {

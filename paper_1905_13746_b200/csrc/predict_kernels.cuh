@@ -189,6 +189,14 @@ __device__ __forceinline__ void write_row(const PredictParams& p, int64_t r, int
   }
 }
 
+// Device-side kernel gate (GNB_ORDER_AUTO): both K-PRED kernels are launched
+// and the one not chosen by the tile-mix count exits at once.
+__device__ __forceinline__ bool gated_off(const PredictParams& p) {
+  if (p.gate == nullptr) return false;
+  const bool mixed = static_cast<int64_t>(__ldg(p.gate)) * 16 > p.gate_tiles;
+  return mixed != (p.gate_want != 0);
+}
+
 // ------------------------------------------------------------------ TMA kernel
 // A consumer thread owns R rows of the tile (rows lane + 32*(w + NW*i)), so one
 // broadcast table read feeds R*CP independent accumulator chains.
@@ -289,6 +297,7 @@ __device__ __forceinline__ void score_chunk_mixed(const PredictParams& p, double
 template <int CP, typename T, int R, int NW, int STAGES, bool GATHER, int B, bool FMA>
 __global__ void __launch_bounds__((NW + 1) * 32)
     predict_tma_kernel(const __grid_constant__ PredictMaps maps, const PredictParams p) {
+  if (gated_off(p)) return;
   const CUtensorMap& xmap = maps.main;
   using L = PredictSmem<CP, T, R, NW, STAGES, GATHER, B>;
   constexpr int ROWS = L::kRows;
@@ -697,11 +706,17 @@ __global__ void __launch_bounds__(5 * 32, MINB)
         if (early) {
           // row -> registers, release the stage, then score from registers
           uint4 v[RQ];
+          uint32_t f = 0;
 #pragma unroll
           for (int q = 0; q < RQ; ++q)
             if (q < nq) v[q] = *reinterpret_cast<const uint4*>(xrow + 16 * q);
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&empty[stage]);
+#pragma unroll
+          for (int q = 0; q < RQ; ++q)
+            if (q < nq) f |= v[q].x;
+          // the release waits for every lane's loads (see predict_mixed_kernel)
+          const uint32_t dep =
+              __ballot_sync(0xffffffffu, f != 0u) & static_cast<uint32_t>(p.dep_zero);
+          if (lane == 0) mbar_arrive(&empty[stage] + dep);
           released = true;
           const double* st = res + s * static_cast<int>(L.res_stride);
 #pragma unroll
@@ -762,6 +777,298 @@ __global__ void __launch_bounds__(5 * 32, MINB)
       }
       const int64_t r = tile * ROWS + row;
       if (r < p.n_rows) write_row<CP>(p, r, slot, neg, acc);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ mixed-slot kernel
+// Rows of many size groups interleaved (a ragged batch in any order, e.g. the
+// reference's per-file scoring of a shuffled corpus, engine.py:198-202): every
+// slot's [prior | table] is resident in smem once per CTA, X streams in FILE
+// order through the same 128-B 2-D TMA boxes as the kernel above (no device
+// slot sort, no gather, every byte read once in order), and the producer
+// counting-sorts each tile's rows by routed slot (stable, match_any leaders +
+// smem histogram) so consumer lane t scores row rid[t]: lanes of one slot read
+// the same table entry (broadcast), lanes of neighbouring slots hit distinct
+// bank groups (slot stride = an odd number of 16-B units at CP = 2).
+// A consumer thread keeps its row's chunks in registers one step AHEAD: it
+// waits for chunk k+1, copies its 8 quads to registers and releases that stage
+// before scoring chunk k, so every stage of the ring is in flight except for
+// the few cycles between a TMA completion and the consumers' LDS.  1 CTA per SM
+// (the tables take most of the shared memory); same arithmetic, same order.
+struct MixSmem {
+  uint32_t x_bytes, tab_feats, stride, hdr_bytes, n_hdr, x, res, hdr, sizes, hist, bar, total;
+  __host__ __device__ MixSmem(int rows, int F, int eq, int cf, int stages, int ahead, int slots) {
+    const int nch = (F + cf - 1) / cf;
+    x_bytes = static_cast<uint32_t>(rows) * kChunkBytesPerRow;
+    tab_feats = static_cast<uint32_t>((F + eq - 1) / eq * eq);  // features read per slot
+    stride = 2u * (1u + tab_feats);  // doubles per slot (CP = 2): odd number of 16-B units
+    hdr_bytes = static_cast<uint32_t>(rows) * 8;  // slot[rows] | rid[rows]
+    // header ring: the producer can be at most ceil(stages / nch) tiles ahead
+    // of the consumers' header reads (a tile's header is read before its first
+    // stage is released)
+    n_hdr = static_cast<uint32_t>((stages + nch - 1) / nch);
+    x = 0;  // 1024-B aligned (SWIZZLE_128B)
+    res = x + stages * x_bytes;
+    hdr = res + (static_cast<uint32_t>(slots) * stride * 8 + 15) / 16 * 16;
+    sizes = hdr + n_hdr * hdr_bytes;
+    hist = sizes + ahead * rows * 4;
+    bar = (hist + (slots + 1) * 4 + 7) / 8 * 8;
+    total = bar + 2 * stages * 8;
+  }
+};
+
+template <typename T, int NW, int AHEAD, bool FMA>
+__global__ void __launch_bounds__((NW + 1) * 32, 1)
+    predict_mixed_kernel(const __grid_constant__ PredictMaps maps, const PredictParams p) {
+  constexpr int CP = 2, ROWS = NW * 32, CF = Elem<T>::kPerRow, EQ = Elem<T>::kPerQuad;
+  constexpr int QPC = kChunkBytesPerRow / 16;  // quads per chunk row
+  static_assert(ROWS <= 256, "TMA box rows <= 256");
+  if (gated_off(p)) return;
+  const CUtensorMap& xmap = maps.main;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  const int ST = p.mixed_stages, NCH = p.n_chunks, S = p.n_slots;
+  const MixSmem L(ROWS, p.n_features, EQ, CF, ST, AHEAD, S);
+  const int HD = static_cast<int>(L.n_hdr);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.bar);
+  uint64_t* empty = full + ST;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t n_tiles = p.n_tiles;
+  // Prologue (as the row-box kernel): the producer initialises the barriers and
+  // starts streaming; the consumers copy the resident tables meanwhile.
+  if (warp == NW) {
+    if (lane == 0) {
+      for (int s = 0; s < ST; ++s) {
+        mbar_init(&full[s], 32);
+        mbar_init(&empty[s], NW);
+      }
+      mbar_fence_init();
+      prefetch_tensormap(&xmap);
+    }
+    __syncwarp();
+    named_bar_arrive(1, (NW + 1) * 32);
+  } else {
+    const int64_t slot_tab = static_cast<int64_t>(p.n_tab_blocks) * kTabBlockFeatures * CP;
+    double* res = reinterpret_cast<double*>(smem + L.res);
+    const int stride = static_cast<int>(L.stride);
+    for (int i = threadIdx.x; i < S * stride; i += NW * 32) {
+      const int s = i / stride, k = i - s * stride;
+      res[i] = k < CP ? __ldg(p.prior + s * CP + k) : __ldg(p.tab + s * slot_tab + (k - CP));
+    }
+    named_bar_sync(1, (NW + 1) * 32);
+  }
+
+  if (warp == NW) {
+    // ---------------------------------------------------------- producer
+    const uint64_t pol_x = p.x_policy == 1 ? policy_evict_first() : policy_evict_normal();
+    int* szr = reinterpret_cast<int*>(smem + L.sizes);
+    int* hist = reinterpret_cast<int*>(smem + L.hist);
+    const uint32_t lt_mask = (1u << lane) - 1u;
+    auto fetch_sizes = [&](int64_t tile, int k) {
+      if (tile < n_tiles) {
+#pragma unroll
+        for (int i = 0; i < ROWS / 32; ++i) {
+          const int64_t r = tile * ROWS + lane + 32 * i;
+          cp_async4(szr + k * ROWS + lane + 32 * i, p.size + (r < p.n_rows ? r : p.n_rows - 1));
+        }
+      }
+      cp_async_commit();
+    };
+#pragma unroll
+    for (int k = 0; k < AHEAD; ++k) fetch_sizes(blockIdx.x + int64_t(k) * gridDim.x, k);
+    int k_cur = 0, stage = 0, h = 0;
+    uint32_t phase = 0;
+    for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+      const int64_t r0 = tile * ROWS;
+      for (int sc = 0; sc < NCH; ++sc) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        if (lane == 0) {  // X first: it does not depend on routing
+          mbar_expect_tx(&full[stage], L.x_bytes);
+          tma_load_2d(smem + L.x + stage * L.x_bytes, &xmap, sc * CF, static_cast<int32_t>(r0),
+                      &full[stage], pol_x);
+        }
+        if (sc == 0) {
+          // route the tile (size -> group -> slot; key 0 = out of range)
+          int key[ROWS / 32], rank[ROWS / 32];
+          cp_async_wait<AHEAD - 1>();
+#pragma unroll
+          for (int i = 0; i < ROWS / 32; ++i) {
+            const int64_t r = r0 + lane + 32 * i;
+            const int sz = szr[k_cur * ROWS + lane + 32 * i];
+            key[i] = (r < p.n_rows && sz >= 0 && sz < p.limit) ? __ldg(p.route + sz / p.width) + 1
+                                                               : 0;
+          }
+          fetch_sizes(tile + int64_t(AHEAD) * gridDim.x, k_cur);
+          if (++k_cur == AHEAD) k_cur = 0;
+          // stable counting sort by key: ranks within a key in row order
+          for (int b = lane; b <= S; b += 32) hist[b] = 0;
+          __syncwarp();
+#pragma unroll
+          for (int i = 0; i < ROWS / 32; ++i) {
+            const uint32_t peers = __match_any_sync(0xffffffffu, key[i]);
+            const int leader = __ffs(peers) - 1;
+            int base = 0;
+            if (lane == leader) base = atomicAdd(&hist[key[i]], __popc(peers));
+            base = __shfl_sync(0xffffffffu, base, leader);
+            rank[i] = base + __popc(peers & lt_mask);
+          }
+          __syncwarp();
+          int carry = 0;  // exclusive scan of the histogram
+          for (int b0 = 0; b0 <= S; b0 += 32) {
+            const int b = b0 + lane;
+            const int v = b <= S ? hist[b] : 0;
+            int inc = v;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+              const int t = __shfl_up_sync(0xffffffffu, inc, d);
+              if (lane >= d) inc += t;
+            }
+            if (b <= S) hist[b] = carry + inc - v;
+            carry += __shfl_sync(0xffffffffu, inc, 31);
+          }
+          __syncwarp();
+          int* hs = reinterpret_cast<int*>(smem + L.hdr + h * L.hdr_bytes);
+#pragma unroll
+          for (int i = 0; i < ROWS / 32; ++i) {
+            const int pos = hist[key[i]] + rank[i];
+            hs[pos] = key[i] - 1;
+            hs[ROWS + pos] = lane + 32 * i;
+          }
+          if (++h == HD) h = 0;
+          __syncwarp();
+        }
+        mbar_arrive(&full[stage]);
+        if (++stage == ST) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else {
+    // ---------------------------------------------------------- consumers
+    const int t = lane + 32 * warp;
+    const double* res = reinterpret_cast<const double*>(smem + L.res);
+    const int stride = static_cast<int>(L.stride);
+    int stage = 0, h = 0;
+    uint32_t phase = 0;
+    // (tile, sc) of the step whose quads are in registers / being fetched
+    int64_t tile = blockIdx.x;
+    int sc = 0;
+    // fetch step (tile, sc): its header (first chunk of a tile), its quads
+    // into registers, then release the stage.  The release must not overtake
+    // the loads: SYNCS.ARRIVE carries no scoreboard wait on earlier LDS, and
+    // with the shared-memory pipe busy (bank conflicts of shuffled rows) a TMA
+    // refill of the released stage was seen to land before the loads read it.
+    // So every lane folds one word of each loaded quad (int32: all four, the
+    // negative-count flag) and the warp's ballot of that fold feeds the
+    // arrive's address (+ (ballot & dep_zero), an opaque zero): the arrive
+    // issues only after every lane's loads have returned.
+    auto fetch = [&](uint4 (&v)[QPC], int fsc, int& slot, int& rid, uint32_t& fold) {
+      mbar_wait(&full[stage], phase);
+      if (fsc == 0) {
+        const int* hs = reinterpret_cast<const int*>(smem + L.hdr + h * L.hdr_bytes);
+        slot = hs[t];
+        rid = hs[ROWS + t];
+        if (++h == HD) h = 0;
+      }
+      const int nq = (min(CF, p.n_features - fsc * CF) + EQ - 1) / EQ;
+      const uint8_t* box = smem + L.x + stage * L.x_bytes;
+      uint32_t f = 0;
+      if (nq == QPC) {
+#pragma unroll
+        for (int q = 0; q < QPC; ++q) v[q] = *reinterpret_cast<const uint4*>(box + swz128(rid, q));
+#pragma unroll
+        for (int q = 0; q < QPC; ++q)
+          f |= Elem<T>::kSigned ? (v[q].x | v[q].y | v[q].z | v[q].w) : v[q].x;
+      } else {
+#pragma unroll
+        for (int q = 0; q < QPC; ++q)
+          if (q < nq) v[q] = *reinterpret_cast<const uint4*>(box + swz128(rid, q));
+#pragma unroll
+        for (int q = 0; q < QPC; ++q)
+          if (q < nq) f |= Elem<T>::kSigned ? (v[q].x | v[q].y | v[q].z | v[q].w) : v[q].x;
+      }
+      fold = f;
+      const uint32_t dep = __ballot_sync(0xffffffffu, f != 0u) & static_cast<uint32_t>(p.dep_zero);
+      if (lane == 0) mbar_arrive(&empty[stage] + dep);
+      if (++stage == ST) {
+        stage = 0;
+        phase ^= 1;
+      }
+    };
+    double acc[CP] = {0.0, 0.0};
+    uint32_t neg = 0;
+    auto score_quad2 = [&](const uint4& vq, const double* tq) {
+#pragma unroll
+      for (int e = 0; e < EQ; ++e) {
+        const double xd = converted<T, FMA>(vq, e);
+        const double2 t2 = *reinterpret_cast<const double2*>(tq + e * CP);
+        acc[0] = madd<FMA>(acc[0], xd, t2.x);
+        acc[1] = madd<FMA>(acc[1], xd, t2.y);
+      }
+    };
+    // score step (tile, sc) from registers; the last chunk writes the row
+    auto score = [&](const uint4 (&v)[QPC], int ssc, int slot, int rid, int64_t stile,
+                     uint32_t fold) {
+      const double* st = res + max(slot, 0) * stride;
+      if (ssc == 0) {
+        acc[0] = st[0];
+        acc[1] = st[1];
+        neg = 0;
+      }
+      if (Elem<T>::kSigned) neg |= fold;
+      const int nq = (min(CF, p.n_features - ssc * CF) + EQ - 1) / EQ;
+      const double* tab = st + CP + ssc * CF * CP;
+      if (nq == QPC) {
+#pragma unroll
+        for (int q = 0; q < QPC; ++q) score_quad2(v[q], tab + EQ * q * CP);
+      } else {
+#pragma unroll
+        for (int q = 0; q < QPC; ++q)
+          if (q < nq) score_quad2(v[q], tab + EQ * q * CP);
+      }
+      if (ssc == NCH - 1) {
+        const int64_t r = stile * ROWS + rid;
+        if (r < p.n_rows) write_row<CP>(p, r, slot, neg, acc);
+      }
+    };
+    if (tile < n_tiles) {
+      uint4 va[QPC], vb[QPC];
+      int slot_a = -1, rid_a = 0, slot_b = -1, rid_b = 0;
+      uint32_t fa = 0, fb = 0;
+      fetch(va, 0, slot_a, rid_a, fa);
+      // ping-pong between two register sets (no copies): A scored while B
+      // holds the next step, then the roles swap
+      for (;;) {
+        int nsc = sc + 1;
+        int64_t ntile = tile;
+        if (nsc == NCH) {
+          nsc = 0;
+          ntile += gridDim.x;
+        }
+        const bool more = ntile < n_tiles;
+        slot_b = nsc == 0 ? -1 : slot_a;
+        rid_b = nsc == 0 ? 0 : rid_a;
+        if (more) fetch(vb, nsc, slot_b, rid_b, fb);
+        score(va, sc, slot_a, rid_a, tile, fa);
+        if (!more) break;
+        sc = nsc;
+        tile = ntile;
+        nsc = sc + 1;
+        if (nsc == NCH) {
+          nsc = 0;
+          ntile += gridDim.x;
+        }
+        const bool more2 = ntile < n_tiles;
+        slot_a = nsc == 0 ? -1 : slot_b;
+        rid_a = nsc == 0 ? 0 : rid_b;
+        if (more2) fetch(va, nsc, slot_a, rid_a, fa);
+        score(vb, sc, slot_b, rid_b, tile, fb);
+        if (!more2) break;
+        sc = nsc;
+        tile = ntile;
+      }
     }
   }
 }
@@ -965,6 +1272,44 @@ static cudaError_t launch_rowbox(const PredictMaps& map, const PredictParams& p,
   return launch_rowbox_a<CP, T, 2, FMA>(map, p, stream);
 }
 
+// Mixed-slot mode: consumer warps per CTA (tile rows = 32 * NW), ring depth =
+// as many 128-B-box stages as fit next to the resident tables (<= 8).
+inline constexpr int kMixedNW = 8;
+inline constexpr int kMixedAhead = 2;
+inline constexpr int kMixedMinStages = 3;
+inline int mixed_stages_fit(int F, int eb, int S) {
+  const int cf = kChunkBytesPerRow / eb, eq = 16 / eb;
+  for (int st = 8; st >= kMixedMinStages; --st)
+    if (MixSmem(kMixedNW * 32, F, eq, cf, st, kMixedAhead, S).total + 1024 <= 227u * 1024u)
+      return st;
+  return 0;
+}
+
+template <typename T, bool FMA>
+static cudaError_t launch_mixed(const PredictMaps& map, PredictParams p, cudaStream_t stream) {
+  constexpr auto kern = predict_mixed_kernel<T, kMixedNW, kMixedAhead, FMA>;
+  constexpr int ROWS = kMixedNW * 32;
+  int sms = 0;
+  cudaError_t e = kernel_prepare<kern>(&sms);
+  if (e != cudaSuccess) return e;
+  p.n_tiles = (p.n_rows + ROWS - 1) / ROWS;
+  p.n_chunks = (p.n_features + Elem<T>::kPerRow - 1) / Elem<T>::kPerRow;
+  p.dep_zero = 0;
+  p.mixed_stages = mixed_stages_fit(p.n_features, static_cast<int>(sizeof(T)), p.n_slots);
+  static const int st_env = [] {  // GNB_MIXED_STAGES: fewer stages (A/B probes only)
+    const char* e = getenv("GNB_MIXED_STAGES");
+    return e ? atoi(e) : 0;
+  }();
+  if (st_env >= 2 && st_env < p.mixed_stages) p.mixed_stages = st_env;
+  if (p.mixed_stages < kMixedMinStages) return cudaErrorInvalidConfiguration;
+  const MixSmem L(ROWS, p.n_features, Elem<T>::kPerQuad, Elem<T>::kPerRow, p.mixed_stages,
+                  kMixedAhead, p.n_slots);
+  const int grid = static_cast<int>(p.n_tiles < sms ? p.n_tiles : sms);
+  if (grid == 0) return cudaSuccess;
+  kern<<<grid, (kMixedNW + 1) * 32, L.total + 1024, stream>>>(map, p);
+  return cudaGetLastError();
+}
+
 template <int CP, typename T, bool FMA>
 static cudaError_t launch_generic(const PredictParams& p, cudaStream_t stream) {
   const int64_t blocks64 = (p.n_rows + 255) / 256;
@@ -998,6 +1343,8 @@ inline int cp2_variant() {
 template <typename T, bool FMA>
 cudaError_t launch_typed(const PredictMaps* map, const PredictParams& p, int CP,
                          cudaStream_t stream) {
+  if (map != nullptr && p.mixed_rows > 0 && p.perm == nullptr && CP == 2)
+    return launch_mixed<T, FMA>(*map, p, stream);
   if (map != nullptr && p.rowbox_quads > 0 && p.perm == nullptr) {
     switch (CP) {
       case 2: return launch_rowbox<2, T, FMA>(*map, p, stream);

@@ -36,6 +36,7 @@ def _dev(t: torch.Tensor, name: str, dtype) -> int:
 
 
 _X_TYPES = {torch.int32: N.X_I32, torch.uint16: N.X_U16, torch.uint8: N.X_U8}
+_ORDERS = {"auto": N.GNB_ORDER_AUTO, "grouped": N.GNB_ORDER_GROUPED, "mixed": N.GNB_ORDER_MIXED}
 
 
 def _rows(x: torch.Tensor, name: str = "x", dtypes=(torch.int32,)):
@@ -96,6 +97,17 @@ class DeviceTables:
         return cls(rt, packed, S, Cn, F, group_size_bytes, max_size_bytes)
 
 
+def needs_slot_sort(x_dtype: torch.dtype, tables: DeviceTables) -> bool:
+    """True when a ragged batch in arbitrary row order should go through
+    slot_sort + predict(perm=...): K-PRED's mixed-slot kernel (every slot's table
+    resident in shared memory, rows sorted by slot inside each tile) scores any
+    row order at streaming speed whenever gnb_predict_mixed_rows() > 0."""
+    if tables.n_slots < 2:
+        return False
+    return N.lib.gnb_predict_mixed_rows(tables.n_features, _X_TYPES[x_dtype],
+                                        tables.n_classes, tables.n_slots) == 0
+
+
 def slot_sort(size_bytes: torch.Tensor, tables: DeviceTables, *, stream=None) -> torch.Tensor:
     """perm[n]: row indices grouped by routed model slot (device counting sort)."""
     n = size_bytes.shape[0]
@@ -112,7 +124,8 @@ def slot_sort(size_bytes: torch.Tensor, tables: DeviceTables, *, stream=None) ->
 
 def predict(x: torch.Tensor, size_bytes: torch.Tensor, tables: DeviceTables, *,
             logpost: bool = True, label_out=None, logpost_out=None, stream=None,
-            generic: bool = False, perm: torch.Tensor | None = None, mode: str = "exact"):
+            generic: bool = False, perm: torch.Tensor | None = None, mode: str = "exact",
+            order: str = "auto"):
     """Score every row: label[N] int32 (class index, or -1 size out of range,
     -2 negative count) and, if requested, log-posteriors [N, C] fp64.
 
@@ -122,9 +135,15 @@ def predict(x: torch.Tensor, size_bytes: torch.Tensor, tables: DeviceTables, *,
     perm (from slot_sort): score in slot-grouped order -- for ragged batches
     whose rows are not grouped by size group; results are identical.
     mode: "exact" (default; the reference's mul-then-add roundings, bit-identical
-    log-posteriors) or "fma" (one fused rounding per term, ~1e-12 relative)."""
+    log-posteriors) or "fma" (one fused rounding per term, ~1e-12 relative).
+    order: "auto" (default: the device counts the tiles that mix models and picks
+    the kernel, no host sync), "grouped" (rows grouped by size group) or "mixed"
+    (rows in any order: the mixed-slot kernel) -- a speed hint; results are
+    identical."""
     if mode not in ("exact", "fma"):
         raise InvalidConfigError(f"mode must be 'exact' or 'fma', got {mode!r}")
+    if order not in _ORDERS:
+        raise InvalidConfigError(f"order must be one of {sorted(_ORDERS)}, got {order!r}")
     xp, n, F, ldx = _rows(x, dtypes=tuple(_X_TYPES))
     if F != tables.n_features:
         raise InvalidConfigError(f"x has {F} columns, tables have {tables.n_features} features")
@@ -139,10 +158,11 @@ def predict(x: torch.Tensor, size_bytes: torch.Tensor, tables: DeviceTables, *,
             tables.route.data_ptr(), tables.n_slots, tables.n_classes, tables.packed.data_ptr(),
             _vec(label, n, "label_out"), lp.data_ptr() if lp is not None else None,
             _stream(stream))
-    if mode == "fma":
+    if mode == "fma" or order != "auto":
         pp = _vec(perm, n, "perm") if perm is not None else None
         a = list(args)
-        a[10:10] = [pp, N.GNB_MODE_FMA]   # after packed
+        flags = (N.GNB_MODE_FMA if mode == "fma" else N.GNB_MODE_EXACT) | _ORDERS[order]
+        a[10:10] = [pp, flags]   # after packed
         N.check(N.lib.gnb_predict_mode(xp, _X_TYPES[x.dtype], *a), "gnb_predict_mode")
     elif generic:
         if x.dtype != torch.int32:
