@@ -899,10 +899,21 @@ def run_sweep(args, world, rank, local):
                                 fin.log_lik[:1, :, :nf], width=5120, limit=5120, threads=8)
         exact = bool(np.array_equal(label[idx].cpu().numpy(), want) and
                      lp[idx].cpu().numpy().tobytes() == wlp.tobytes())
+        # the same byte count through a plain device copy (half read, half
+        # written) timed identically (flush, sleep, events): what ONE isolated
+        # launch of this size can reach at all (launch + ramp + wave tail)
+        half = n * bps // 2 // 4
+        src = torch.ones(half, dtype=torch.int32, device=dev)
+        dst = torch.empty_like(src)
+        copy_ms, _ = _timed_launches(lambda: dst.copy_(src), args.steps, max(args.warmup, 3))
+        del src, dst
         rows.append({"F": nf, "ldx": int(x.stride(0)), "ms": round(mean_ms, 4),
                      "samples_per_s": round(n / (mean_ms / 1e3), 1),
                      "achieved_gbs": round(n * bps / (mean_ms / 1e3) / 1e9, 1),
                      "frac": round(n * bps / (mean_ms / 1e3) / 1e9 / peak, 4),
+                     "copy_same_bytes": {"ms": round(copy_ms, 4),
+                                         "frac": round(n * bps / (copy_ms / 1e3) / 1e9 / peak, 4)},
+                     "frac_of_copy": round(copy_ms / mean_ms, 4),
                      "bit_exact_subsample_vs_oracle": exact})
         del x, size, lab, label, lp
     return {"metric": METRIC, "workload": "cfg2: F sweep at 1M samples, 2 classes, L2 flushed "

@@ -203,9 +203,10 @@ static bool rowbox_bulk() {
   return v != 0;
 }
 
-// The 4-byte tile-mix counter of GNB_ORDER_AUTO, one per (device, stream):
-// reuse on the same stream is stream-ordered (memset -> count -> gated
-// kernels), different streams never share one.  Allocated once, never freed.
+// The tile-mix gate of GNB_ORDER_AUTO ([count, done, decision] ints), one per
+// (device, stream): reuse on the same stream is stream-ordered (count ->
+// decision -> gated kernels; the counting kernel leaves the counters at 0),
+// different streams never share one.  Allocated and zeroed once, never freed.
 static int32_t* gate_counter(cudaStream_t stream) {
   static std::mutex mu;
   static std::map<std::pair<int, uintptr_t>, int32_t*> counters;
@@ -213,8 +214,13 @@ static int32_t* gate_counter(cudaStream_t stream) {
   if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
   std::lock_guard<std::mutex> lock(mu);
   int32_t*& c = counters[{dev, reinterpret_cast<uintptr_t>(stream)}];
-  if (c == nullptr && cudaMalloc(reinterpret_cast<void**>(&c), sizeof(int32_t)) != cudaSuccess)
-    c = nullptr;
+  if (c == nullptr) {
+    if (cudaMalloc(reinterpret_cast<void**>(&c), 4 * sizeof(int32_t)) != cudaSuccess) return c = nullptr;
+    if (cudaMemset(c, 0, 4 * sizeof(int32_t)) != cudaSuccess) {
+      cudaFree(c);
+      return c = nullptr;
+    }
+  }
   return c;
 }
 
@@ -277,13 +283,11 @@ static int predict_device(const void* x, int x_type, int64_t n_rows, int32_t F, 
         gmap.tail = gmap.main;
         int32_t* cnt = gate_counter(stream);
         if (cnt == nullptr) return fail(GNB_ENOMEM, "predict: gate counter allocation failed");
-        GNB_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t), stream), "memset");
         GNB_CUDA(tile_mix_launch(p.size, n, width, limit, route, cnt, stream), "tile_mix");
         PredictParams pm = p, pg = p;
         pm.mixed_rows = mr;
         pg.mixed_rows = 0;
-        pm.gate = pg.gate = cnt;
-        pm.gate_tiles = pg.gate_tiles = (n + kMixTileRows - 1) / kMixTileRows;
+        pm.gate = pg.gate = cnt + 2;
         pm.gate_want = 1;
         pg.gate_want = 0;
         GNB_CUDA(predict_launch(&mmap, pm, stream, force_generic), "predict launch");

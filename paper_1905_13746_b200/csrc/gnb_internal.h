@@ -47,10 +47,10 @@ struct PredictParams {
   int32_t mixed_rows;    // > 0: mixed-slot mode (resident tables, in-tile slot sort), tile rows
   int32_t mixed_stages;  // mixed-slot ring depth, set by predict_launch
   int32_t dep_zero;      // always 0: an opaque zero for data dependencies in SASS
-  // device-side kernel gate (GNB_ORDER_AUTO): *gate = number of 128-row tiles
-  // that mix slots; a gated kernel runs iff (*gate * 16 > gate_tiles) == gate_want
+  // device-side kernel gate (GNB_ORDER_AUTO): *gate = 1 when more than 1 in 16
+  // of the 128-row tiles mix slots (tile_mix_launch); a gated kernel runs iff
+  // *gate == gate_want
   const int32_t* gate;
-  int64_t gate_tiles;
   int32_t gate_want;
 };
 
@@ -86,9 +86,11 @@ int predict_rowbox_quads(int n_features, int x_type, int n_classes);
 // in smem): tile rows (= TMA box height), 0 when the shape does not use it.
 // Batches in any row order then need no device slot sort.
 int predict_mixed_rows(int n_features, int x_type, int n_classes, int n_slots);
-// *count += number of 128-row tiles whose in-range rows route to more than one slot
+// gate[2] = 1 when more than 1 in 16 of the 128-row tiles route their in-range
+// rows to more than one slot, else 0.  gate[0..1] are scratch counters that
+// must be 0 on entry and are 0 again on exit.
 cudaError_t tile_mix_launch(const int32_t* size, int64_t n, int width, int limit,
-                            const int32_t* route, int32_t* count, cudaStream_t stream);
+                            const int32_t* route, int32_t* gate, cudaStream_t stream);
 constexpr int kMixTileRows = 128;
 constexpr int kRowBoxRows = 128;
 // K-PRED tensor maps: `main` for every chunk; `tail` for the last chunk of a

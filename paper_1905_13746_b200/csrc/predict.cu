@@ -109,11 +109,13 @@ int predict_mixed_rows(int n_features, int x_type, int n_classes, int n_slots) {
 }
 
 // One warp per 128-row tile (grid-strided): min/max routed slot of the tile's
-// in-range rows, one atomic per mixed tile.  Reads the 4-B sizes only.
+// in-range rows; one atomic per warp.  The last block to finish writes the
+// decision gate[2] = (mixed tiles * 16 > tiles) and resets gate[0..1], so the
+// counter needs no memset per call (zeroed once when it is allocated).
 __global__ void __launch_bounds__(256) tile_mix_kernel(const int32_t* __restrict__ size,
                                                        int64_t n, int width, int limit,
                                                        const int32_t* __restrict__ route,
-                                                       int32_t* __restrict__ count) {
+                                                       int32_t* __restrict__ gate) {
   const int lane = threadIdx.x & 31;
   const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
   const int64_t tiles = (n + kMixTileRows - 1) / kMixTileRows;
@@ -137,16 +139,27 @@ __global__ void __launch_bounds__(256) tile_mix_kernel(const int32_t* __restrict
     hi = __reduce_max_sync(0xffffffffu, hi);
     mixed += lo < hi;
   }
-  if (lane == 0 && mixed) atomicAdd(count, mixed);
+  if (lane == 0 && mixed) atomicAdd(&gate[0], mixed);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(&gate[1], 1) == static_cast<int>(gridDim.x) - 1) {  // last block
+      const int total = atomicAdd(&gate[0], 0);
+      gate[2] = static_cast<int64_t>(total) * 16 > tiles ? 1 : 0;
+      gate[0] = 0;
+      gate[1] = 0;
+      __threadfence();
+    }
+  }
 }
 
 cudaError_t tile_mix_launch(const int32_t* size, int64_t n, int width, int limit,
-                            const int32_t* route, int32_t* count, cudaStream_t stream) {
+                            const int32_t* route, int32_t* gate, cudaStream_t stream) {
   const int64_t tiles = (n + kMixTileRows - 1) / kMixTileRows;
   const int64_t blocks64 = (tiles + 7) / 8;
   const int blocks = static_cast<int>(blocks64 < 148 * 8 ? blocks64 : 148 * 8);
   if (blocks == 0) return cudaSuccess;
-  tile_mix_kernel<<<blocks, 256, 0, stream>>>(size, n, width, limit, route, count);
+  tile_mix_kernel<<<blocks, 256, 0, stream>>>(size, n, width, limit, route, gate);
   return cudaGetLastError();
 }
 

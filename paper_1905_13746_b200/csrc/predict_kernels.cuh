@@ -192,9 +192,7 @@ __device__ __forceinline__ void write_row(const PredictParams& p, int64_t r, int
 // Device-side kernel gate (GNB_ORDER_AUTO): both K-PRED kernels are launched
 // and the one not chosen by the tile-mix count exits at once.
 __device__ __forceinline__ bool gated_off(const PredictParams& p) {
-  if (p.gate == nullptr) return false;
-  const bool mixed = static_cast<int64_t>(__ldg(p.gate)) * 16 > p.gate_tiles;
-  return mixed != (p.gate_want != 0);
+  return p.gate != nullptr && __ldg(p.gate) != p.gate_want;
 }
 
 // ------------------------------------------------------------------ TMA kernel

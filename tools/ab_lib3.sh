@@ -1,0 +1,10 @@
+# same-box A/B of in-tree builds (GNB_LIB=...): cfg4 + cfg2 sweep, two repetitions
+libs=${LIBS:-"libgnb_base.so libgnb.so"}
+for rep in 1 2; do
+for lib in $libs; do
+  GNB_LIB=$lib timeout 600 python bench.py --steps 20 --warmup 5 --no-cpu-baseline --no-e2e --no-object-api 2>/dev/null | grep '^{' | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$lib cfg4', d['value'], d['roofline']['frac'], d['clocks'])"
+  GNB_LIB=$lib timeout 600 python bench.py --workload sweep --steps 20 --warmup 3 2>/dev/null | grep '^{' | python -c "
+import json,sys
+d=json.loads(sys.stdin.read())
+print('$lib sweep', [(r['F'], r['frac']) for r in d['rows']])"
+done; done
