@@ -69,7 +69,10 @@ enum { GNB_MODE_EXACT = 0, GNB_MODE_FMA = 1 };
  *                      take the 6-CTA kernel, interleaved ones the mixed-slot
  *                      kernel;
  *   GNB_ORDER_GROUPED  rows grouped by size group (GroupedCorpus order): no check;
- *   GNB_ORDER_MIXED    rows in any order: mixed-slot kernel, no check.
+ *   GNB_ORDER_MIXED    rows in any order: mixed-slot kernel, no check (where
+ *                      gnb_predict_mixed_rows() is 0 this is the 6-CTA kernel
+ *                      reading tables through L1 -- pass a gnb_slot_sort perm
+ *                      instead).
  * Results are identical for every hint. */
 enum { GNB_ORDER_AUTO = 0, GNB_ORDER_GROUPED = 0x10, GNB_ORDER_MIXED = 0x20 };
 

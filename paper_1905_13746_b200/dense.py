@@ -144,6 +144,8 @@ def predict(x: torch.Tensor, size_bytes: torch.Tensor, tables: DeviceTables, *,
         raise InvalidConfigError(f"mode must be 'exact' or 'fma', got {mode!r}")
     if order not in _ORDERS:
         raise InvalidConfigError(f"order must be one of {sorted(_ORDERS)}, got {order!r}")
+    if order == "mixed" and perm is None and not generic and needs_slot_sort(x.dtype, tables):
+        perm = slot_sort(size_bytes, tables, stream=stream)  # no mixed-slot kernel for this shape
     xp, n, F, ldx = _rows(x, dtypes=tuple(_X_TYPES))
     if F != tables.n_features:
         raise InvalidConfigError(f"x has {F} columns, tables have {tables.n_features} features")

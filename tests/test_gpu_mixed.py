@@ -124,6 +124,27 @@ def test_order_hints_give_identical_results(order_hint, rows):
     assert lp[ok].tobytes() == wlp[ok].tobytes()
 
 
+def test_mixed_hint_sorts_when_kernel_does_not_apply():
+    """order="mixed" on a shape without the mixed-slot kernel (C = 3) takes the
+    device slot sort + gather4 path; same results as the oracle."""
+    rng = np.random.default_rng(23)
+    S, G, F, width = 5, 8, 200, 100
+    prior, ll, route = _tables(rng, S, 3, F, G)
+    N = 20_000
+    size = rng.integers(-5, G * width + 5, size=N)
+    x = rng.integers(0, 30, size=(N, F))
+    dev = torch.device("cuda")
+    t = dense.DeviceTables.build(prior, ll, route, group_size_bytes=width, max_size_bytes=G * width)
+    assert dense.needs_slot_sort(torch.int32, t)
+    lab, lp = dense.predict(torch.from_numpy(x.astype(np.int32)).to(dev),
+                            torch.from_numpy(size.astype(np.int32)).to(dev), t, order="mixed")
+    want, wlp = O.predict_dense(x, size, route, prior, ll, width=width, limit=G * width)
+    lab, lp = lab.cpu().numpy(), lp.cpu().numpy()
+    assert lab.tolist() == want.tolist()
+    ok = want >= 0
+    assert lp[ok].tobytes() == wlp[ok].tobytes()
+
+
 def test_order_hint_rejected():
     t = dense.DeviceTables.build(np.log([[0.5, 0.5]]), np.log(np.full((1, 2, 4), 0.25)),
                                  np.zeros(1, np.int32), group_size_bytes=10, max_size_bytes=10)
