@@ -83,3 +83,20 @@ def test_pack_u4_layout_and_odd_ldx():
                                         None, None, None, 0, None) == N.GNB_EINVAL
     assert N.lib.gnb_predict_host_typed(None, 9, 1, 3, 3, None, 1, 1, None, 1, 2, None,
                                         None, None, None, 0, None) == N.GNB_EINVAL
+
+
+def test_mixed_rows_kernel_choice():
+    """gnb_predict_mixed_rows (host-only shape logic): the mixed-slot kernel takes
+    C = 2 batches of >= 2 slots whose tables fit next to >= 3 ring stages, and
+    never short rows (row-box kernel) or bad arguments."""
+    f = N.lib.gnb_predict_mixed_rows
+    assert f(200, N.X_I32, 2, 29) == 256          # cfg3: 29 x 200 features = 93 KB of tables
+    assert f(300, N.X_U8, 2, 29) == 256          # uint8 rows of 300 features (not row-box)
+    assert f(200, N.X_U8, 2, 29) == 0             # uint8 F=200 is 13 quads: row-box kernel
+    assert f(200, N.X_I32, 2, 1) == 0             # one slot: uniform tiles
+    assert f(200, N.X_I32, 4, 29) == 0            # class pad 4
+    assert f(50, N.X_I32, 2, 8) == 0              # short rows: row-box kernel
+    assert f(2000, N.X_I32, 2, 64) == 0           # 2 MB of tables
+    assert f(200, N.X_I32, 2, 40) == 256          # 129 KB of tables + 3 stages fit
+    assert f(200, N.X_I32, 2, 45) == 0            # 145 KB: fewer than 3 stages fit
+    assert f(0, N.X_I32, 2, 4) == 0 and f(200, 7, 2, 4) == 0 and f(200, N.X_I32, 17, 4) == 0
