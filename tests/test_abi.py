@@ -91,7 +91,7 @@ def test_mixed_rows_kernel_choice():
     never short rows (row-box kernel) or bad arguments."""
     f = N.lib.gnb_predict_mixed_rows
     assert f(200, N.X_I32, 2, 29) == 256          # cfg3: 29 x 200 features = 93 KB of tables
-    assert f(300, N.X_U8, 2, 29) == 256          # uint8 rows of 300 features (not row-box)
+    assert f(300, N.X_U8, 2, 20) == 256          # uint8 rows of 300 features (not row-box)
     assert f(200, N.X_U8, 2, 29) == 0             # uint8 F=200 is 13 quads: row-box kernel
     assert f(200, N.X_I32, 2, 1) == 0             # one slot: uniform tiles
     assert f(200, N.X_I32, 4, 29) == 0            # class pad 4
