@@ -7,6 +7,7 @@
 #include <condition_variable>
 #include <functional>
 #include <thread>
+#include <tuple>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -204,24 +205,37 @@ static bool rowbox_bulk() {
 }
 
 // The tile-mix gate of GNB_ORDER_AUTO ([count, done, decision] ints), one per
-// (device, stream): reuse on the same stream is stream-ordered (count ->
-// decision -> gated kernels; the counting kernel leaves the counters at 0),
-// different streams never share one.  Allocated and zeroed once, never freed.
-static int32_t* gate_counter(cudaStream_t stream) {
+// (device, stream; per host thread for cudaStreamPerThread, whose handle names
+// a different stream in every thread).  A call holds the gate's mutex while it
+// enqueues count -> gated kernels, so calls sharing a stream from several host
+// threads cannot interleave their sequences; after that, stream order keeps
+// the next call's count behind this call's kernels.  The counting kernel
+// leaves the counters at 0.  Allocated and zeroed once, never freed.
+struct Gate {
+  int32_t* dev = nullptr;
+  std::mutex mu;
+};
+static Gate* gate_for(cudaStream_t stream) {
   static std::mutex mu;
-  static std::map<std::pair<int, uintptr_t>, int32_t*> counters;
+  static std::map<std::tuple<int, uintptr_t, std::thread::id>, Gate> gates;
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  const std::thread::id tid =
+      stream == cudaStreamPerThread ? std::this_thread::get_id() : std::thread::id();
   std::lock_guard<std::mutex> lock(mu);
-  int32_t*& c = counters[{dev, reinterpret_cast<uintptr_t>(stream)}];
-  if (c == nullptr) {
-    if (cudaMalloc(reinterpret_cast<void**>(&c), 4 * sizeof(int32_t)) != cudaSuccess) return c = nullptr;
-    if (cudaMemset(c, 0, 4 * sizeof(int32_t)) != cudaSuccess) {
-      cudaFree(c);
-      return c = nullptr;
+  Gate& g = gates[{dev, reinterpret_cast<uintptr_t>(stream), tid}];
+  if (g.dev == nullptr) {
+    if (cudaMalloc(reinterpret_cast<void**>(&g.dev), 4 * sizeof(int32_t)) != cudaSuccess) {
+      g.dev = nullptr;
+      return nullptr;
+    }
+    if (cudaMemset(g.dev, 0, 4 * sizeof(int32_t)) != cudaSuccess) {
+      cudaFree(g.dev);
+      g.dev = nullptr;
+      return nullptr;
     }
   }
-  return c;
+  return &g;
 }
 
 // True when predict_device will take the mixed-slot kernel (rows of any slot
@@ -281,8 +295,10 @@ static int predict_device(const void* x, int x_type, int64_t n_rows, int32_t F, 
           return fail(GNB_ECUDA, "predict: cuTensorMapEncodeTiled failed");
         mmap.tail = mmap.main;
         gmap.tail = gmap.main;
-        int32_t* cnt = gate_counter(stream);
-        if (cnt == nullptr) return fail(GNB_ENOMEM, "predict: gate counter allocation failed");
+        Gate* gate = gate_for(stream);
+        if (gate == nullptr) return fail(GNB_ENOMEM, "predict: gate counter allocation failed");
+        std::lock_guard<std::mutex> gate_lock(gate->mu);
+        int32_t* cnt = gate->dev;
         GNB_CUDA(tile_mix_launch(p.size, n, width, limit, route, cnt, stream), "tile_mix");
         PredictParams pm = p, pg = p;
         pm.mixed_rows = mr;

@@ -239,3 +239,47 @@ def test_same_bytes_with_and_without_mixed_kernel(S):
         assert r.returncode == 0, r.stderr.decode()[-2000:]
         outs.append(r.stdout)
     assert outs[0] == outs[1] == outs[2]
+
+
+def test_auto_gate_from_concurrent_host_threads():
+    """GNB_ORDER_AUTO from several host threads at once, on one shared stream and
+    on per-thread streams: each call's count -> gated-kernel sequence stays its
+    own (results equal the single-threaded ones)."""
+    import threading
+    rng = np.random.default_rng(31)
+    S, G, F, width = 12, 14, 200, 100
+    prior, ll, route = _tables(rng, S, 2, F, G)
+    dev = torch.device("cuda")
+    t = dense.DeviceTables.build(prior, ll, route, group_size_bytes=width, max_size_bytes=G * width)
+    cases = []
+    for i in range(4):
+        N = 60_000 + 1000 * i
+        size = np.sort(rng.integers(0, G * width, size=N))
+        if i % 2:
+            size = rng.permutation(size)      # odd threads: shuffled -> mixed-slot kernel
+        x = torch.from_numpy(rng.integers(0, 20, size=(N, F)).astype(np.int32)).to(dev)
+        sd = torch.from_numpy(size.astype(np.int32)).to(dev)
+        lab, lp = dense.predict(x, sd, t)
+        torch.cuda.synchronize()
+        cases.append((x, sd, lab.clone(), lp.clone()))
+    for per_thread_stream in (False, True):
+        errors = []
+
+        def work(i):
+            x, sd, lab0, lp0 = cases[i]
+            s = torch.cuda.Stream() if per_thread_stream else torch.cuda.current_stream()
+            with torch.cuda.stream(s):
+                for _ in range(15):
+                    lab, lp = dense.predict(x, sd, t, stream=s)
+                    s.synchronize()
+                    if not (torch.equal(lab, lab0) and torch.equal(lp.view(torch.int64),
+                                                                   lp0.view(torch.int64))):
+                        errors.append(i)
+                        return
+
+        th = [threading.Thread(target=work, args=(i,)) for i in range(4)]
+        for h in th:
+            h.start()
+        for h in th:
+            h.join()
+        assert not errors, errors
