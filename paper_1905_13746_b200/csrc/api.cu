@@ -111,6 +111,16 @@ static bool encode_map(CUtensorMap* map, const void* base, int64_t n_rows, int32
                        int box_cols = 0, int promo = -1) {
   auto fn = encode_fn();
   if (fn == nullptr) return false;
+  // cuTensorMapEncodeTiled is a driver call and needs a current context: a
+  // fresh host thread has none until its first runtime call that binds the
+  // primary context (cudaFree(nullptr) does, and is cheap once bound).
+  static thread_local int bound_device = -1;
+  int cur = 0;
+  if (cudaGetDevice(&cur) != cudaSuccess) return false;
+  if (bound_device != cur) {
+    if (cudaFree(nullptr) != cudaSuccess) return false;
+    bound_device = cur;
+  }
   const int eb = elem_bytes(x_type);
   const CUtensorMapDataType dt = x_type == GNB_X_U8    ? CU_TENSOR_MAP_DATA_TYPE_UINT8
                                  : x_type == GNB_X_U16 ? CU_TENSOR_MAP_DATA_TYPE_UINT16

@@ -263,19 +263,22 @@ def test_auto_gate_from_concurrent_host_threads():
         torch.cuda.synchronize()
         cases.append((x, sd, lab.clone(), lp.clone()))
     for per_thread_stream in (False, True):
-        errors = []
+        errors = []  # filled by the worker threads
 
         def work(i):
-            x, sd, lab0, lp0 = cases[i]
-            s = torch.cuda.Stream() if per_thread_stream else torch.cuda.current_stream()
-            with torch.cuda.stream(s):
-                for _ in range(15):
-                    lab, lp = dense.predict(x, sd, t, stream=s)
-                    s.synchronize()
-                    if not (torch.equal(lab, lab0) and torch.equal(lp.view(torch.int64),
-                                                                   lp0.view(torch.int64))):
-                        errors.append(i)
-                        return
+            try:
+                x, sd, lab0, lp0 = cases[i]
+                s = torch.cuda.Stream() if per_thread_stream else torch.cuda.current_stream()
+                with torch.cuda.stream(s):
+                    for _ in range(15):
+                        lab, lp = dense.predict(x, sd, t, stream=s)
+                        s.synchronize()
+                        if not (torch.equal(lab, lab0) and torch.equal(lp.view(torch.int64),
+                                                                       lp0.view(torch.int64))):
+                            errors.append((i, "mismatch"))
+                            return
+            except Exception as e:  # noqa: BLE001 -- reported by the assert below
+                errors.append((i, repr(e)))
 
         th = [threading.Thread(target=work, args=(i,)) for i in range(4)]
         for h in th:
