@@ -70,7 +70,8 @@ def test_shuffled_many_slots(S, F, N):
 
 
 @pytest.mark.parametrize("S,F,dtype", [(29, 200, torch.int32), (7, 105, torch.int32),
-                                         (40, 300, torch.uint8), (3, 33, torch.int32)])
+                                         (40, 300, torch.uint8), (3, 33, torch.int32),
+                                         (72, 105, torch.int32)])
 def test_many_tiles_per_cta(S, F, dtype):
     """Several tiles per persistent CTA (the header ring and the stage ring wrap
     many times): every row of a shuffled ragged batch vs the C oracle."""
@@ -158,6 +159,8 @@ def test_kernel_is_taken_for_these_shapes():
     """The shapes above run the mixed-slot kernel (not the row box / sort paths)."""
     I32 = 0
     assert _mixed_rows(200, I32, 2, 29) == 256
+    assert _mixed_rows(105, I32, 2, 72) == 256     # the most slots that fit at F=105: a
+    assert _mixed_rows(105, I32, 2, 75) == 0       # 73-bin histogram, 3 warp-wide scan passes
     assert _mixed_rows(105, I32, 2, 2) == 256
     assert _mixed_rows(200, I32, 2, 1) == 0        # one slot: uniform tiles, 6-CTA kernel
     assert _mixed_rows(200, I32, 3, 29) == 0       # C > 2: other class pads
