@@ -214,13 +214,16 @@ static bool rowbox_bulk() {
   return v != 0;
 }
 
-// The tile-mix gate of GNB_ORDER_AUTO ([count, done, decision] ints), one per
-// (device, stream; per host thread for cudaStreamPerThread, whose handle names
-// a different stream in every thread).  A call holds the gate's mutex while it
-// enqueues count -> gated kernels, so calls sharing a stream from several host
-// threads cannot interleave their sequences; after that, stream order keeps
-// the next call's count behind this call's kernels.  The counting kernel
-// leaves the counters at 0.  Allocated and zeroed once, never freed.
+// Per-(device, stream) K-PRED scratch (per host thread for cudaStreamPerThread,
+// whose handle names a different stream in every thread), 8 ints, allocated
+// and zeroed once, never freed:
+//   [0..2] the tile-mix gate of GNB_ORDER_AUTO ([count, done, decision]); a
+//          call holds `mu` while it enqueues count -> gated kernels, so calls
+//          sharing a stream from several host threads cannot interleave those
+//          sequences (stream order does the rest); the counting kernel leaves
+//          the counters at 0;
+//   [4..5] the 128-B-box kernel's dynamic tile counter (left at 0 by the last
+//          producer of each launch; launches on one stream run in order).
 struct Gate {
   int32_t* dev = nullptr;
   std::mutex mu;
@@ -235,17 +238,26 @@ static Gate* gate_for(cudaStream_t stream) {
   std::lock_guard<std::mutex> lock(mu);
   Gate& g = gates[{dev, reinterpret_cast<uintptr_t>(stream), tid}];
   if (g.dev == nullptr) {
-    if (cudaMalloc(reinterpret_cast<void**>(&g.dev), 4 * sizeof(int32_t)) != cudaSuccess) {
+    if (cudaMalloc(reinterpret_cast<void**>(&g.dev), 8 * sizeof(int32_t)) != cudaSuccess) {
       g.dev = nullptr;
       return nullptr;
     }
-    if (cudaMemset(g.dev, 0, 4 * sizeof(int32_t)) != cudaSuccess) {
+    if (cudaMemset(g.dev, 0, 8 * sizeof(int32_t)) != cudaSuccess) {
       cudaFree(g.dev);
       g.dev = nullptr;
       return nullptr;
     }
   }
   return &g;
+}
+
+// GNB_DYNAMIC_TILES=0: static grid-stride tiles in the 128-B-box kernel (A/B).
+static bool dynamic_tiles() {
+  static const int v = [] {  // read once (thread-safe static init)
+    const char* e = getenv("GNB_DYNAMIC_TILES");
+    return e ? atoi(e) : 1;
+  }();
+  return v != 0;
 }
 
 // True when predict_device will take the mixed-slot kernel (rows of any slot
@@ -286,6 +298,11 @@ static int predict_device(const void* x, int x_type, int64_t n_rows, int32_t F, 
     const int order = mode & (GNB_ORDER_GROUPED | GNB_ORDER_MIXED);
     PredictMaps map;
     const PredictMaps* mp = nullptr;
+    if (use_tma && dynamic_tiles()) {
+      Gate* sg = gate_for(stream);
+      if (sg == nullptr) return fail(GNB_ENOMEM, "predict: scratch allocation failed");
+      p.tile_ctr = sg->dev + 4;
+    }
     if (use_tma) {
       // row-box mode (short rows): whole rows per box, unswizzled; gather mode:
       // box height 1 (tile::gather4 loads 4 rows per instruction)

@@ -52,6 +52,9 @@ struct PredictParams {
   // *gate == gate_want
   const int32_t* gate;
   int32_t gate_want;
+  // nullable: [next dynamic tile - gridDim.x, producers done]; 0 on entry, left
+  // at 0 by the last producer (128-B-box kernel's dynamic tile scheduling)
+  int32_t* tile_ctr;
 };
 
 struct FitParams {

@@ -207,8 +207,8 @@ struct PredictSmem {
   static constexpr int kTabChunk = Elem<T>::kPerRow * CP * 8;          // one chunk's table
   static constexpr int kPrior = CP * 8;                                // the slot's prior
   static constexpr int kTabBytes = kPrior + B * kTabChunk;             // prior + tables
-  // tile_slot + row_slot[kRows] (+ row_id[kRows] in gather mode)
-  static constexpr int kHdrBytes = ((4 + kRows * 4 * (GATHER ? 2 : 1)) + 15) / 16 * 16;
+  // tile_slot + tile + row_slot[kRows] (+ row_id[kRows] in gather mode)
+  static constexpr int kHdrBytes = ((8 + kRows * 4 * (GATHER ? 2 : 1)) + 15) / 16 * 16;
   static constexpr int kX = 0;
   static constexpr int kTab = kX + STAGES * kXBytes;
   static constexpr int kHdr = kTab + STAGES * kTabBytes;
@@ -220,6 +220,7 @@ struct PredictSmem {
 
 struct StageHdr {
   int tile_slot;  // >= 0: every valid row uses this slot; table slice staged
+  int tile;       // the tile this stage belongs to; -1 = no more tiles (end marker)
   int row_slot[1];  // [kRows]; in gather mode followed by row_id[kRows]
 };
 
@@ -331,7 +332,13 @@ __global__ void __launch_bounds__((NW + 1) * 32)
     const uint64_t pol_t = policy_evict_last();
     int stage = 0;
     uint32_t phase = 0;
-    for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    // Tiles: the CTA's first is blockIdx.x; after that, with p.tile_ctr, the
+    // next unclaimed tile in index order (one atomic per tile) -- CTAs whose
+    // SM gets less DRAM bandwidth take fewer tiles, so they all finish
+    // together instead of spreading the launch's last ~20 us (a static
+    // grid-stride split finished CTAs of equal tile count 113-134 us apart
+    // at 1M x 200).  Tiles are still handed out in order (DRAM locality).
+    for (int64_t tile = blockIdx.x; tile < n_tiles;) {
       const int64_t r0 = tile * ROWS;
       int slots[ROWS / 32], ids[ROWS / 32];
       int lo = INT_MAX, hi = INT_MIN;
@@ -366,7 +373,10 @@ __global__ void __launch_bounds__((NW + 1) * 32)
             if (GATHER) hdr->row_slot[ROWS + lane + 32 * i] = ids[i];
           }
         }
-        if (lane == 0) hdr->tile_slot = tile_slot;
+        if (lane == 0) {
+          hdr->tile_slot = tile_slot;
+          hdr->tile = static_cast<int>(tile);
+        }
         __syncwarp();
         uint8_t* box = smem + L::kX + stage * L::kXBytes;
         if (lane == 0) {
@@ -407,6 +417,27 @@ __global__ void __launch_bounds__((NW + 1) * 32)
           phase ^= 1;
         }
       }
+      if (p.tile_ctr != nullptr) {
+        int next = 0;
+        if (lane == 0) next = static_cast<int>(gridDim.x) + atomicAdd(p.tile_ctr, 1);
+        tile = __shfl_sync(0xffffffffu, next, 0);
+      } else {
+        tile += gridDim.x;
+      }
+    }
+    // end marker: one more stage whose header says "no more tiles"
+    mbar_wait(&empty[stage], phase ^ 1);
+    if (lane == 0) reinterpret_cast<StageHdr*>(smem + L::kHdr + stage * L::kHdrBytes)->tile = -1;
+    __syncwarp();
+    mbar_arrive(&full[stage]);
+    if (p.tile_ctr != nullptr && lane == 0) {
+      // the last producer to finish leaves the counters at 0 for the next launch
+      __threadfence();
+      if (atomicAdd(p.tile_ctr + 1, 1) == static_cast<int>(gridDim.x) - 1) {
+        p.tile_ctr[0] = 0;
+        p.tile_ctr[1] = 0;
+        __threadfence();
+      }
     }
   } else {
     // ---------------------------------------------------------- consumers
@@ -415,10 +446,11 @@ __global__ void __launch_bounds__((NW + 1) * 32)
     for (int i = 0; i < R; ++i) rows[i] = lane + 32 * (warp + NW * i);
     int stage = 0;
     uint32_t phase = 0;
-    for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    for (;;) {
       double acc[R][CP];
       int slot[R], rid[R];
       uint32_t neg[R];
+      int64_t tile = 0;
 #pragma unroll
       for (int i = 0; i < R; ++i) neg[i] = 0;
       for (int sc = 0; sc < NSC; ++sc) {
@@ -426,6 +458,10 @@ __global__ void __launch_bounds__((NW + 1) * 32)
         const StageHdr* hdr =
             reinterpret_cast<const StageHdr*>(smem + L::kHdr + stage * L::kHdrBytes);
         const int ts = hdr->tile_slot;
+        if (sc == 0) {
+          tile = hdr->tile;
+          if (tile < 0) break;  // end marker (released below)
+        }
         if (sc == 0) {
 #pragma unroll
           for (int i = 0; i < R; ++i) {
@@ -461,6 +497,11 @@ __global__ void __launch_bounds__((NW + 1) * 32)
           stage = 0;
           phase ^= 1;
         }
+      }
+      if (tile < 0) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[stage]);
+        break;
       }
 #pragma unroll
       for (int i = 0; i < R; ++i) {
