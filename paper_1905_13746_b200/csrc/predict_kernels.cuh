@@ -550,7 +550,7 @@ struct RowBoxSmem {
     // one slot = [prior: cp doubles][tab_feats x cp log-likelihoods]
     res_stride = static_cast<uint32_t>(1 + tab_feats) * cp;  // doubles
     tab_bytes = resident_slots > 0 ? 0u : res_stride * 8;
-    hdr_bytes = (4 + kRowBoxRows * 4 + 15) / 16 * 16;
+    hdr_bytes = (8 + kRowBoxRows * 4 + 15) / 16 * 16;  // tile_slot, tile, slot[rows]
     x = 0;
     res = x + stages * x_bytes;
     tab = res + static_cast<uint32_t>(resident_slots) * res_stride * 8;
@@ -656,10 +656,29 @@ __global__ void __launch_bounds__(5 * 32, MINB)
       }
       cp_async_commit();
     };
+    // Tiles are claimed when their sizes are prefetched (kRowBoxAhead ahead):
+    // the CTA's first is blockIdx.x, later ones the next unclaimed tile from
+    // p.tile_ctr (dynamic scheduling, as in the 128-B-box kernel), else
+    // grid-strided.  tq[0] is the tile being issued, tq[1..] the claimed ones.
+    int64_t tq[kRowBoxAhead];
+    int64_t j_static = 0;
+    auto claim = [&]() -> int64_t {
+      if (p.tile_ctr != nullptr && j_static > 0) {
+        int nt = 0;
+        if (lane == 0) nt = static_cast<int>(gridDim.x) + atomicAdd(p.tile_ctr, 1);
+        return __shfl_sync(0xffffffffu, nt, 0);
+      }
+      return blockIdx.x + (j_static++) * int64_t(gridDim.x);
+    };
 #pragma unroll
-    for (int k = 0; k < kRowBoxAhead; ++k) fetch_sizes(blockIdx.x + int64_t(k) * gridDim.x, k);
+    for (int k = 0; k < kRowBoxAhead; ++k) {
+      tq[k] = claim();
+      fetch_sizes(tq[k], k);
+    }
     int k_cur = 0;
-    for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    for (;;) {
+      const int64_t tile = tq[0];
+      if (tile >= n_tiles) break;
       const int64_t r0 = tile * ROWS;
       // X first: it does not depend on routing, so the copy is in flight while
       // the producer waits for the tile's sizes and routes them (this also
@@ -695,15 +714,21 @@ __global__ void __launch_bounds__(5 * 32, MINB)
         }
         slots[i] = s;
       }
-      fetch_sizes(tile + int64_t(kRowBoxAhead) * gridDim.x, k_cur);
+#pragma unroll
+      for (int k = 0; k + 1 < kRowBoxAhead; ++k) tq[k] = tq[k + 1];
+      tq[kRowBoxAhead - 1] = claim();
+      fetch_sizes(tq[kRowBoxAhead - 1], k_cur);
       if (++k_cur == kRowBoxAhead) k_cur = 0;
       lo = __reduce_min_sync(0xffffffffu, lo);
       hi = __reduce_max_sync(0xffffffffu, hi);
       const int tile_slot = (lo == INT_MAX) ? 0 : (lo == hi ? lo : -1);
       int* hdr = reinterpret_cast<int*>(smem + L.hdr + stage * L.hdr_bytes);
 #pragma unroll
-      for (int i = 0; i < ROWS / 32; ++i) hdr[1 + lane + 32 * i] = slots[i];
-      if (lane == 0) hdr[0] = tile_slot;
+      for (int i = 0; i < ROWS / 32; ++i) hdr[2 + lane + 32 * i] = slots[i];
+      if (lane == 0) {
+        hdr[0] = tile_slot;
+        hdr[1] = static_cast<int>(tile);
+      }
       __syncwarp();
       if (lane == 0) {
         const bool stage_tab = !resident && tile_slot >= 0;
@@ -722,6 +747,20 @@ __global__ void __launch_bounds__(5 * 32, MINB)
         phase ^= 1;
       }
     }
+    // end marker: one more stage whose header says "no more tiles"
+    mbar_wait(&empty[stage], phase ^ 1);
+    if (lane == 0) reinterpret_cast<int*>(smem + L.hdr + stage * L.hdr_bytes)[1] = -1;
+    __syncwarp();
+    mbar_arrive(&full[stage]);
+    if (p.tile_ctr != nullptr && lane == 0) {
+      // the last producer to finish leaves the counters at 0 for the next launch
+      __threadfence();
+      if (atomicAdd(p.tile_ctr + 1, 1) == static_cast<int>(gridDim.x) - 1) {
+        p.tile_ctr[0] = 0;
+        p.tile_ctr[1] = 0;
+        __threadfence();
+      }
+    }
   } else {
     // ---------------------------------------------------------- consumers
     const int row = lane + 32 * warp;
@@ -731,11 +770,17 @@ __global__ void __launch_bounds__(5 * 32, MINB)
     const double* res = reinterpret_cast<const double*>(smem + L.res);
     int stage = 0;
     uint32_t phase = 0;
-    for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    for (;;) {
       mbar_wait(&full[stage], phase);
       const int* hdr = reinterpret_cast<const int*>(smem + L.hdr + stage * L.hdr_bytes);
+      const int64_t tile = hdr[1];
+      if (tile < 0) {  // end marker
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[stage]);
+        break;
+      }
       const int ts = hdr[0];
-      const int slot = hdr[1 + row];
+      const int slot = hdr[2 + row];
       const int s = ts >= 0 ? ts : max(slot, 0);
       double acc[CP];
       uint32_t neg = 0;
@@ -842,7 +887,7 @@ struct MixSmem {
     x_bytes = static_cast<uint32_t>(rows) * kChunkBytesPerRow;
     tab_feats = static_cast<uint32_t>((F + eq - 1) / eq * eq);  // features read per slot
     stride = 2u * (1u + tab_feats);  // doubles per slot (CP = 2): odd number of 16-B units
-    hdr_bytes = static_cast<uint32_t>(rows) * 8;  // slot[rows] | rid[rows]
+    hdr_bytes = static_cast<uint32_t>(rows) * 8 + 16;  // slot[rows] | rid[rows] | tile
     // header ring: the producer can be at most ceil(stages / nch) tiles ahead
     // of the consumers' header reads (a tile's header is read before its first
     // stage is released)
@@ -914,11 +959,28 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1)
       }
       cp_async_commit();
     };
+    // tiles claimed when their sizes are prefetched (as in the row-box kernel):
+    // blockIdx.x first, then the next unclaimed tile from p.tile_ctr
+    int64_t tq[AHEAD];
+    int64_t j_static = 0;
+    auto claim = [&]() -> int64_t {
+      if (p.tile_ctr != nullptr && j_static > 0) {
+        int nt = 0;
+        if (lane == 0) nt = static_cast<int>(gridDim.x) + atomicAdd(p.tile_ctr, 1);
+        return __shfl_sync(0xffffffffu, nt, 0);
+      }
+      return blockIdx.x + (j_static++) * int64_t(gridDim.x);
+    };
 #pragma unroll
-    for (int k = 0; k < AHEAD; ++k) fetch_sizes(blockIdx.x + int64_t(k) * gridDim.x, k);
+    for (int k = 0; k < AHEAD; ++k) {
+      tq[k] = claim();
+      fetch_sizes(tq[k], k);
+    }
     int k_cur = 0, stage = 0, h = 0;
     uint32_t phase = 0;
-    for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    for (;;) {
+      const int64_t tile = tq[0];
+      if (tile >= n_tiles) break;
       const int64_t r0 = tile * ROWS;
       for (int sc = 0; sc < NCH; ++sc) {
         mbar_wait(&empty[stage], phase ^ 1);
@@ -938,7 +1000,10 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1)
             key[i] = (r < p.n_rows && sz >= 0 && sz < p.limit) ? __ldg(p.route + sz / p.width) + 1
                                                                : 0;
           }
-          fetch_sizes(tile + int64_t(AHEAD) * gridDim.x, k_cur);
+#pragma unroll
+          for (int k = 0; k + 1 < AHEAD; ++k) tq[k] = tq[k + 1];
+          tq[AHEAD - 1] = claim();
+          fetch_sizes(tq[AHEAD - 1], k_cur);
           if (++k_cur == AHEAD) k_cur = 0;
           // stable counting sort by key: ranks within a key in row order
           for (int b = lane; b <= S; b += 32) hist[b] = 0;
@@ -974,6 +1039,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1)
             hs[pos] = key[i] - 1;
             hs[ROWS + pos] = lane + 32 * i;
           }
+          if (lane == 0) hs[2 * ROWS] = static_cast<int>(tile);
           if (++h == HD) h = 0;
           __syncwarp();
         }
@@ -984,6 +1050,20 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1)
         }
       }
     }
+    // end marker: one more stage whose header says "no more tiles"
+    mbar_wait(&empty[stage], phase ^ 1);
+    if (lane == 0) reinterpret_cast<int*>(smem + L.hdr + h * L.hdr_bytes)[2 * ROWS] = -1;
+    __syncwarp();
+    mbar_arrive(&full[stage]);
+    if (p.tile_ctr != nullptr && lane == 0) {
+      // the last producer to finish leaves the counters at 0 for the next launch
+      __threadfence();
+      if (atomicAdd(p.tile_ctr + 1, 1) == static_cast<int>(gridDim.x) - 1) {
+        p.tile_ctr[0] = 0;
+        p.tile_ctr[1] = 0;
+        __threadfence();
+      }
+    }
   } else {
     // ---------------------------------------------------------- consumers
     const int t = lane + 32 * warp;
@@ -991,8 +1071,9 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1)
     const int stride = static_cast<int>(L.stride);
     int stage = 0, h = 0;
     uint32_t phase = 0;
-    // (tile, sc) of the step whose quads are in registers / being fetched
-    int64_t tile = blockIdx.x;
+    // (tile, sc) of the step whose quads are in registers / being fetched;
+    // a tile's index arrives with its header (claimed by the producer)
+    int64_t tile = 0;
     int sc = 0;
     // fetch step (tile, sc): its header (first chunk of a tile), its quads
     // into registers, then release the stage.  The release must not overtake
@@ -1003,13 +1084,21 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1)
     // negative-count flag) and the warp's ballot of that fold feeds the
     // arrive's address (+ (ballot & dep_zero), an opaque zero): the arrive
     // issues only after every lane's loads have returned.
-    auto fetch = [&](uint4 (&v)[QPC], int fsc, int& slot, int& rid, uint32_t& fold) {
+    // Returns false (stage released, nothing loaded) on the producer's end marker.
+    auto fetch = [&](uint4 (&v)[QPC], int fsc, int& slot, int& rid, uint32_t& fold,
+                     int64_t& ftile) {
       mbar_wait(&full[stage], phase);
       if (fsc == 0) {
         const int* hs = reinterpret_cast<const int*>(smem + L.hdr + h * L.hdr_bytes);
+        ftile = hs[2 * ROWS];
+        if (++h == HD) h = 0;
+        if (ftile < 0) {  // end marker
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty[stage]);
+          return false;
+        }
         slot = hs[t];
         rid = hs[ROWS + t];
-        if (++h == HD) h = 0;
       }
       const int nq = (min(CF, p.n_features - fsc * CF) + EQ - 1) / EQ;
       const uint8_t* box = smem + L.x + stage * L.x_bytes;
@@ -1035,6 +1124,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1)
         stage = 0;
         phase ^= 1;
       }
+      return true;
     };
     double acc[CP] = {0.0, 0.0};
     uint32_t neg = 0;
@@ -1072,41 +1162,32 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1)
         if (r < p.n_rows) write_row<CP>(p, r, slot, neg, acc);
       }
     };
-    if (tile < n_tiles) {
+    {
       uint4 va[QPC], vb[QPC];
       int slot_a = -1, rid_a = 0, slot_b = -1, rid_b = 0;
       uint32_t fa = 0, fb = 0;
-      fetch(va, 0, slot_a, rid_a, fa);
-      // ping-pong between two register sets (no copies): A scored while B
-      // holds the next step, then the roles swap
-      for (;;) {
-        int nsc = sc + 1;
-        int64_t ntile = tile;
-        if (nsc == NCH) {
-          nsc = 0;
-          ntile += gridDim.x;
+      int64_t tile_b = 0;
+      if (fetch(va, 0, slot_a, rid_a, fa, tile)) {
+        // ping-pong between two register sets (no copies): A scored while B
+        // holds the next step, then the roles swap
+        for (;;) {
+          int nsc = sc + 1 == NCH ? 0 : sc + 1;
+          slot_b = nsc == 0 ? -1 : slot_a;
+          rid_b = nsc == 0 ? 0 : rid_a;
+          tile_b = tile;
+          const bool more = fetch(vb, nsc, slot_b, rid_b, fb, tile_b);
+          score(va, sc, slot_a, rid_a, tile, fa);
+          if (!more) break;
+          sc = nsc;
+          tile = tile_b;
+          nsc = sc + 1 == NCH ? 0 : sc + 1;
+          slot_a = nsc == 0 ? -1 : slot_b;
+          rid_a = nsc == 0 ? 0 : rid_b;
+          const bool more2 = fetch(va, nsc, slot_a, rid_a, fa, tile);
+          score(vb, sc, slot_b, rid_b, tile_b, fb);
+          if (!more2) break;
+          sc = nsc;
         }
-        const bool more = ntile < n_tiles;
-        slot_b = nsc == 0 ? -1 : slot_a;
-        rid_b = nsc == 0 ? 0 : rid_a;
-        if (more) fetch(vb, nsc, slot_b, rid_b, fb);
-        score(va, sc, slot_a, rid_a, tile, fa);
-        if (!more) break;
-        sc = nsc;
-        tile = ntile;
-        nsc = sc + 1;
-        if (nsc == NCH) {
-          nsc = 0;
-          ntile += gridDim.x;
-        }
-        const bool more2 = ntile < n_tiles;
-        slot_a = nsc == 0 ? -1 : slot_b;
-        rid_a = nsc == 0 ? 0 : rid_b;
-        if (more2) fetch(va, nsc, slot_a, rid_a, fa);
-        score(vb, sc, slot_b, rid_b, tile, fb);
-        if (!more2) break;
-        sc = nsc;
-        tile = ntile;
       }
     }
   }
@@ -1334,6 +1415,10 @@ static cudaError_t launch_mixed(const PredictMaps& map, PredictParams p, cudaStr
   p.n_tiles = (p.n_rows + ROWS - 1) / ROWS;
   p.n_chunks = (p.n_features + Elem<T>::kPerRow - 1) / Elem<T>::kPerRow;
   p.dep_zero = 0;
+  // static grid-stride tiles: with one producer per SM the claim's atomic
+  // round trip sits on the producer's path, and this kernel is bound by shared
+  // memory, not by per-SM DRAM bandwidth -- dynamic tiles measured 4 % slower
+  p.tile_ctr = nullptr;
   p.mixed_stages = mixed_stages_fit(p.n_features, static_cast<int>(sizeof(T)), p.n_slots);
   static const int st_env = [] {  // GNB_MIXED_STAGES: fewer stages (A/B probes only)
     const char* e = getenv("GNB_MIXED_STAGES");
