@@ -222,21 +222,22 @@ static bool rowbox_bulk() {
 //          sharing a stream from several host threads cannot interleave those
 //          sequences (stream order does the rest); the counting kernel leaves
 //          the counters at 0;
-//   [4..5] the 128-B-box kernel's dynamic tile counter (left at 0 by the last
-//          producer of each launch; launches on one stream run in order).
-struct Gate {
+//   [4..5] the dynamic tile counter of the 128-B-box and row-box kernels (left
+//          at 0 by the last producer of each launch; launches on one stream run
+//          in order).
+struct Scratch {
   int32_t* dev = nullptr;
   std::mutex mu;
 };
-static Gate* gate_for(cudaStream_t stream) {
+static Scratch* scratch_for(cudaStream_t stream) {
   static std::mutex mu;
-  static std::map<std::tuple<int, uintptr_t, std::thread::id>, Gate> gates;
+  static std::map<std::tuple<int, uintptr_t, std::thread::id>, Scratch> gates;
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
   const std::thread::id tid =
       stream == cudaStreamPerThread ? std::this_thread::get_id() : std::thread::id();
   std::lock_guard<std::mutex> lock(mu);
-  Gate& g = gates[{dev, reinterpret_cast<uintptr_t>(stream), tid}];
+  Scratch& g = gates[{dev, reinterpret_cast<uintptr_t>(stream), tid}];
   if (g.dev == nullptr) {
     if (cudaMalloc(reinterpret_cast<void**>(&g.dev), 8 * sizeof(int32_t)) != cudaSuccess) {
       g.dev = nullptr;
@@ -251,7 +252,8 @@ static Gate* gate_for(cudaStream_t stream) {
   return &g;
 }
 
-// GNB_DYNAMIC_TILES=0: static grid-stride tiles in the 128-B-box kernel (A/B).
+// GNB_DYNAMIC_TILES=0: static grid-stride tiles in the 128-B-box and row-box
+// kernels (A/B).
 static bool dynamic_tiles() {
   static const int v = [] {  // read once (thread-safe static init)
     const char* e = getenv("GNB_DYNAMIC_TILES");
@@ -299,7 +301,7 @@ static int predict_device(const void* x, int x_type, int64_t n_rows, int32_t F, 
     PredictMaps map;
     const PredictMaps* mp = nullptr;
     if (use_tma && dynamic_tiles()) {
-      Gate* sg = gate_for(stream);
+      Scratch* sg = scratch_for(stream);
       if (sg == nullptr) return fail(GNB_ENOMEM, "predict: scratch allocation failed");
       p.tile_ctr = sg->dev + 4;
     }
@@ -322,7 +324,7 @@ static int predict_device(const void* x, int x_type, int64_t n_rows, int32_t F, 
           return fail(GNB_ECUDA, "predict: cuTensorMapEncodeTiled failed");
         mmap.tail = mmap.main;
         gmap.tail = gmap.main;
-        Gate* gate = gate_for(stream);
+        Scratch* gate = scratch_for(stream);
         if (gate == nullptr) return fail(GNB_ENOMEM, "predict: gate counter allocation failed");
         std::lock_guard<std::mutex> gate_lock(gate->mu);
         int32_t* cnt = gate->dev;
