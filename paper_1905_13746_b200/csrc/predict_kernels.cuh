@@ -22,6 +22,14 @@
 //   * argmax (ties -> lowest class index = benign) and the out-of-range status
 //     are fused into the epilogue; label (+ optional log-posteriors) written
 //     once, coalesced.
+//   * persistent CTAs claim tiles dynamically (first tile blockIdx.x, then the
+//     next unclaimed index from a per-stream atomic counter; the tile index
+//     travels in the stage header, an end-marker stage stops the consumers),
+//     so SMs that get less DRAM bandwidth simply take fewer tiles.
+//   * kernels: 128-B boxes (predict_tma_kernel, also gather mode for slot-
+//     sorted batches), whole-row boxes for short rows (predict_rowbox_kernel),
+//     every slot's table resident for batches in any row order
+//     (predict_mixed_kernel), and an L1 kernel for any layout.
 //
 // This header holds the kernels and their launch templates; the translation
 // units predict_<storage>_<mode>.cu instantiate launch_typed<T, FMA> (so the
