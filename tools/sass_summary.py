@@ -58,6 +58,8 @@ def main():
                                    "predict_tma_kernel<2, int, 1, 4, 2, true, 1, false>",
                                    "predict_rowbox_kernel<2, int, 2, false, 13, 4, true>",
                                    "predict_rowbox_kernel<2, int, 2, false, 26, 2, false>",
+                                   "predict_mixed_kernel<int, 8, 2, false>",
+                                   "tile_mix_kernel",
                                    "fit_tma_kernel", "gather_kernel<int>", "unpack_u4",
                                    "slot_sort", "fin_select"))}
     doc = {"library": "paper_1905_13746_b200/libgnb.so (sm_100a)",
