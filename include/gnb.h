@@ -76,6 +76,8 @@ enum { GNB_MODE_EXACT = 0, GNB_MODE_FMA = 1 };
  * Results are identical for every hint. */
 enum { GNB_ORDER_AUTO = 0, GNB_ORDER_GROUPED = 0x10, GNB_ORDER_MIXED = 0x20 };
 
+/* 3: row-order hints (GNB_ORDER_*) in gnb_predict_mode's mode, and
+ * gnb_predict_mixed_rows; every version-2 entry point is unchanged. */
 int gnb_abi_version(void);
 const char* gnb_strerror(int code);
 const char* gnb_last_error(void);

@@ -151,7 +151,7 @@ static constexpr int64_t kMaxRowsPerLaunch = int64_t(1) << 30;  // TMA coordinat
 
 extern "C" {
 
-int gnb_abi_version(void) { return 2; }
+int gnb_abi_version(void) { return 3; }
 
 const char* gnb_strerror(int code) {
   switch (code) {

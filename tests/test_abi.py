@@ -17,7 +17,7 @@ def test_every_declared_symbol_is_exported():
 
 
 def test_version_and_strerror():
-    assert N.lib.gnb_abi_version() == 2
+    assert N.lib.gnb_abi_version() == 3
     assert N.lib.gnb_strerror(0) == b"ok"
 
 
