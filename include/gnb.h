@@ -82,6 +82,13 @@ int gnb_abi_version(void);
 const char* gnb_strerror(int code);
 const char* gnb_last_error(void);
 
+/* Streams: the device entry points are stream-ordered.  K-PRED keeps a small
+ * per-(device, stream) scratch (the GNB_ORDER_AUTO gate and the dynamic tile
+ * counter), allocated on first use and reset by the kernels themselves; work
+ * issued on one stream handle must therefore run in that stream's order -- do
+ * not replay a captured CUDA graph on another stream concurrently with K-PRED
+ * work issued on (or captured from) the same stream handle. */
+
 /* ------------------------------------------------------------------ predict
  * Replaces: classifier.log_posterior + classifier.predict
  *           (pkg/src/groupnb/classifier.py:132-158) inside
